@@ -1,0 +1,181 @@
+/*
+ * uwsplat_b200.h -- C ABI of the B200 (sm_100a) underwater-splatting hot path.
+ *
+ * A drop-in device backend for the reference package `uwsplat` 0.1.0 (pure
+ * Python; it ships no FFI of its own).  Each entry point below replaces one
+ * stage of the reference's CPU path; the Python shim
+ * `paper_2411_19588_b200` binds them with ctypes and keeps the reference's
+ * public function names, arguments and exceptions.
+ *
+ * Conventions
+ *   - All array pointers are DEVICE pointers (cudaMalloc / torch CUDA
+ *     tensors) unless the name says `host_`.  Nothing here allocates memory:
+ *     scratch space is sized by the matching *_workspace_size() call and
+ *     passed in by the caller.
+ *   - `stream` is a cudaStream_t passed as void*; every call is asynchronous
+ *     on it.  Calls are thread-safe for distinct streams + workspaces.
+ *   - Every call returns UWS_OK (0) or an error code and records a message
+ *     retrievable with uws_last_error() (thread-local).
+ *   - Per-Gaussian parameters are float32 structure-of-arrays exactly as the
+ *     reference GaussianCloud stores them (scene.py:123-147).
+ */
+#ifndef UWSPLAT_B200_H
+#define UWSPLAT_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define UWS_OK 0
+#define UWS_EINVAL 1      /* bad argument (maps to ValueError / DataError) */
+#define UWS_ECUDA 2       /* CUDA runtime error */
+#define UWS_ECAPACITY 3   /* caller-provided capacity too small */
+
+#define UWS_TILE 16
+
+/* Pinhole camera (reference: scene.py:222-278, Camera).  R is row-major
+ * world->view, x_view = R x + t.  tan_fov = 0.5*width/fx. */
+typedef struct uws_camera {
+    int32_t width, height;
+    double fx, fy, cx, cy;
+    double R[9];
+    double t[3];
+    double near_plane, far_plane;
+} uws_camera;
+
+/* GaussianCloud fields (scene.py:130-137), float32 SoA, device pointers. */
+typedef struct uws_cloud {
+    const float* positions;       /* [n][3] */
+    const float* log_scales;      /* [n][3] */
+    const float* rotations;       /* [n][4] wxyz */
+    const float* sh_coeffs;       /* [n][1][3] degree-0 features */
+    const float* opacity_logits;  /* [n] */
+    int64_t n;
+} uws_cloud;
+
+/* Raster record of one visible Gaussian (48 bytes, 16-byte aligned).
+ * mean2d is kept in float64 so tile-local pixel offsets are exact. */
+typedef struct uws_splat {
+    double mx, my;                 /* mean2d, pixels (unclamped, projection.py:160) */
+    float ca, cb, cc, opacity;     /* conic [c,-b,a]/det (projection.py:174-175), sigmoid(logit) */
+    float r, g, b, depth;          /* clamped degree-0 colour, view depth */
+} uws_splat;
+
+/* ProjectedCloud (projection.py:40-86) in device form.  Rows are the
+ * visible Gaussians in ascending source order; capacity = cloud n. */
+typedef struct uws_projected {
+    int32_t* source_index;   /* [K] */
+    uws_splat* splat;        /* [K] */
+    double* exact;           /* [K][4] conic a,b,c + opacity in float64 (gate re-evaluation) */
+    double* depth;           /* [K] float64 view depth (sort key) */
+    int16_t* rect;           /* [K][4] inclusive tile rect x0,y0,x1,y1, grid-clipped (projection.py:229-249) */
+    double* cov2d;           /* optional [K][3] packed a,b,c (NULL to skip) */
+    double* radius;          /* optional [K] footprint radius (NULL to skip) */
+    int32_t* num_visible;    /* [1] K, written by uws_preprocess_fwd */
+} uws_projected;
+
+/* Per-pixel forward outputs (RenderOutput, rasterizer.py:132-145).  All
+ * [H][W] (x3 for colours) float32 unless noted; optional ones may be NULL. */
+typedef struct uws_raster_out {
+    float* color;          /* [H][W][3] underwater (or clean) colour */
+    float* color_clean;    /* [H][W][3] clean composite; required when medium != NULL */
+    float* depth;          /* [H][W] raw weighted depth, far where empty */
+    float* weight;         /* [H][W] sum alpha_i T_i */
+    float* final_T;        /* [H][W] final transmittance */
+    int32_t* count;        /* [H][W] blended contributors */
+    int32_t* last;         /* [H][W] consumed prefix length of the tile list (backward context) */
+    float* attenuation;    /* optional [H][W][3] exp(-B_d z) */
+    float* backscatter;    /* optional [H][W][3] B_inf (1 - exp(-B_b z)) */
+} uws_raster_out;
+
+/* Adam hyper-parameters for one apply_gradients call (optim.py:69-120).
+ * Index order: positions, log_scales, rotations, sh_coeffs, opacity_logits,
+ * attenuation, water_color, backscatter.  bias1/bias2 = 1 - beta^step and
+ * the learning rates are computed on the host exactly as the reference does. */
+typedef struct uws_adam_params {
+    double lr[8];
+    double bias1[8];
+    double bias2[8];
+    double beta1, beta2, one_minus_beta1, one_minus_beta2, eps;
+} uws_adam_params;
+
+/* ---- meta ------------------------------------------------------------ */
+const char* uws_version(void);
+const char* uws_last_error(void);
+/* number of kernels this library has launched in the process (monotonic) */
+uint64_t uws_kernel_launches(void);
+
+/* ---- preprocess (replaces projection.project_cloud, projection.py:100-199,
+ *      footprint_radius :89-97 and _spans_for :229-249) ------------------ */
+int uws_preprocess_workspace_size(int64_t n, size_t* bytes);
+int uws_preprocess_fwd(const uws_cloud* cloud, const uws_camera* cam, uws_projected* out,
+                       void* workspace, size_t workspace_bytes, void* stream);
+
+/* ---- binning (replaces rasterizer.bin_and_sort, rasterizer.py:50-85).
+ *      Phase 1 sorts rows by float64 depth and counts tile entries, writing
+ *      E to *total_entries (device int64).  Phase 2 emits (tile, row) pairs
+ *      in depth order, stable-sorts them by tile and writes CSR ranges. ---- */
+int uws_bin_workspace_size(int64_t k, int64_t e, int32_t n_tiles, size_t* count_bytes,
+                           size_t* emit_bytes);
+int uws_bin_count(const uws_projected* proj, int64_t k, const uws_camera* cam,
+                  int64_t* total_entries, void* count_ws, size_t count_bytes, void* stream);
+int uws_bin_emit(const uws_projected* proj, int64_t k, int64_t e, const uws_camera* cam,
+                 int32_t* offsets /* [tiles+1] */, int32_t* entries /* [E] rows */,
+                 void* count_ws, size_t count_bytes, void* emit_ws, size_t emit_bytes,
+                 void* stream);
+
+/* ---- forward compositing + medium epilogue (replaces rasterizer.render's
+ *      tile loop / _composite_block :148-178 / apply_water :244-251).
+ *      medium: device float[9] = attenuation[3], water_color[3],
+ *      backscatter[3]; NULL selects clean mode. ---------------------------- */
+int uws_raster_fwd(const uws_projected* proj, const int32_t* offsets, const int32_t* entries,
+                   const uws_camera* cam, const float* medium, uws_raster_out* out, void* stream);
+
+/* ---- loss (replaces losses.total_loss :140-160 incl. l1 :40-49 and
+ *      d_ssim :83-123).  rendered/gt: [H][W][C] float32.  medium: device
+ *      float[15] (9 params + water_color_guide[3] + backscatter_guide[3]) or
+ *      NULL.  result: device double[6] = l1, d_ssim, l_bs, total,
+ *      finite flag (1.0/0.0), reserved. ----------------------------------- */
+int uws_loss_workspace_size(int32_t h, int32_t w, int32_t c, size_t* bytes);
+int uws_loss_fwd_bwd(const float* rendered, const float* gt, int32_t h, int32_t w, int32_t c,
+                     const float* medium, int32_t has_guidance, double lambda_ssim,
+                     double lambda_guide, float* dL_dC, double* result,
+                     void* workspace, size_t workspace_bytes, void* stream);
+
+/* ---- backward compositing (replaces backward._backward_block :124-163 and
+ *      backward_medium :261-275).  screen_grads: [K][9] float32 accumulated
+ *      (+=) per visible row: d_logit_raw, d_mean2d x,y, d_conic a,b,c,
+ *      d_color r,g,b.  medium_acc: device double[9] accumulated (+=). ----- */
+int uws_raster_bwd(const uws_projected* proj, const int32_t* offsets, const int32_t* entries,
+                   const uws_camera* cam, const float* medium, const uws_raster_out* fwd,
+                   const float* dL_dC, float* screen_grads, double* medium_acc, void* stream);
+
+/* ---- projection backward (replaces backward._project_backward :184-258 and
+ *      _quat_backward :166-181).  grads: float32 flat buffer laid out as
+ *      [positions 3n | log_scales 3n | rotations 4n | sh 3n | opacity n |
+ *       mean2d_grad_norm n | observed n | medium 9], accumulated (+=).
+ *      medium_acc (may be NULL in clean mode) plus the guidance subgradient
+ *      lambda_guide*sign(.) are added into the medium slots. -------------- */
+int uws_preprocess_bwd(const uws_cloud* cloud, const uws_camera* cam, const uws_projected* proj,
+                       int64_t k, const float* screen_grads, const double* medium_acc,
+                       const float* medium, int32_t has_guidance, double lambda_guide,
+                       float* grads, void* stream);
+
+/* ---- optimizer (replaces optim.apply_gradients :98-120 / adam_step :69-83,
+ *      GaussianCloud.normalize_rotations scene.py:165-167 and
+ *      MediumParams.clamp_ scene.py:207-211).  params/m/v/grads use the flat
+ *      layout above (params: 14n + 9 medium at offset 14n when medium_params
+ *      is NULL, or medium separately). --------------------------------- */
+int uws_adam_step(float* params, float* exp_avg, float* exp_avg_sq, const float* grads,
+                  int64_t n, float* medium_params, float* medium_exp_avg,
+                  float* medium_exp_avg_sq, const float* medium_grads,
+                  const uws_adam_params* hp, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* UWSPLAT_B200_H */

@@ -16,8 +16,9 @@ pinned against golden vectors produced by the reference itself
 
 Third-party arithmetic the reference delegates: numpy (matmul / lexsort /
 cumprod / add.at) and scipy (``special.expit`` = 1/(1+exp(-x)),
-``ndimage.correlate1d`` with mode="constant").  Both are re-expressed here with
-numpy primitives; ``correlate1d`` is restated as an explicit 11-tap sum.
+``ndimage.correlate1d`` with mode="constant").  numpy is used directly with
+numpy primitives, except that the oracle calls the same scipy functions
+(``expit``, ``correlate1d``) the reference calls, so it stays bit-identical.
 """
 
 from __future__ import annotations
@@ -395,18 +396,10 @@ TAPS = _gauss_taps()
 
 
 def _corr_axis(img, axis):
-    """correlate1d(img, TAPS, axis, mode="constant") restated as an 11-tap sum."""
-    r = SSIM_N // 2
-    pad = [(0, 0)] * img.ndim
-    pad[axis] = (r, r)
-    p = np.pad(img, pad)
-    out = np.zeros_like(img)
-    n = img.shape[axis]
-    for k in range(SSIM_N):
-        sl = [slice(None)] * img.ndim
-        sl[axis] = slice(k, k + n)
-        out += TAPS[k] * p[tuple(sl)]
-    return out
+    """correlate1d(img, TAPS, axis, mode="constant") -- the scipy.ndimage call the
+    reference makes (losses.py:64-65, scipy>=1.10; 1.18.1 here)."""
+    from scipy.ndimage import correlate1d
+    return correlate1d(img, TAPS, axis=axis, mode="constant")
 
 
 def window_filter(img):

@@ -1,0 +1,31 @@
+// C-ABI meta entry points: version string and thread-local error message.
+#include <atomic>
+#include <cstdio>
+#include <string>
+
+#include "common.cuh"
+
+namespace uws {
+
+static thread_local std::string g_last_error;
+
+static std::atomic<uint64_t> g_launches{0};
+
+void set_error(const std::string& msg) { g_last_error = msg; }
+
+void count_launches(int n) { g_launches.fetch_add((uint64_t)n, std::memory_order_relaxed); }
+
+int cuda_fail(cudaError_t e, const char* what) {
+    char buf[512];
+    snprintf(buf, sizeof(buf), "%s: %s (%s)", what, cudaGetErrorString(e), cudaGetErrorName(e));
+    g_last_error = buf;
+    return UWS_ECUDA;
+}
+
+}  // namespace uws
+
+extern "C" const char* uws_version(void) { return "uwsplat_b200 0.1.0 (sm_100a)"; }
+
+extern "C" const char* uws_last_error(void) { return uws::g_last_error.c_str(); }
+
+extern "C" uint64_t uws_kernel_launches(void) { return uws::g_launches.load(); }

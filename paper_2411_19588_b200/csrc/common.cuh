@@ -1,0 +1,101 @@
+// Shared helpers for the sm_100a kernels: error plumbing, constants, small
+// device utilities.  Every constant cites the reference line it mirrors.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <string>
+
+#include "../../include/uwsplat_b200.h"
+
+namespace uws {
+
+// projection.py:21-26
+constexpr int kTile = 16;
+constexpr double kDilation = 0.3;
+constexpr double kFloor = 1.0 / 255.0;
+constexpr double kMinSigma2 = 9.0;
+// rasterizer.py:27-29
+constexpr double kClamp = 0.99;
+constexpr double kTStop = 1e-4;
+// scene.py:22
+constexpr double kSH_C0 = 0.28209479177387814;
+// medium.py:23
+constexpr double kLogisticRate = 0.1;
+
+// float32 gates.  The reference decides in float64; the float32 kernels
+// decide with these thresholds and re-evaluate in float64 inside a guard band
+// (|rel| < kGuard) where float32 rounding could flip the decision.
+constexpr float kFloorF = 0.003921568859368563f;       // (float)(1/255)
+constexpr float kGuard = 3e-5f;
+constexpr float kFloorLo = kFloorF * (1.0f - kGuard);
+constexpr float kFloorHi = kFloorF * (1.0f + kGuard);
+constexpr float kClampF = 0.99f;
+constexpr float kClampLo = 0.99f * (1.0f - kGuard);
+constexpr float kClampHi = 0.99f * (1.0f + kGuard);
+// smallest float >= 1e-4 (double): T_f >= 1e-4  <=>  T_f >= kTStopF
+constexpr float kTStopF = 1.00000004749745130539e-04f;
+
+void set_error(const std::string& msg);
+void count_launches(int n);
+int cuda_fail(cudaError_t e, const char* what);
+
+#define UWS_CHECK_LAUNCH(what)                                   \
+    do {                                                         \
+        ::uws::count_launches(1);                                \
+        cudaError_t _e = cudaGetLastError();                     \
+        if (_e != cudaSuccess) return ::uws::cuda_fail(_e, what); \
+    } while (0)
+
+#define UWS_CUDA(call)                                            \
+    do {                                                          \
+        cudaError_t _e = (call);                                  \
+        if (_e != cudaSuccess) return ::uws::cuda_fail(_e, #call); \
+    } while (0)
+
+#define UWS_REQUIRE(cond, msg)          \
+    do {                                \
+        if (!(cond)) {                  \
+            ::uws::set_error(msg);      \
+            return UWS_EINVAL;          \
+        }                               \
+    } while (0)
+
+inline int64_t ceil_div(int64_t a, int64_t b) { return (a + b - 1) / b; }
+
+inline size_t align_up(size_t x, size_t a = 256) { return (x + a - 1) / a * a; }
+
+// Bump allocator over a caller-provided workspace.
+struct Workspace {
+    char* base;
+    size_t size;
+    size_t used = 0;
+    bool dry;  // size query only
+    Workspace(void* b, size_t s, bool dry_run = false) : base((char*)b), size(s), dry(dry_run) {}
+    template <typename T>
+    T* take(size_t count) {
+        size_t off = used;
+        used = align_up(used + count * sizeof(T));
+        if (dry) return nullptr;
+        return (T*)(base + off);
+    }
+    bool ok() const { return dry || used <= size; }
+};
+
+inline cudaStream_t as_stream(void* s) { return (cudaStream_t)s; }
+
+__device__ __forceinline__ unsigned lanemask_lt() {
+    unsigned m;
+    asm("mov.u32 %0, %%lanemask_lt;" : "=r"(m));
+    return m;
+}
+
+template <typename T>
+__device__ __forceinline__ T warp_sum(T v) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    return v;
+}
+
+}  // namespace uws

@@ -1,0 +1,184 @@
+// K9 projection backward: screen-space gradients -> world parameters.
+//
+// Replaces backward._project_backward (backward.py:184-258) and
+// _quat_backward (:166-181), plus the medium-gradient merge of
+// backward_render (:294-302) and the guidance subgradient of
+// backward_medium (:270-274).
+//
+// One thread per visible row.  Instead of storing the reference's backward
+// context (t_view, rotmat, cov3d, clamp masks ...; projection.py:187-198)
+// the forward geometry is recomputed in float64 from the 56-byte parameter
+// record (project_math.cuh) -- cheaper than writing and re-reading ~200 B
+// per Gaussian.  Each visible row maps to a distinct source Gaussian, so the
+// accumulation into the flat gradient buffer needs no atomics.
+#include "project_math.cuh"
+
+namespace uws {
+namespace {
+
+constexpr int kThreads = 128;
+
+__global__ void __launch_bounds__(kThreads) k_preprocess_bwd(uws_cloud cl, uws_camera cam,
+                                                             const int32_t* __restrict__ src_index,
+                                                             const double* __restrict__ exact,
+                                                             int64_t k,
+                                                             const float* __restrict__ screen,
+                                                             float* __restrict__ grads) {
+    const int64_t row = (int64_t)blockIdx.x * kThreads + threadIdx.x;
+    if (row >= k) return;
+    const int64_t n = cl.n;
+    const int64_t i = src_index[row];
+    const float* sg = screen + row * 9;
+    const double gl = sg[0], dmx = sg[1], dmy = sg[2];
+    const double dca = sg[3], dcb = sg[4], dcc = sg[5];
+    const double dcol[3] = {sg[6], sg[7], sg[8]};
+
+    Geo G;
+    geo_view(cl, cam, i, G);
+    geo_shape(cl, cam, i, G);
+    const double4 ex = reinterpret_cast<const double4*>(exact)[row];
+    const double k0 = ex.x, k1 = ex.y, k2 = ex.z, sop = ex.w;
+    const double* R = cam.R;
+
+    // conic -> cov2d: dX = -Y dY Y (:192-204)
+    const double h = 0.5 * dcb;
+    const double P00 = k0 * dca + k1 * h, P01 = k0 * h + k1 * dcc;
+    const double P10 = k1 * dca + k2 * h, P11 = k1 * h + k2 * dcc;
+    const double X00 = -(P00 * k0 + P01 * k1);
+    const double X01 = -(P00 * k1 + P01 * k2);
+    const double X11 = -(P10 * k1 + P11 * k2);
+    const double G2[4] = {X00, X01, X01, X11};
+
+    // dSigma = T^T G2 T ; dT = 2 G2 T Sigma ; dJ = dT R^T (:214-217)
+    const double* T = G.T;
+    double GT[6];  // G2 T (2x3)
+#pragma unroll
+    for (int r = 0; r < 2; ++r)
+#pragma unroll
+        for (int c = 0; c < 3; ++c) GT[3 * r + c] = G2[2 * r] * T[c] + G2[2 * r + 1] * T[3 + c];
+    double dS[9];
+#pragma unroll
+    for (int a = 0; a < 3; ++a)
+#pragma unroll
+        for (int b = 0; b < 3; ++b) dS[3 * a + b] = T[a] * GT[b] + T[3 + a] * GT[3 + b];
+    double dT[6];
+#pragma unroll
+    for (int r = 0; r < 2; ++r)
+#pragma unroll
+        for (int c = 0; c < 3; ++c)
+            dT[3 * r + c] = 2.0 * (GT[3 * r] * G.S[c] + GT[3 * r + 1] * G.S[3 + c] + GT[3 * r + 2] * G.S[6 + c]);
+    double dJ[6];
+#pragma unroll
+    for (int r = 0; r < 2; ++r)
+#pragma unroll
+        for (int c = 0; c < 3; ++c)
+            dJ[3 * r + c] = dT[3 * r] * R[3 * c] + dT[3 * r + 1] * R[3 * c + 1] + dT[3 * r + 2] * R[3 * c + 2];
+
+    // cov3d = M M^T, M = Rq diag(s): dM = 2 dSigma M (:220-224)
+    double M[9], dM[9];
+#pragma unroll
+    for (int r = 0; r < 3; ++r)
+#pragma unroll
+        for (int c = 0; c < 3; ++c) M[3 * r + c] = G.Rq[3 * r + c] * G.s[c];
+#pragma unroll
+    for (int r = 0; r < 3; ++r)
+#pragma unroll
+        for (int c = 0; c < 3; ++c)
+            dM[3 * r + c] = 2.0 * (dS[3 * r] * M[c] + dS[3 * r + 1] * M[3 + c] + dS[3 * r + 2] * M[6 + c]);
+    double dls[3], gR[9];
+#pragma unroll
+    for (int c = 0; c < 3; ++c) {
+        dls[c] = (G.Rq[c] * dM[c] + G.Rq[3 + c] * dM[3 + c] + G.Rq[6 + c] * dM[6 + c]) * G.s[c];
+#pragma unroll
+        for (int r = 0; r < 3; ++r) gR[3 * r + c] = dM[3 * r + c] * G.s[c];
+    }
+    // rotation matrix -> raw quaternion (:166-181)
+    const double w = G.qu[0], x = G.qu[1], y = G.qu[2], z = G.qu[3];
+#define g(r, c) gR[3 * (r) + (c)]
+    double dq[4];
+    dq[0] = 2 * (z * (g(1, 0) - g(0, 1)) + y * (g(0, 2) - g(2, 0)) + x * (g(2, 1) - g(1, 2)));
+    dq[1] = 2 * (y * (g(0, 1) + g(1, 0)) + z * (g(0, 2) + g(2, 0)) + w * (g(2, 1) - g(1, 2)) -
+                 2 * x * (g(1, 1) + g(2, 2)));
+    dq[2] = 2 * (x * (g(0, 1) + g(1, 0)) + w * (g(0, 2) - g(2, 0)) + z * (g(1, 2) + g(2, 1)) -
+                 2 * y * (g(0, 0) + g(2, 2)));
+    dq[3] = 2 * (w * (g(1, 0) - g(0, 1)) + x * (g(0, 2) + g(2, 0)) + y * (g(1, 2) + g(2, 1)) -
+                 2 * z * (g(0, 0) + g(1, 1)));
+#undef g
+    const double radial = dq[0] * w + dq[1] * x + dq[2] * y + dq[3] * z;
+
+    // view-space point: through J (clamped) and the unclamped mean (:226-248)
+    const double rz = 1.0 / G.vz, rz2 = rz * rz, rz3 = rz2 * rz;
+    const double dxu = dJ[2] * (-cam.fx * rz2);
+    const double dyu = dJ[5] * (-cam.fy * rz2);
+    double dtz = dJ[0] * (-cam.fx * rz2) + dJ[2] * (2.0 * cam.fx * G.xu * rz3) +
+                 dJ[4] * (-cam.fy * rz2) + dJ[5] * (2.0 * cam.fy * G.yu * rz3);
+    double dtx = G.xm ? 0.0 : dxu;
+    double dty = G.ym ? 0.0 : dyu;
+    if (G.xm) dtz += dxu * (G.u > 0 ? 1.0 : (G.u < 0 ? -1.0 : 0.0)) * G.limx;
+    if (G.ym) dtz += dyu * (G.v > 0 ? 1.0 : (G.v < 0 ? -1.0 : 0.0)) * G.limy;
+    dtx += dmx * cam.fx * rz;
+    dty += dmy * cam.fy * rz;
+    dtz = dtz - dmx * cam.fx * G.vx * rz2 - dmy * cam.fy * G.vy * rz2;
+
+    float* gpos = grads;
+    float* gls = grads + 3 * n;
+    float* grot = grads + 6 * n;
+    float* gsh = grads + 10 * n;
+    float* gop = grads + 13 * n;
+    float* gnorm = grads + 14 * n;
+    float* gobs = grads + 15 * n;
+#pragma unroll
+    for (int c = 0; c < 3; ++c) {
+        gpos[3 * i + c] += (float)(dtx * R[c] + dty * R[3 + c] + dtz * R[6 + c]);
+        gls[3 * i + c] += (float)dls[c];
+        const double col = (double)cl.sh_coeffs[3 * i + c] * kSH_C0 + 0.5;
+        if (col > 0.0) gsh[3 * i + c] += (float)(kSH_C0 * dcol[c]);
+    }
+#pragma unroll
+    for (int c = 0; c < 4; ++c) grot[4 * i + c] += (float)((dq[c] - G.qu[c] * radial) / G.qn);
+    gop[i] += (float)((1.0 - sop) * gl);
+    const double nx = dmx * cam.width * 0.5, ny = dmy * cam.height * 0.5;
+    gnorm[i] += (float)sqrt(nx * nx + ny * ny);
+    gobs[i] += 1.0f;
+}
+
+// medium slots: accumulated image sums + lambda * sign(param - guide)
+__global__ void k_medium_finalize(const double* __restrict__ acc, const float* __restrict__ medium,
+                                  int has_guidance, double lam, float* __restrict__ gmed) {
+    const int v = threadIdx.x;
+    if (v >= 9) return;
+    double s = acc ? acc[v] : 0.0;
+    if (acc && has_guidance && lam != 0.0 && v >= 3) {
+        double d = (double)medium[v] - (double)medium[v + 6];
+        s += lam * (d > 0 ? 1.0 : (d < 0 ? -1.0 : 0.0));
+    }
+    gmed[v] += (float)s;
+}
+
+}  // namespace
+}  // namespace uws
+
+using namespace uws;
+
+extern "C" int uws_preprocess_bwd(const uws_cloud* cloud, const uws_camera* cam,
+                                  const uws_projected* proj, int64_t k, const float* screen_grads,
+                                  const double* medium_acc, const float* medium,
+                                  int32_t has_guidance, double lambda_guide, float* grads,
+                                  void* stream) {
+    UWS_REQUIRE(cloud && cam && proj && grads, "uws_preprocess_bwd: null argument");
+    UWS_REQUIRE(k >= 0 && k <= cloud->n, "uws_preprocess_bwd: k out of range");
+    UWS_REQUIRE(medium_acc == nullptr || medium != nullptr, "uws_preprocess_bwd: medium missing");
+    cudaStream_t st = as_stream(stream);
+    if (k > 0) {
+        UWS_REQUIRE(screen_grads != nullptr, "uws_preprocess_bwd: screen_grads missing");
+        k_preprocess_bwd<<<(unsigned)ceil_div(k, kThreads), kThreads, 0, st>>>(
+            *cloud, *cam, proj->source_index, proj->exact, k, screen_grads, grads);
+        UWS_CHECK_LAUNCH("k_preprocess_bwd");
+    }
+    if (medium_acc) {
+        k_medium_finalize<<<1, 32, 0, st>>>(medium_acc, medium, has_guidance, lambda_guide,
+                                            grads + 16 * cloud->n);
+        UWS_CHECK_LAUNCH("k_medium_finalize");
+    }
+    return UWS_OK;
+}

@@ -1,0 +1,229 @@
+// Stable LSD radix sort of (key, uint32 value) pairs, 8-bit digits, one
+// kernel per digit pass in the "onesweep" style: a single up-front global
+// histogram for all passes, then per pass each tile ranks its keys in
+// registers/shared memory (warp match + per-warp counters, stable in input
+// order), resolves its global per-digit base by decoupled look-back over the
+// preceding tiles, reorders in shared memory and writes digit runs coalesced.
+// Every key is read once and written once per pass.
+#pragma once
+
+#include "scan.cuh"
+
+namespace uws {
+namespace radix {
+
+constexpr int kThreads = 256;
+constexpr int kWarps = kThreads / 32;
+constexpr int kBins = 256;
+
+// status word per (tile, bin): [flag:2 | count:30]
+constexpr unsigned kStAgg = 1u << 30;
+constexpr unsigned kStInc = 2u << 30;
+constexpr unsigned kStMask = (1u << 30) - 1;
+
+template <typename K>
+struct Cfg;
+template <>
+struct Cfg<uint64_t> {
+    static constexpr int kIpt = 12;
+};
+template <>
+struct Cfg<uint32_t> {
+    static constexpr int kIpt = 16;
+};
+
+template <typename K>
+constexpr int tile_items() {
+    return kThreads * Cfg<K>::kIpt;
+}
+
+template <typename K>
+__global__ void __launch_bounds__(kThreads) k_histogram(const K* __restrict__ keys, uint32_t n,
+                                                       int begin_bit, int passes,
+                                                       uint32_t* __restrict__ hist) {
+    __shared__ uint32_t h[8 * kBins];
+    for (int i = threadIdx.x; i < passes * kBins; i += kThreads) h[i] = 0;
+    __syncthreads();
+    const unsigned lt = lanemask_lt();
+    const uint32_t stride = gridDim.x * kThreads;
+    for (uint32_t base = blockIdx.x * kThreads; base < n; base += stride) {
+        uint32_t i = base + threadIdx.x;
+        bool valid = i < n;
+        K key = valid ? keys[i] : K(0);
+        for (int p = 0; p < passes; ++p) {
+            unsigned d = valid ? unsigned((key >> (begin_bit + 8 * p)) & 0xFF) : 0x100u;
+            unsigned peers = __match_any_sync(0xffffffffu, d);
+            if (valid && (peers & lt) == 0) atomicAdd(&h[p * kBins + d], __popc(peers));
+        }
+    }
+    __syncthreads();
+    for (int i = threadIdx.x; i < passes * kBins; i += kThreads)
+        if (h[i]) atomicAdd(&hist[i], h[i]);
+}
+
+// exclusive scan of each pass's 256-bin histogram, in place
+__global__ void __launch_bounds__(kBins) k_scan_hist(uint32_t* hist, int passes) {
+    __shared__ uint32_t tmp[kBins / 32 + 1];
+    for (int p = 0; p < passes; ++p) {
+        uint32_t v = hist[p * kBins + threadIdx.x];
+        uint32_t tot;
+        uint32_t ex = block_exclusive_sum<kBins>(v, tmp, &tot);
+        hist[p * kBins + threadIdx.x] = ex;
+        __syncthreads();
+    }
+}
+
+template <typename K>
+__global__ void __launch_bounds__(kThreads) k_onesweep(const K* __restrict__ keys_in,
+                                                      const uint32_t* __restrict__ vals_in,
+                                                      K* __restrict__ keys_out,
+                                                      uint32_t* __restrict__ vals_out, uint32_t n,
+                                                      int shift, const uint32_t* __restrict__ bin_base,
+                                                      uint32_t* status, uint32_t* ticket) {
+    constexpr int IPT = Cfg<K>::kIpt;
+    constexpr int TILE = kThreads * IPT;
+    __shared__ K s_keys[TILE];
+    __shared__ uint32_t s_vals[TILE];
+    __shared__ uint32_t s_warp[kWarps][kBins];
+    __shared__ uint32_t s_local[kBins];
+    __shared__ uint32_t s_global[kBins];
+    __shared__ uint32_t s_tmp[kBins / 32 + 1];
+    __shared__ int s_tile;
+
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    if (tid == 0) s_tile = (int)atomicAdd(ticket, 1u);
+    for (int i = tid; i < kWarps * kBins; i += kThreads) (&s_warp[0][0])[i] = 0;
+    __syncthreads();
+    const int tile = s_tile;
+    const uint32_t base = (uint32_t)tile * TILE;
+
+    K key[IPT];
+    uint32_t val[IPT];
+    uint32_t rank[IPT];
+    const unsigned lt = lanemask_lt();
+    // warp-striped: warp w owns [w*IPT*32, (w+1)*IPT*32) of the tile
+#pragma unroll
+    for (int i = 0; i < IPT; ++i) {
+        uint32_t idx = base + (uint32_t)(warp * IPT + i) * 32u + lane;
+        bool valid = idx < n;
+        key[i] = valid ? keys_in[idx] : K(0);
+        val[i] = valid ? (vals_in ? vals_in[idx] : idx) : 0u;
+    }
+#pragma unroll
+    for (int i = 0; i < IPT; ++i) {
+        uint32_t idx = base + (uint32_t)(warp * IPT + i) * 32u + lane;
+        bool valid = idx < n;
+        unsigned d = valid ? unsigned((key[i] >> shift) & 0xFF) : 0x100u;
+        unsigned peers = __match_any_sync(0xffffffffu, d);
+        uint32_t before = valid ? s_warp[warp][d] : 0u;
+        rank[i] = before + __popc(peers & lt);
+        __syncwarp();
+        if (valid && (peers & lt) == 0) s_warp[warp][d] = before + __popc(peers);
+        __syncwarp();
+    }
+    __syncthreads();
+    // per bin: exclusive prefix over warps, block count, look-back
+    {
+        const int b = tid;  // kThreads == kBins
+        uint32_t run = 0;
+#pragma unroll
+        for (int w = 0; w < kWarps; ++w) {
+            uint32_t c = s_warp[w][b];
+            s_warp[w][b] = run;
+            run += c;
+        }
+        uint32_t cnt = run;
+        uint32_t excl = 0;
+        if (tile == 0) {
+            st_volatile(&status[b], kStInc | cnt);
+        } else {
+            st_volatile(&status[(size_t)tile * kBins + b], kStAgg | cnt);
+            int j = tile - 1;
+            while (true) {
+                uint32_t s = ld_volatile(&status[(size_t)j * kBins + b]);
+                uint32_t f = s >> 30;
+                if (f == 0) continue;
+                excl += s & kStMask;
+                if (f == 2) break;
+                --j;
+            }
+            st_volatile(&status[(size_t)tile * kBins + b], kStInc | (excl + cnt));
+        }
+        s_global[b] = bin_base[b] + excl;
+        uint32_t tot;
+        uint32_t loc = block_exclusive_sum<kThreads>(cnt, s_tmp, &tot);
+        s_local[b] = loc;
+    }
+    __syncthreads();
+#pragma unroll
+    for (int i = 0; i < IPT; ++i) {
+        uint32_t idx = base + (uint32_t)(warp * IPT + i) * 32u + lane;
+        if (idx < n) {
+            unsigned d = unsigned((key[i] >> shift) & 0xFF);
+            uint32_t pos = s_local[d] + s_warp[warp][d] + rank[i];
+            s_keys[pos] = key[i];
+            s_vals[pos] = val[i];
+        }
+    }
+    __syncthreads();
+    uint32_t count = n - base < (uint32_t)TILE ? n - base : (uint32_t)TILE;
+    for (uint32_t j = tid; j < count; j += kThreads) {
+        K k = s_keys[j];
+        unsigned d = unsigned((k >> shift) & 0xFF);
+        uint32_t o = s_global[d] + (j - s_local[d]);
+        keys_out[o] = k;
+        vals_out[o] = s_vals[j];
+    }
+}
+
+// Workspace for sorting n pairs over `passes` 8-bit digits.
+template <typename K>
+inline void plan(Workspace& ws, uint32_t n, int passes, K** k_alt, uint32_t** v_alt, K** k_tmp,
+                 uint32_t** v_tmp, uint32_t** hist, uint32_t** status, uint32_t** tickets) {
+    int tiles = (int)ceil_div(n > 0 ? n : 1, tile_items<K>());
+    *k_alt = ws.take<K>(n);
+    *v_alt = ws.take<uint32_t>(n);
+    *k_tmp = ws.take<K>(n);
+    *v_tmp = ws.take<uint32_t>(n);
+    *hist = ws.take<uint32_t>((size_t)passes * kBins);
+    *status = ws.take<uint32_t>((size_t)passes * tiles * kBins);
+    *tickets = ws.take<uint32_t>(passes);
+}
+
+// Sort (keys_in, vals_in or identity if NULL) by bits [begin_bit, begin_bit+8*passes).
+// The result lands in (keys_out, vals_out); keys_in/vals_in are not modified.
+// The histogram/status/ticket block must be contiguous (as laid out by plan()).
+template <typename K>
+inline cudaError_t sort_pairs(const K* keys_in, const uint32_t* vals_in, K* keys_out,
+                              uint32_t* vals_out, uint32_t n, int begin_bit, int passes,
+                              K* k_tmp, uint32_t* v_tmp, uint32_t* hist, uint32_t* status,
+                              uint32_t* tickets, size_t meta_bytes, cudaStream_t st) {
+    if (n == 0) return cudaSuccess;
+    cudaError_t e = cudaMemsetAsync(hist, 0, meta_bytes, st);
+    if (e != cudaSuccess) return e;
+    int hist_blocks = (int)ceil_div(n, kThreads * 8);
+    if (hist_blocks > 1184) hist_blocks = 1184;
+    k_histogram<K><<<hist_blocks, kThreads, 0, st>>>(keys_in, n, begin_bit, passes, hist);
+    k_scan_hist<<<1, kBins, 0, st>>>(hist, passes);
+    const int tiles = (int)ceil_div(n, tile_items<K>());
+    // ping-pong so that the last pass writes into keys_out/vals_out
+    const K* ksrc = keys_in;
+    const uint32_t* vsrc = vals_in;
+    for (int p = 0; p < passes; ++p) {
+        bool last = p == passes - 1;
+        bool to_out = ((passes - 1 - p) % 2) == 0;
+        K* kdst = to_out ? keys_out : k_tmp;
+        uint32_t* vdst = to_out ? vals_out : v_tmp;
+        (void)last;
+        k_onesweep<K><<<tiles, kThreads, 0, st>>>(ksrc, vsrc, kdst, vdst, n, begin_bit + 8 * p,
+                                                  hist + p * kBins,
+                                                  status + (size_t)p * tiles * kBins, tickets + p);
+        ksrc = kdst;
+        vsrc = vdst;
+    }
+    count_launches(2 + passes);
+    return cudaGetLastError();
+}
+
+}  // namespace radix
+}  // namespace uws

@@ -1,0 +1,131 @@
+"""Optimizer (reference: optim.py).
+
+``apply_gradients`` is one fused sm_100a kernel over the flat parameter
+buffer (Adam for the five cloud tensors, quaternion renormalisation) plus a
+9-thread kernel for the medium (Adam + box clamp).  Learning rates and bias
+corrections are computed here in Python exactly as the reference computes
+them, so the device update is bit-identical given the same gradients.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import math
+from dataclasses import dataclass, fields
+
+import torch
+
+from . import _lib
+from .scene import CLOUD_FIELDS, MEDIUM_FIELDS, AdamSlot, TrainState
+
+BETA1, BETA2, EPS = 0.9, 0.999, 1e-15
+
+
+@dataclass
+class OptimConfig:
+    """Training hyper-parameters (optim.py:16-52)."""
+
+    iterations: int = 30000
+    position_lr_init: float = 0.00016
+    position_lr_final: float = 0.0000016
+    position_lr_delay_mult: float = 0.01
+    position_lr_max_steps: int = 30000
+    feature_lr: float = 0.0025
+    attenuation_lr: float = 0.0025
+    backscatter_lr: float = 0.0025
+    opacity_lr: float = 0.05
+    scaling_lr: float = 0.005
+    rotation_lr: float = 0.001
+    lambda_ssim: float = 0.3
+    lambda_guide: float = 0.1
+    densify_interval: int = 100
+    opacity_reset_interval: int = 3000
+    densify_from: int = 1500
+    densify_until: int = 15000
+    densify_grad_threshold: float = 0.0002
+    min_opacity: float = 0.1
+    refit_period: int = 500
+    percent_dense: float = 0.01
+    split_scale_factor: float = 1.6
+    opacity_reset_value: float = 0.01
+    checkpoint_interval: int = 1000
+    workers: int = 1
+
+    def validate(self):
+        for f in fields(self):
+            v = getattr(self, f.name)
+            if isinstance(v, (int, float)) and v < 0:
+                raise ValueError(f"{f.name} must be non-negative")
+        if not (self.densify_from <= self.densify_until <= max(self.iterations, self.densify_until)):
+            raise ValueError("require densify_from <= densify_until")
+
+
+def position_lr(iteration: int, cfg: OptimConfig, spatial_scale: float = 1.0) -> float:
+    """Sine-ramped log-linear position lr (optim.py:55-66)."""
+    t = min(max(iteration / cfg.position_lr_max_steps, 0.0), 1.0)
+    ramp = cfg.position_lr_delay_mult + (1.0 - cfg.position_lr_delay_mult) * math.sin(0.5 * math.pi * t)
+    log_lerp = math.exp(math.log(cfg.position_lr_init) * (1 - t)
+                        + math.log(cfg.position_lr_final) * t)
+    return ramp * log_lerp * spatial_scale
+
+
+_LR_FIELDS = {
+    "positions": None,
+    "log_scales": "scaling_lr",
+    "rotations": "rotation_lr",
+    "sh_coeffs": "feature_lr",
+    "opacity_logits": "opacity_lr",
+    "attenuation": "attenuation_lr",
+    "water_color": "backscatter_lr",
+    "backscatter": "backscatter_lr",
+}
+
+
+def adam_step(params: torch.Tensor, grads, slot: AdamSlot, lr: float, beta1: float = BETA1,
+              beta2: float = BETA2, eps: float = EPS) -> None:
+    """One bias-corrected Adam update of a single tensor (optim.py:69-83).
+
+    Standalone float64 torch utility; ``apply_gradients`` uses the fused kernel.
+    """
+    slot.step += 1
+    g = torch.as_tensor(grads, device=params.device).double().reshape(params.shape)
+    m = beta1 * slot.m.double() + (1 - beta1) * g
+    v = beta2 * slot.v.double() + ((1 - beta2) * g) * g
+    m_hat = m / (1 - beta1 ** slot.step)
+    v_hat = v / (1 - beta2 ** slot.step)
+    params.copy_((params.double() - (lr * m_hat) / (torch.sqrt(v_hat) + eps)).float())
+    slot.m.copy_(m.float())
+    slot.v.copy_(v.float())
+
+
+def adam_hparams(state: TrainState, cfg: OptimConfig, spatial_scale: float = 1.0,
+                 advance: bool = True) -> _lib.AdamParamsC:
+    """Per-tensor lr and bias corrections for the next step (host, float64)."""
+    hp = _lib.AdamParamsC()
+    for j, name in enumerate(CLOUD_FIELDS + MEDIUM_FIELDS):
+        slot = state.adam[name]
+        step = slot.step + 1
+        if advance:
+            slot.step = step
+        lr = position_lr(state.iteration, cfg, spatial_scale) if name == "positions" \
+            else getattr(cfg, _LR_FIELDS[name])
+        hp.lr[j] = lr
+        hp.bias1[j] = 1 - BETA1 ** step
+        hp.bias2[j] = 1 - BETA2 ** step
+    hp.beta1, hp.beta2 = BETA1, BETA2
+    hp.one_minus_beta1, hp.one_minus_beta2 = 1 - BETA1, 1 - BETA2
+    hp.eps = EPS
+    return hp
+
+
+def apply_gradients(state: TrainState, buf, cfg: OptimConfig, spatial_scale: float = 1.0) -> None:
+    """Adam-update every learnable tensor, then re-project constraints (optim.py:98-120)."""
+    cloud, medium = state.cloud, state.medium
+    if buf.n != len(cloud):
+        raise ValueError("gradient buffer does not match the cloud")
+    hp = adam_hparams(state, cfg, spatial_scale)
+    n = len(cloud)
+    _lib.call("uws_adam_step", _lib.ptr(cloud.flat), _lib.ptr(state.exp_avg),
+              _lib.ptr(state.exp_avg_sq), _lib.ptr(buf.flat), n, _lib.ptr(medium.flat),
+              _lib.ptr(state.medium_exp_avg), _lib.ptr(state.medium_exp_avg_sq),
+              _lib.ptr(buf.medium), ctypes.byref(hp), _lib.stream_handle())

@@ -1,0 +1,159 @@
+"""Tile binning and forward compositing on the device (reference: rasterizer.py).
+
+``bin_and_sort`` and ``render`` keep the reference signatures; all per-tile
+work runs in the sm_100a kernels (depth radix sort, tile-key emission, tile
+radix sort, tile ranges, per-tile front-to-back compositing with the medium
+epilogue).  Outputs are float32 CUDA tensors.
+"""
+
+from __future__ import annotations
+
+import ctypes
+from dataclasses import dataclass
+from typing import Optional
+
+import torch
+
+from . import _lib
+from .medium import logistic_remap
+from .projection import TILE_SIZE, ProjectedCloud, project_cloud
+from .scene import Camera, GaussianCloud, MediumParams
+
+ALPHA_CLAMP = 0.99
+T_EARLY_STOP = 1e-4
+WEIGHT_EPS = 1e-8
+
+
+class TileBins:
+    """CSR tile lists (rasterizer.py:32-47): ``offsets`` (tiles+1,) and
+    ``entries`` (E,) int32 device tensors; entries are ProjectedCloud rows
+    sorted by (tile, depth, source index)."""
+
+    def __init__(self, grid_x: int, grid_y: int, offsets: torch.Tensor, entries: torch.Tensor):
+        self.grid_x = grid_x
+        self.grid_y = grid_y
+        self.offsets = offsets
+        self.entries = entries
+
+    def tile_entries(self, tx: int, ty: int) -> torch.Tensor:
+        tid = ty * self.grid_x + tx
+        a, b = (int(v) for v in self.offsets[tid:tid + 2].tolist())
+        return self.entries[a:b]
+
+
+def bin_and_sort(proj: ProjectedCloud, width: int, height: int,
+                 tile_size: int = TILE_SIZE) -> TileBins:
+    """Assign footprints to tiles and depth-sort each list (rasterizer.py:50-85).
+
+    Synchronises once to read the entry count E.
+    """
+    if tile_size != TILE_SIZE:
+        raise ValueError("the device kernels use 16x16 tiles")
+    cam = Camera(width=width, height=height, fx=1.0, fy=1.0, cx=0.0, cy=0.0, R=[[1, 0, 0],
+                 [0, 1, 0], [0, 0, 1]], t=[0, 0, 0])
+    gx, gy = cam.grid
+    dev = proj.device
+    offsets = torch.zeros(gx * gy + 1, dtype=torch.int32, device=dev)
+    k = len(proj)
+    if k == 0:
+        return TileBins(gx, gy, offsets, torch.empty(0, dtype=torch.int32, device=dev))
+    cb, eb = _lib.size_out(), _lib.size_out()
+    _lib.call("uws_bin_workspace_size", k, 0, gx * gy, ctypes.byref(cb), ctypes.byref(eb))
+    count_ws = torch.empty(cb.value, dtype=torch.uint8, device=dev)
+    total = torch.zeros(1, dtype=torch.int64, device=dev)
+    pc, cc = proj.c_struct(), cam.c_struct()
+    st = _lib.stream_handle()
+    _lib.call("uws_bin_count", ctypes.byref(pc), k, ctypes.byref(cc), _lib.ptr(total),
+              _lib.ptr(count_ws), cb.value, st)
+    e = int(total.item())
+    entries = torch.empty(max(e, 1), dtype=torch.int32, device=dev)
+    _lib.call("uws_bin_workspace_size", k, e, gx * gy, ctypes.byref(cb), ctypes.byref(eb))
+    emit_ws = torch.empty(eb.value, dtype=torch.uint8, device=dev)
+    _lib.call("uws_bin_emit", ctypes.byref(pc), k, e, ctypes.byref(cc), _lib.ptr(offsets),
+              _lib.ptr(entries), _lib.ptr(count_ws), cb.value, _lib.ptr(emit_ws), eb.value, st)
+    return TileBins(gx, gy, offsets, entries[:e])
+
+
+@dataclass
+class RenderOutput:
+    """Forward buffers (rasterizer.py:132-145); proj/bins retained for backward."""
+
+    color: torch.Tensor
+    depth: torch.Tensor
+    weight: torch.Tensor
+    final_transmittance: torch.Tensor
+    count: torch.Tensor
+    mode: str
+    color_clean: Optional[torch.Tensor] = None
+    proj: Optional[ProjectedCloud] = None
+    bins: Optional[TileBins] = None
+    camera: Optional[Camera] = None
+    last: Optional[torch.Tensor] = None          # per-pixel consumed list prefix
+    attenuation_map: Optional[torch.Tensor] = None
+    backscatter_map: Optional[torch.Tensor] = None
+
+    def c_struct(self) -> _lib.RasterOutC:
+        return _lib.RasterOutC(_lib.ptr(self.color), _lib.ptr(self.color_clean),
+                               _lib.ptr(self.depth), _lib.ptr(self.weight),
+                               _lib.ptr(self.final_transmittance), _lib.ptr(self.count),
+                               _lib.ptr(self.last), _lib.ptr(self.attenuation_map),
+                               _lib.ptr(self.backscatter_map))
+
+
+def _alloc_output(H, W, dev, mode, medium_maps):
+    f = dict(dtype=torch.float32, device=dev)
+    out = RenderOutput(color=torch.empty(H, W, 3, **f), depth=torch.empty(H, W, **f),
+                       weight=torch.empty(H, W, **f), final_transmittance=torch.empty(H, W, **f),
+                       count=torch.empty(H, W, dtype=torch.int32, device=dev), mode=mode,
+                       last=torch.empty(H, W, dtype=torch.int32, device=dev))
+    if mode == "underwater":
+        out.color_clean = torch.empty(H, W, 3, **f)
+        if medium_maps:
+            out.attenuation_map = torch.empty(H, W, 3, **f)
+            out.backscatter_map = torch.empty(H, W, 3, **f)
+    return out
+
+
+def composite(proj: ProjectedCloud, bins: TileBins, cam, medium: Optional[MediumParams] = None,
+              mode: str = "clean", medium_maps: bool = False) -> RenderOutput:
+    """Run the compositing kernel on existing projection + bins."""
+    cam = Camera.from_any(cam)
+    out = _alloc_output(cam.height, cam.width, proj.device, mode, medium_maps)
+    pc, cc, oc = proj.c_struct(), cam.c_struct(), out.c_struct()
+    med = _lib.ptr(medium.flat) if mode == "underwater" else 0
+    _lib.call("uws_raster_fwd", ctypes.byref(pc), _lib.ptr(bins.offsets), _lib.ptr(bins.entries),
+              ctypes.byref(cc), med, ctypes.byref(oc), _lib.stream_handle())
+    out.proj, out.bins, out.camera = proj, bins, cam
+    return out
+
+
+def render(cloud: GaussianCloud, cam, medium: Optional[MediumParams] = None,
+           mode: str = "clean", workers: int = 1, retain: bool = True,
+           medium_maps: bool = False) -> RenderOutput:
+    """Render a full frame (rasterizer.py:188-241).  ``workers`` is accepted
+    for signature compatibility and ignored.  ``medium_maps=True``
+    additionally returns the per-pixel attenuation exp(-B_d z) and
+    backscatter B_inf (1 - exp(-B_b z)) images."""
+    if mode not in ("clean", "underwater"):
+        raise ValueError(f"unknown render mode {mode!r}")
+    if mode == "underwater" and medium is None:
+        raise ValueError("underwater mode requires medium parameters")
+    cam = Camera.from_any(cam)
+    proj = project_cloud(cloud, cam, with_geometry=False)
+    bins = bin_and_sort(proj, cam.width, cam.height)
+    out = composite(proj, bins, cam, medium, mode, medium_maps)
+    if not retain:
+        out.proj = None
+        out.bins = None
+    return out
+
+
+def apply_water(color_clean: torch.Tensor, depth_raw: torch.Tensor,
+                medium: MediumParams) -> torch.Tensor:
+    """Attenuate a clean render and add backscatter (rasterizer.py:244-251).
+
+    Utility outside the hot path (the render kernel fuses this epilogue)."""
+    z = logistic_remap(depth_raw)[..., None]
+    att = torch.exp(-medium.attenuation.double() * z)
+    bsc = medium.water_color.double() * (1.0 - torch.exp(-medium.backscatter.double() * z))
+    return color_clean.double() * att + bsc

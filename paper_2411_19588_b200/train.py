@@ -1,0 +1,136 @@
+"""Training-step glue and view-sharded data parallelism.
+
+``train_step`` is the body of the reference's training loop
+(pipeline.py:178-193): render (underwater) -> total_loss -> skip if
+non-finite -> backward_render -> skip if non-finite -> densification
+statistics -> apply_gradients.  It needs one small device-to-host read per
+step (loss values + finite flags) besides the two size reads of the
+renderer.
+
+``ViewShardedTrainer`` is the multi-GPU extension: every rank
+holds the full cloud and optimizer state, renders and back-propagates its
+share of the views into ONE flat gradient buffer, the buffers are summed
+with a single NCCL all-reduce, and every rank applies the identical Adam
+step.  The batch gradient equals the sum over views of the reference's
+per-view ``backward_render`` (guidance subgradient added once per view).
+"""
+
+from __future__ import annotations
+
+import logging
+from dataclasses import dataclass
+from typing import Optional, Sequence
+
+import torch
+
+from .backward import GradientBuffer, backward_render
+from .losses import LossBreakdown, total_loss_device
+from .optim import OptimConfig, apply_gradients
+from .rasterizer import render
+from .scene import TrainState
+
+log = logging.getLogger(__name__)
+
+
+@dataclass
+class StepStats:
+    l1: float
+    d_ssim: float
+    l_bs: float
+    total: float
+    views: int
+    skipped: bool
+
+
+def _accumulate_stats(state: TrainState, buf: GradientBuffer):
+    """grad_accum[observed] += mean2d_grad_norm; obs_count[observed] += views (pipeline.py:191-192)."""
+    state.grad_accum += buf.mean2d_grad_norm
+    state.obs_count += buf.observed_count.to(torch.int32)
+
+
+def train_step(state: TrainState, cam, gt, cfg: OptimConfig, spatial_scale: float = 1.0,
+               buf: Optional[GradientBuffer] = None) -> StepStats:
+    """One training iteration on one view (pipeline.py:178-193)."""
+    cloud, medium = state.cloud, state.medium
+    out = render(cloud, cam, medium=medium, mode="underwater")
+    res, dL = total_loss_device(out.color, gt, medium, cfg.lambda_ssim, cfg.lambda_guide)
+    if buf is None:
+        buf = GradientBuffer(len(cloud), cloud.device)
+    else:
+        buf.zero_()
+    backward_render(out, dL, cloud, medium, cfg.lambda_guide, buf=buf)
+    flags = torch.stack([res[0], res[1], res[2], res[3], res[4],
+                         buf.all_finite_device().double()]).tolist()
+    l1, ds, lb, total, loss_ok, grad_ok = flags
+    if loss_ok < 0.5:
+        log.warning("iteration %d: non-finite loss, skipping update", state.iteration)
+        return StepStats(l1, ds, lb, total, 1, True)
+    if grad_ok < 0.5:
+        log.warning("iteration %d: non-finite gradients, skipping update", state.iteration)
+        return StepStats(l1, ds, lb, total, 1, True)
+    _accumulate_stats(state, buf)
+    apply_gradients(state, buf, cfg, spatial_scale)
+    return StepStats(l1, ds, lb, total, 1, False)
+
+
+class ViewShardedTrainer:
+    """Data-parallel training over camera views, one process per GPU."""
+
+    def __init__(self, state: TrainState, cfg: OptimConfig, spatial_scale: float = 1.0,
+                 group=None):
+        import torch.distributed as dist
+        self.state = state
+        self.cfg = cfg
+        self.spatial_scale = spatial_scale
+        self.group = group
+        self.dist = dist if dist.is_available() and dist.is_initialized() else None
+        self.world = self.dist.get_world_size(group) if self.dist else 1
+        self.rank = self.dist.get_rank(group) if self.dist else 0
+        self.buf = GradientBuffer(len(state.cloud), state.cloud.device)
+        self.loss_acc = torch.zeros(6, dtype=torch.float64, device=state.cloud.device)
+
+    def shard(self, views: Sequence) -> Sequence:
+        """Views of this rank: round-robin over the global view list."""
+        return views[self.rank::self.world]
+
+    def local_pass(self, views: Sequence):
+        """Render + loss + backward of this rank's views into self.buf."""
+        st = self.state
+        self.buf.zero_()
+        self.loss_acc.zero_()
+        for cam, gt in views:
+            out = render(st.cloud, cam, medium=st.medium, mode="underwater")
+            res, dL = total_loss_device(out.color, gt, st.medium, self.cfg.lambda_ssim,
+                                        self.cfg.lambda_guide)
+            backward_render(out, dL, st.cloud, st.medium, self.cfg.lambda_guide, buf=self.buf)
+            self.loss_acc[:4] += res[:4]
+            self.loss_acc[4] += 1.0 - res[4]       # count of non-finite losses
+        self.loss_acc[5] = float(len(views))
+
+    def reduce(self):
+        """Sum gradients (and loss statistics) over ranks: one NCCL all-reduce each."""
+        if self.dist is not None and self.world > 1:
+            self.dist.all_reduce(self.buf.flat, group=self.group)
+            self.dist.all_reduce(self.loss_acc, group=self.group)
+
+    def step(self, views: Sequence, sharded: bool = False) -> StepStats:
+        """One optimizer step over a batch of (camera, gt) views.
+
+        ``views`` is the global batch (sharded here) unless ``sharded=True``.
+        """
+        mine = views if sharded else self.shard(views)
+        self.local_pass(mine)
+        self.reduce()
+        finite = self.buf.all_finite_device().double()
+        vals = torch.cat([self.loss_acc, finite[None]]).tolist()
+        nviews = max(vals[5], 1.0)
+        stats = StepStats(vals[0] / nviews, vals[1] / nviews, vals[2] / nviews, vals[3] / nviews,
+                          int(vals[5]), False)
+        if vals[4] > 0 or vals[6] < 0.5:
+            log.warning("iteration %d: non-finite loss or gradients, skipping update",
+                        self.state.iteration)
+            stats.skipped = True
+            return stats
+        _accumulate_stats(self.state, self.buf)
+        apply_gradients(self.state, self.buf, self.cfg, self.spatial_scale)
+        return stats
