@@ -90,7 +90,7 @@ class GaussianCloud:
         device = torch.device(device) if device is not None else default_device()
         pos = _as_f32(positions, (-1, 3), device)
         n = pos.shape[0]
-        sh = _as_f32(sh_coeffs, (n, -1, 3), device)
+        sh = _as_f32(sh_coeffs, (n, -1, 3) if n else (0, 1, 3), device)
         if sh.shape[1] != 1:
             raise ValueError("only constant (degree-0) color features are supported")
         self._n = n

@@ -42,6 +42,39 @@ class StepStats:
     skipped: bool
 
 
+GRAD_LAYOUT = (("d_positions", 3), ("d_log_scales", 3), ("d_rotations", 4), ("d_sh_coeffs", 3),
+               ("d_opacity_logits", 1), ("mean2d_grad_norm", 1), ("observed", 1))
+
+
+def pack_gradients(grads: dict, n: int) -> torch.Tensor:
+    """Pack per-field gradients (any device, e.g. CPU for tests) into the flat
+    GradientBuffer layout ``[14n params | n norm | n observed | 9 medium | pad]``."""
+    parts = []
+    for name, w in GRAD_LAYOUT:
+        t = torch.as_tensor(grads[name]).reshape(n * w).to(torch.float32)
+        parts.append(t)
+    med = torch.cat([torch.as_tensor(grads[k]).reshape(3).to(torch.float32)
+                     for k in ("d_attenuation", "d_water_color", "d_backscatter")])
+    parts += [med, torch.zeros(7, dtype=torch.float32)]
+    return torch.cat(parts)
+
+
+def unpack_gradients(flat: torch.Tensor, n: int) -> dict:
+    out, o = {}, 0
+    for name, w in GRAD_LAYOUT:
+        out[name] = flat[o:o + n * w].reshape((n, w) if w > 1 else (n,))
+        o += n * w
+    for k in ("d_attenuation", "d_water_color", "d_backscatter"):
+        out[k] = flat[o:o + 3]
+        o += 3
+    return out
+
+
+def shard_views(views: Sequence, rank: int, world: int) -> Sequence:
+    """Round-robin assignment of the global view batch to ranks."""
+    return views[rank::world]
+
+
 def _accumulate_stats(state: TrainState, buf: GradientBuffer):
     """grad_accum[observed] += mean2d_grad_norm; obs_count[observed] += views (pipeline.py:191-192)."""
     state.grad_accum += buf.mean2d_grad_norm
@@ -91,7 +124,7 @@ class ViewShardedTrainer:
 
     def shard(self, views: Sequence) -> Sequence:
         """Views of this rank: round-robin over the global view list."""
-        return views[self.rank::self.world]
+        return shard_views(views, self.rank, self.world)
 
     def local_pass(self, views: Sequence):
         """Render + loss + backward of this rank's views into self.buf."""
