@@ -184,7 +184,7 @@ def run_gpu(args):
     medium = uw.MediumParams(**MEDIUM)
     state = uw.TrainState(cloud, medium, iteration=1)
     cfg = uw.OptimConfig()
-    trainer = uw.ViewShardedTrainer(state, cfg)
+    trainer = uw.ViewShardedTrainer(state, cfg, W, H)
     cam = uw.Camera.look_at(view_eye(rank), (0, 0, 12), width=W, height=H, fx=1.2 * W, fy=1.2 * W)
     gt_host = torch.from_numpy(gt_image(rank)).pin_memory()
     gt_dev = gt_host.to(dev)

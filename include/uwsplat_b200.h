@@ -115,15 +115,27 @@ int uws_preprocess_fwd(const uws_cloud* cloud, const uws_camera* cam, uws_projec
                        void* workspace, size_t workspace_bytes, void* stream);
 
 /* ---- binning (replaces rasterizer.bin_and_sort, rasterizer.py:50-85).
- *      Phase 1 sorts rows by float64 depth and counts tile entries, writing
- *      E to *total_entries (device int64).  Phase 2 emits (tile, row) pairs
- *      in depth order, stable-sorts them by tile and writes CSR ranges. ---- */
-int uws_bin_workspace_size(int64_t k, int64_t e, int32_t n_tiles, size_t* count_bytes,
-                           size_t* emit_bytes);
-int uws_bin_count(const uws_projected* proj, int64_t k, const uws_camera* cam,
-                  int64_t* total_entries, void* count_ws, size_t count_bytes, void* stream);
-int uws_bin_emit(const uws_projected* proj, int64_t k, int64_t e, const uws_camera* cam,
-                 int32_t* offsets /* [tiles+1] */, int32_t* entries /* [E] rows */,
+ *      Sizes live on the device so a training step needs no host sync:
+ *      K is read from proj->num_visible (k_cap only sizes grids/workspace).
+ *      uws_bin_count stable-sorts the visible rows by float64 depth and
+ *      counts, per tile row, the entries of each 2048-rank block; it writes
+ *      totals[0] = E (tile entries) and totals[1] = S (row segments).
+ *      uws_bin_emit builds the tile lists by two levels of stable bucketing
+ *      -- rank order -> tile-row lists -> tile lists -- and the CSR ranges.
+ *      If E > e_cap or S > s_cap it sets *overflow = 1, writes all-zero
+ *      offsets (empty lists) and nothing else -- and, if skip_counter is
+ *      given, adds 65536 to it so a following uws_adam_step is a no-op; the
+ *      caller grows its buffers to the totals and re-runs.  count_ws is sized with (k_cap, 0) and must
+ *      be the same buffer in both calls; emit_ws with (k_cap, s_cap). */
+int uws_bin_workspace_size(int64_t k_cap, int64_t s_cap, int32_t n_tiles_x, int32_t n_tiles_y,
+                           size_t* count_bytes, size_t* emit_bytes);
+int uws_bin_count(const uws_projected* proj, int64_t k_cap, const uws_camera* cam,
+                  int64_t* totals /* device [2]: E, S */, void* count_ws, size_t count_bytes,
+                  void* stream);
+int uws_bin_emit(const uws_projected* proj, int64_t k_cap, int64_t e_cap, int64_t s_cap,
+                 const uws_camera* cam, const int64_t* totals /* device, from uws_bin_count */,
+                 int32_t* offsets /* [tiles+1] */, int32_t* entries /* [e_cap] rows */,
+                 int32_t* overflow /* device flag */, float* skip_counter /* optional */,
                  void* count_ws, size_t count_bytes, void* emit_ws, size_t emit_bytes,
                  void* stream);
 
@@ -138,11 +150,12 @@ int uws_raster_fwd(const uws_projected* proj, const int32_t* offsets, const int3
  *      d_ssim :83-123).  rendered/gt: [H][W][C] float32.  medium: device
  *      float[15] (9 params + water_color_guide[3] + backscatter_guide[3]) or
  *      NULL.  result: device double[6] = l1, d_ssim, l_bs, total,
- *      finite flag (1.0/0.0), reserved. ----------------------------------- */
+ *      finite flag (1.0/0.0), reserved.  nonfinite (optional device float):
+ *      incremented when the total is not finite (pipeline.py:182-184). ---- */
 int uws_loss_workspace_size(int32_t h, int32_t w, int32_t c, size_t* bytes);
 int uws_loss_fwd_bwd(const float* rendered, const float* gt, int32_t h, int32_t w, int32_t c,
                      const float* medium, int32_t has_guidance, double lambda_ssim,
-                     double lambda_guide, float* dL_dC, double* result,
+                     double lambda_guide, float* dL_dC, double* result, float* nonfinite,
                      void* workspace, size_t workspace_bytes, void* stream);
 
 /* ---- backward compositing (replaces backward._backward_block :124-163 and
@@ -156,23 +169,31 @@ int uws_raster_bwd(const uws_projected* proj, const int32_t* offsets, const int3
 /* ---- projection backward (replaces backward._project_backward :184-258 and
  *      _quat_backward :166-181).  grads: float32 flat buffer laid out as
  *      [positions 3n | log_scales 3n | rotations 4n | sh 3n | opacity n |
- *       mean2d_grad_norm n | observed n | medium 9], accumulated (+=).
- *      medium_acc (may be NULL in clean mode) plus the guidance subgradient
- *      lambda_guide*sign(.) are added into the medium slots. -------------- */
+ *       mean2d_grad_norm n | observed n | medium 9 | non-finite counter |
+ *       pad 6], accumulated (+=); K is read from proj->num_visible.
+ *      screen_grads and medium_acc are consumed and left zeroed.  The
+ *      guidance subgradient lambda_guide*sign(.) is added into the medium
+ *      slots (backward.py:270-274).  nonfinite (optional device float) is
+ *      incremented when an accumulated gradient is not finite
+ *      (GradientBuffer.all_finite, backward.py:66-69). ----------------- */
 int uws_preprocess_bwd(const uws_cloud* cloud, const uws_camera* cam, const uws_projected* proj,
-                       int64_t k, const float* screen_grads, const double* medium_acc,
+                       int64_t k_cap, float* screen_grads, double* medium_acc,
                        const float* medium, int32_t has_guidance, double lambda_guide,
-                       float* grads, void* stream);
+                       float* grads, float* nonfinite, void* stream);
 
 /* ---- optimizer (replaces optim.apply_gradients :98-120 / adam_step :69-83,
  *      GaussianCloud.normalize_rotations scene.py:165-167 and
- *      MediumParams.clamp_ scene.py:207-211).  params/m/v/grads use the flat
- *      layout above (params: 14n + 9 medium at offset 14n when medium_params
- *      is NULL, or medium separately). --------------------------------- */
-int uws_adam_step(float* params, float* exp_avg, float* exp_avg_sq, const float* grads,
-                  int64_t n, float* medium_params, float* medium_exp_avg,
-                  float* medium_exp_avg_sq, const float* medium_grads,
-                  const uws_adam_params* hp, void* stream);
+ *      MediumParams.clamp_ scene.py:207-211).  params/m/v: 14n floats in the
+ *      field layout above; grads: the flat gradient buffer; medium_*: 9
+ *      floats (medium_grads = grads + 16n).  Optional step control for the
+ *      device-resident training loop (pipeline.py:182-192): skip (device
+ *      float) > 0 turns the update into a no-op; grad_accum/obs_count
+ *      receive the densification statistics; zero_grads leaves the whole
+ *      gradient buffer zeroed for the next step. --------------------- */
+int uws_adam_step(float* params, float* exp_avg, float* exp_avg_sq, float* grads, int64_t n,
+                  float* medium_params, float* medium_exp_avg, float* medium_exp_avg_sq,
+                  float* medium_grads, const uws_adam_params* hp, const float* skip,
+                  float* grad_accum, int32_t* obs_count, int32_t zero_grads, void* stream);
 
 #ifdef __cplusplus
 }

@@ -56,26 +56,28 @@ _SIGS = {
     "uws_preprocess_workspace_size": (c_int, [c_int64, POINTER(c_size_t)]),
     "uws_preprocess_fwd": (c_int, [POINTER(CloudC), POINTER(CameraC), POINTER(ProjectedC),
                                    c_void_p, c_size_t, c_void_p]),
-    "uws_bin_workspace_size": (c_int, [c_int64, c_int64, c_int32, POINTER(c_size_t),
+    "uws_bin_workspace_size": (c_int, [c_int64, c_int64, c_int32, c_int32, POINTER(c_size_t),
                                        POINTER(c_size_t)]),
     "uws_bin_count": (c_int, [POINTER(ProjectedC), c_int64, POINTER(CameraC), c_void_p,
                               c_void_p, c_size_t, c_void_p]),
-    "uws_bin_emit": (c_int, [POINTER(ProjectedC), c_int64, c_int64, POINTER(CameraC), c_void_p,
-                             c_void_p, c_void_p, c_size_t, c_void_p, c_size_t, c_void_p]),
+    "uws_bin_emit": (c_int, [POINTER(ProjectedC), c_int64, c_int64, c_int64, POINTER(CameraC),
+                             c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p,
+                             c_size_t, c_void_p, c_size_t, c_void_p]),
     "uws_raster_fwd": (c_int, [POINTER(ProjectedC), c_void_p, c_void_p, POINTER(CameraC),
                                c_void_p, POINTER(RasterOutC), c_void_p]),
     "uws_loss_workspace_size": (c_int, [c_int32, c_int32, c_int32, POINTER(c_size_t)]),
     "uws_loss_fwd_bwd": (c_int, [c_void_p, c_void_p, c_int32, c_int32, c_int32, c_void_p,
                                  c_int32, c_double, c_double, c_void_p, c_void_p, c_void_p,
-                                 c_size_t, c_void_p]),
+                                 c_void_p, c_size_t, c_void_p]),
     "uws_raster_bwd": (c_int, [POINTER(ProjectedC), c_void_p, c_void_p, POINTER(CameraC),
                                c_void_p, POINTER(RasterOutC), c_void_p, c_void_p, c_void_p,
                                c_void_p]),
     "uws_preprocess_bwd": (c_int, [POINTER(CloudC), POINTER(CameraC), POINTER(ProjectedC),
                                    c_int64, c_void_p, c_void_p, c_void_p, c_int32, c_double,
-                                   c_void_p, c_void_p]),
+                                   c_void_p, c_void_p, c_void_p]),
     "uws_adam_step": (c_int, [c_void_p, c_void_p, c_void_p, c_void_p, c_int64, c_void_p,
-                              c_void_p, c_void_p, c_void_p, POINTER(AdamParamsC), c_void_p]),
+                              c_void_p, c_void_p, c_void_p, POINTER(AdamParamsC), c_void_p,
+                              c_void_p, c_void_p, c_int32, c_void_p]),
 }
 
 EXPORTED = tuple(_SIGS)

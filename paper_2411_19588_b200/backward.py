@@ -19,7 +19,7 @@ from .rasterizer import RenderOutput
 from .scene import GaussianCloud, MediumParams, flat_views
 
 GRAD_FLOATS_PER_GAUSSIAN = 16   # 14 params + mean2d_grad_norm + observed
-MEDIUM_SLOTS = 16               # 9 used
+MEDIUM_SLOTS = 16               # 9 medium gradients, the non-finite counter, pad
 
 
 class GradientBuffer:
@@ -48,6 +48,7 @@ class GradientBuffer:
         self.d_attenuation = self.flat[16 * n:16 * n + 3]
         self.d_water_color = self.flat[16 * n + 3:16 * n + 6]
         self.d_backscatter = self.flat[16 * n + 6:16 * n + 9]
+        self.nonfinite = self.flat[16 * n + 9:16 * n + 10]   # device skip counter
         self.generation = -1
 
     @property
@@ -110,8 +111,8 @@ def backward_render(out: RenderOutput, dL_dC, cloud: GaussianCloud,
     dev = cloud.device
     dL = dL_dC if isinstance(dL_dC, torch.Tensor) else torch.as_tensor(dL_dC)
     dL = dL.to(device=dev, dtype=torch.float32).contiguous()
-    k = len(proj)
-    screen = torch.zeros(max(k, 1), 9, dtype=torch.float32, device=dev)
+    k_cap = proj.n_source
+    screen = torch.zeros(max(k_cap, 1), 9, dtype=torch.float32, device=dev)
     med_acc = torch.zeros(9, dtype=torch.float64, device=dev) if underwater else None
     st = _lib.stream_handle()
     pc, cc, oc = proj.c_struct(), cam.c_struct(), out.c_struct()
@@ -121,7 +122,7 @@ def backward_render(out: RenderOutput, dL_dC, cloud: GaussianCloud,
               _lib.ptr(med_acc), st)
     cl = cloud.c_struct()
     guided = 1 if (medium is not None and medium.has_guidance) else 0
-    _lib.call("uws_preprocess_bwd", ctypes.byref(cl), ctypes.byref(cc), ctypes.byref(pc), k,
+    _lib.call("uws_preprocess_bwd", ctypes.byref(cl), ctypes.byref(cc), ctypes.byref(pc), k_cap,
               _lib.ptr(screen), _lib.ptr(med_acc), med, guided, float(lambda_guide),
-              _lib.ptr(buf.flat), st)
+              _lib.ptr(buf.flat), 0, st)
     return buf

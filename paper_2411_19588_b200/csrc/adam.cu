@@ -36,12 +36,40 @@ __device__ __forceinline__ void adam1(float& p, float& m, float& v, float g, con
     v = (float)vv;
 }
 
+struct AdamCtl {
+    const float* skip;      // device: skip the update when *skip > 0 (non-finite count)
+    float* grad_accum;      // densify statistics (pipeline.py:191-192), may be NULL
+    int32_t* obs_count;
+    int zero_grads;         // leave the gradient buffer zeroed for the next step
+};
+
 __global__ void __launch_bounds__(kThreads) k_adam_cloud(float* __restrict__ P, float* __restrict__ M,
                                                          float* __restrict__ V,
-                                                         const float* __restrict__ Gr, int64_t n,
-                                                         uws_adam_params hp) {
+                                                         float* __restrict__ Gr, int64_t n,
+                                                         uws_adam_params hp, AdamCtl ctl) {
     const int64_t i = (int64_t)blockIdx.x * kThreads + threadIdx.x;
     if (i >= n) return;
+    const bool skip = ctl.skip && *ctl.skip > 0.0f;
+    if (skip) {
+        if (ctl.zero_grads) {
+            const int64_t base[5] = {0, 3 * n, 6 * n, 10 * n, 13 * n};
+            const int width[5] = {3, 3, 4, 3, 1};
+#pragma unroll
+            for (int f = 0; f < 5; ++f)
+                for (int c = 0; c < width[f]; ++c) Gr[base[f] + i * width[f] + c] = 0.f;
+            Gr[14 * n + i] = 0.f;
+            Gr[15 * n + i] = 0.f;
+        }
+        return;
+    }
+    if (ctl.grad_accum) {
+        ctl.grad_accum[i] += Gr[14 * n + i];
+        ctl.obs_count[i] += (int32_t)Gr[15 * n + i];
+    }
+    if (ctl.zero_grads) {
+        Gr[14 * n + i] = 0.f;
+        Gr[15 * n + i] = 0.f;
+    }
     const int64_t base[5] = {0, 3 * n, 6 * n, 10 * n, 13 * n};
     const int width[5] = {3, 3, 4, 3, 1};
 #pragma unroll
@@ -54,6 +82,7 @@ __global__ void __launch_bounds__(kThreads) k_adam_cloud(float* __restrict__ P, 
             const int64_t o = base[f] + i * width[f] + c;
             float p = P[o], m = M[o], v = V[o];
             adam1(p, m, v, Gr[o], k, hp);
+            if (ctl.zero_grads) Gr[o] = 0.f;
             q[c] = p;
             M[o] = m;
             V[o] = v;
@@ -76,9 +105,16 @@ __global__ void __launch_bounds__(kThreads) k_adam_cloud(float* __restrict__ P, 
 }
 
 __global__ void k_adam_medium(float* __restrict__ P, float* __restrict__ M, float* __restrict__ V,
-                              const float* __restrict__ Gr, uws_adam_params hp) {
+                              float* __restrict__ Gr, uws_adam_params hp, AdamCtl ctl) {
     const int v = threadIdx.x;
-    if (v >= 9) return;
+    if (v >= 16) return;
+    const bool skip = ctl.skip && *ctl.skip > 0.0f;
+    __syncwarp();
+    if (v >= 9 || skip) {
+        // slots 9..15 (non-finite counter + pad) are reset after every step
+        if (ctl.zero_grads) Gr[v] = 0.f;
+        return;
+    }
     const int f = 5 + v / 3;
     const AdamK k{hp.lr[f], hp.bias1[f], hp.bias2[f]};
     float p = P[v], m = M[v], vv = V[v];
@@ -90,6 +126,7 @@ __global__ void k_adam_medium(float* __restrict__ P, float* __restrict__ M, floa
     P[v] = p;
     M[v] = m;
     V[v] = vv;
+    if (ctl.zero_grads) Gr[v] = 0.f;
 }
 
 }  // namespace
@@ -97,24 +134,35 @@ __global__ void k_adam_medium(float* __restrict__ P, float* __restrict__ M, floa
 
 using namespace uws;
 
-extern "C" int uws_adam_step(float* params, float* exp_avg, float* exp_avg_sq, const float* grads,
+extern "C" int uws_adam_step(float* params, float* exp_avg, float* exp_avg_sq, float* grads,
                              int64_t n, float* medium_params, float* medium_exp_avg,
-                             float* medium_exp_avg_sq, const float* medium_grads,
-                             const uws_adam_params* hp, void* stream) {
+                             float* medium_exp_avg_sq, float* medium_grads,
+                             const uws_adam_params* hp, const float* skip, float* grad_accum,
+                             int32_t* obs_count, int32_t zero_grads, void* stream) {
     UWS_REQUIRE(hp != nullptr && n >= 0, "uws_adam_step: bad argument");
+    UWS_REQUIRE((grad_accum == nullptr) == (obs_count == nullptr),
+                "uws_adam_step: grad_accum and obs_count go together");
     cudaStream_t st = as_stream(stream);
-    if (n > 0) {
-        UWS_REQUIRE(params && exp_avg && exp_avg_sq && grads, "uws_adam_step: null cloud buffer");
-        k_adam_cloud<<<(unsigned)ceil_div(n, kThreads), kThreads, 0, st>>>(params, exp_avg, exp_avg_sq,
-                                                                           grads, n, *hp);
-        UWS_CHECK_LAUNCH("k_adam_cloud");
-    }
+    AdamCtl ctl{skip, grad_accum, obs_count, zero_grads};
+    // the medium kernel reads the skip flag before the cloud kernel may zero it
     if (medium_params) {
         UWS_REQUIRE(medium_exp_avg && medium_exp_avg_sq && medium_grads,
                     "uws_adam_step: null medium buffer");
+        AdamCtl mctl = ctl;
+        mctl.zero_grads = 0;
         k_adam_medium<<<1, 32, 0, st>>>(medium_params, medium_exp_avg, medium_exp_avg_sq,
-                                        medium_grads, *hp);
+                                        medium_grads, *hp, mctl);
         UWS_CHECK_LAUNCH("k_adam_medium");
+    }
+    if (n > 0) {
+        UWS_REQUIRE(params && exp_avg && exp_avg_sq && grads, "uws_adam_step: null cloud buffer");
+        k_adam_cloud<<<(unsigned)ceil_div(n, kThreads), kThreads, 0, st>>>(params, exp_avg, exp_avg_sq,
+                                                                           grads, n, *hp, ctl);
+        UWS_CHECK_LAUNCH("k_adam_cloud");
+    }
+    if (medium_params && zero_grads) {
+        // medium slots + counter/pad (16 floats) zeroed after every reader is done
+        UWS_CUDA(cudaMemsetAsync(medium_grads, 0, 16 * sizeof(float), st));
     }
     return UWS_OK;
 }

@@ -169,7 +169,7 @@ __global__ void __launch_bounds__(kThreads) k_loss_finalize(const double* __rest
                                                             int n_l1, double n_px, double n_win,
                                                             const float* medium, int has_guidance,
                                                             double lam_s, double lam_g,
-                                                            double* result) {
+                                                            double* result, float* nonfinite) {
     __shared__ double rs[kThreads], rl[kThreads];
     double s = 0, l = 0;
     for (int i = threadIdx.x; i < n_s; i += kThreads) s += part_s[i];
@@ -201,6 +201,7 @@ __global__ void __launch_bounds__(kThreads) k_loss_finalize(const double* __rest
         result[3] = total;
         result[4] = isfinite(total) ? 1.0 : 0.0;
         result[5] = 0.0;
+        if (!isfinite(total) && nonfinite) atomicAdd(nonfinite, 1.0f);
     }
 }
 
@@ -256,8 +257,8 @@ extern "C" int uws_loss_workspace_size(int32_t h, int32_t w, int32_t c, size_t* 
 extern "C" int uws_loss_fwd_bwd(const float* rendered, const float* gt, int32_t h, int32_t w,
                                 int32_t c, const float* medium, int32_t has_guidance,
                                 double lambda_ssim, double lambda_guide, float* dL_dC,
-                                double* result, void* workspace, size_t workspace_bytes,
-                                void* stream) {
+                                double* result, float* nonfinite, void* workspace,
+                                size_t workspace_bytes, void* stream) {
     UWS_REQUIRE(rendered && gt && dL_dC && result, "uws_loss_fwd_bwd: null argument");
     UWS_REQUIRE(h >= kN && w >= kN, "uws_loss_fwd_bwd: image smaller than the 11x11 window");
     UWS_REQUIRE(c >= 1, "uws_loss_fwd_bwd: bad channel count");
@@ -280,7 +281,8 @@ extern "C" int uws_loss_fwd_bwd(const float* rendered, const float* gt, int32_t 
                                          dL_dC, p.part_l1);
     UWS_CHECK_LAUNCH("k_ssim_grad");
     k_loss_finalize<<<1, kThreads, 0, st>>>(p.part_s, p.n_s, p.part_l1, p.n_l1, n_px, n_win, medium,
-                                            has_guidance, lambda_ssim, lambda_guide, result);
+                                            has_guidance, lambda_ssim, lambda_guide, result,
+                                            nonfinite);
     UWS_CHECK_LAUNCH("k_loss_finalize");
     return UWS_OK;
 }

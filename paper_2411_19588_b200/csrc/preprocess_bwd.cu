@@ -21,17 +21,21 @@ constexpr int kThreads = 128;
 __global__ void __launch_bounds__(kThreads) k_preprocess_bwd(uws_cloud cl, uws_camera cam,
                                                              const int32_t* __restrict__ src_index,
                                                              const double* __restrict__ exact,
-                                                             int64_t k,
-                                                             const float* __restrict__ screen,
-                                                             float* __restrict__ grads) {
+                                                             const int32_t* __restrict__ k_dev,
+                                                             float* __restrict__ screen,
+                                                             float* __restrict__ grads,
+                                                             float* __restrict__ nonfinite) {
     const int64_t row = (int64_t)blockIdx.x * kThreads + threadIdx.x;
-    if (row >= k) return;
+    if (row >= (int64_t)*k_dev) return;
     const int64_t n = cl.n;
     const int64_t i = src_index[row];
-    const float* sg = screen + row * 9;
+    float* sg = screen + row * 9;
     const double gl = sg[0], dmx = sg[1], dmy = sg[2];
     const double dca = sg[3], dcb = sg[4], dcc = sg[5];
     const double dcol[3] = {sg[6], sg[7], sg[8]};
+    // leave the screen-space accumulator zeroed for the next view
+#pragma unroll
+    for (int v = 0; v < 9; ++v) sg[v] = 0.f;
 
     Geo G;
     geo_view(cl, cam, i, G);
@@ -127,32 +131,53 @@ __global__ void __launch_bounds__(kThreads) k_preprocess_bwd(uws_cloud cl, uws_c
     float* gop = grads + 13 * n;
     float* gnorm = grads + 14 * n;
     float* gobs = grads + 15 * n;
+    bool finite = true;
 #pragma unroll
     for (int c = 0; c < 3; ++c) {
-        gpos[3 * i + c] += (float)(dtx * R[c] + dty * R[3 + c] + dtz * R[6 + c]);
-        gls[3 * i + c] += (float)dls[c];
+        float v = gpos[3 * i + c] + (float)(dtx * R[c] + dty * R[3 + c] + dtz * R[6 + c]);
+        gpos[3 * i + c] = v;
+        finite &= isfinite(v);
+        v = gls[3 * i + c] + (float)dls[c];
+        gls[3 * i + c] = v;
+        finite &= isfinite(v);
         const double col = (double)cl.sh_coeffs[3 * i + c] * kSH_C0 + 0.5;
-        if (col > 0.0) gsh[3 * i + c] += (float)(kSH_C0 * dcol[c]);
+        v = gsh[3 * i + c] + (col > 0.0 ? (float)(kSH_C0 * dcol[c]) : 0.0f);
+        gsh[3 * i + c] = v;
+        finite &= isfinite(v);
     }
 #pragma unroll
-    for (int c = 0; c < 4; ++c) grot[4 * i + c] += (float)((dq[c] - G.qu[c] * radial) / G.qn);
-    gop[i] += (float)((1.0 - sop) * gl);
+    for (int c = 0; c < 4; ++c) {
+        float v = grot[4 * i + c] + (float)((dq[c] - G.qu[c] * radial) / G.qn);
+        grot[4 * i + c] = v;
+        finite &= isfinite(v);
+    }
+    {
+        float v = gop[i] + (float)((1.0 - sop) * gl);
+        gop[i] = v;
+        finite &= isfinite(v);
+    }
     const double nx = dmx * cam.width * 0.5, ny = dmy * cam.height * 0.5;
     gnorm[i] += (float)sqrt(nx * nx + ny * ny);
     gobs[i] += 1.0f;
+    if (!finite && nonfinite) atomicAdd(nonfinite, 1.0f);
 }
 
-// medium slots: accumulated image sums + lambda * sign(param - guide)
-__global__ void k_medium_finalize(const double* __restrict__ acc, const float* __restrict__ medium,
-                                  int has_guidance, double lam, float* __restrict__ gmed) {
+// medium slots: accumulated image sums + lambda * sign(param - guide); the
+// accumulator is left zeroed for the next view
+__global__ void k_medium_finalize(double* __restrict__ acc, const float* __restrict__ medium,
+                                  int has_guidance, double lam, float* __restrict__ gmed,
+                                  float* __restrict__ nonfinite) {
     const int v = threadIdx.x;
     if (v >= 9) return;
     double s = acc ? acc[v] : 0.0;
+    if (acc) acc[v] = 0.0;
     if (acc && has_guidance && lam != 0.0 && v >= 3) {
         double d = (double)medium[v] - (double)medium[v + 6];
         s += lam * (d > 0 ? 1.0 : (d < 0 ? -1.0 : 0.0));
     }
-    gmed[v] += (float)s;
+    const float r = gmed[v] + (float)s;
+    gmed[v] = r;
+    if (!isfinite(r) && nonfinite) atomicAdd(nonfinite, 1.0f);
 }
 
 }  // namespace
@@ -161,23 +186,24 @@ __global__ void k_medium_finalize(const double* __restrict__ acc, const float* _
 using namespace uws;
 
 extern "C" int uws_preprocess_bwd(const uws_cloud* cloud, const uws_camera* cam,
-                                  const uws_projected* proj, int64_t k, const float* screen_grads,
-                                  const double* medium_acc, const float* medium,
-                                  int32_t has_guidance, double lambda_guide, float* grads,
+                                  const uws_projected* proj, int64_t k_cap, float* screen_grads,
+                                  double* medium_acc, const float* medium, int32_t has_guidance,
+                                  double lambda_guide, float* grads, float* nonfinite,
                                   void* stream) {
-    UWS_REQUIRE(cloud && cam && proj && grads, "uws_preprocess_bwd: null argument");
-    UWS_REQUIRE(k >= 0 && k <= cloud->n, "uws_preprocess_bwd: k out of range");
+    UWS_REQUIRE(cloud && cam && proj && grads && proj->num_visible, "uws_preprocess_bwd: null argument");
+    UWS_REQUIRE(k_cap >= 0 && k_cap <= cloud->n, "uws_preprocess_bwd: k out of range");
     UWS_REQUIRE(medium_acc == nullptr || medium != nullptr, "uws_preprocess_bwd: medium missing");
     cudaStream_t st = as_stream(stream);
-    if (k > 0) {
+    if (k_cap > 0) {
         UWS_REQUIRE(screen_grads != nullptr, "uws_preprocess_bwd: screen_grads missing");
-        k_preprocess_bwd<<<(unsigned)ceil_div(k, kThreads), kThreads, 0, st>>>(
-            *cloud, *cam, proj->source_index, proj->exact, k, screen_grads, grads);
+        k_preprocess_bwd<<<(unsigned)ceil_div(k_cap, kThreads), kThreads, 0, st>>>(
+            *cloud, *cam, proj->source_index, proj->exact, proj->num_visible, screen_grads, grads,
+            nonfinite);
         UWS_CHECK_LAUNCH("k_preprocess_bwd");
     }
     if (medium_acc) {
         k_medium_finalize<<<1, 32, 0, st>>>(medium_acc, medium, has_guidance, lambda_guide,
-                                            grads + 16 * cloud->n);
+                                            grads + 16 * cloud->n, nonfinite);
         UWS_CHECK_LAUNCH("k_medium_finalize");
     }
     return UWS_OK;

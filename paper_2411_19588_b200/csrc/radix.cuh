@@ -37,25 +37,40 @@ constexpr int tile_items() {
     return kThreads * Cfg<K>::kIpt;
 }
 
+__device__ __forceinline__ uint32_t dev_count(const uint32_t* n_dev, uint32_t n_cap) {
+    if (!n_dev) return n_cap;
+    uint32_t n = *n_dev;
+    return n < n_cap ? n : n_cap;
+}
+
 template <typename K>
-__global__ void __launch_bounds__(kThreads) k_histogram(const K* __restrict__ keys, uint32_t n,
-                                                       int begin_bit, int passes,
-                                                       uint32_t* __restrict__ hist) {
+__global__ void __launch_bounds__(kThreads) k_histogram(const K* __restrict__ keys, uint32_t n_cap,
+                                                       const uint32_t* n_dev, int begin_bit,
+                                                       int passes, uint32_t* __restrict__ hist) {
     __shared__ uint32_t h[8 * kBins];
     for (int i = threadIdx.x; i < passes * kBins; i += kThreads) h[i] = 0;
     __syncthreads();
+    const uint32_t n = dev_count(n_dev, n_cap);
     const unsigned lt = lanemask_lt();
     const uint32_t stride = gridDim.x * kThreads;
     for (uint32_t base = blockIdx.x * kThreads; base < n; base += stride) {
         uint32_t i = base + threadIdx.x;
         bool valid = i < n;
         K key = valid ? keys[i] : K(0);
+        const unsigned vmask = __ballot_sync(0xffffffffu, valid);
+        if (vmask == 0) continue;  // whole warp past the end (lane 0 would index bin 256)
         for (int p = 0; p < passes; ++p) {
             unsigned d = valid ? unsigned((key >> (begin_bit + 8 * p)) & 0xFF) : 0x100u;
-            unsigned peers = __match_any_sync(0xffffffffu, d);
-            if (valid && (peers & lt) == 0) atomicAdd(&h[p * kBins + d], __popc(peers));
+            unsigned d0 = __shfl_sync(0xffffffffu, d, __ffs(vmask) - 1);
+            if (__all_sync(0xffffffffu, d == d0 || !valid)) {
+                // common for the high digits of nearby keys: one atomic per warp
+                if ((threadIdx.x & 31) == 0) atomicAdd(&h[p * kBins + d0], __popc(vmask));
+            } else if (valid) {
+                atomicAdd(&h[p * kBins + d], 1u);
+            }
         }
     }
+    (void)lt;
     __syncthreads();
     for (int i = threadIdx.x; i < passes * kBins; i += kThreads)
         if (h[i]) atomicAdd(&hist[i], h[i]);
@@ -77,8 +92,9 @@ template <typename K>
 __global__ void __launch_bounds__(kThreads) k_onesweep(const K* __restrict__ keys_in,
                                                       const uint32_t* __restrict__ vals_in,
                                                       K* __restrict__ keys_out,
-                                                      uint32_t* __restrict__ vals_out, uint32_t n,
-                                                      int shift, const uint32_t* __restrict__ bin_base,
+                                                      uint32_t* __restrict__ vals_out, uint32_t n_cap,
+                                                      const uint32_t* n_dev, int shift,
+                                                      const uint32_t* __restrict__ bin_base,
                                                       uint32_t* status, uint32_t* ticket) {
     constexpr int IPT = Cfg<K>::kIpt;
     constexpr int TILE = kThreads * IPT;
@@ -96,6 +112,7 @@ __global__ void __launch_bounds__(kThreads) k_onesweep(const K* __restrict__ key
     __syncthreads();
     const int tile = s_tile;
     const uint32_t base = (uint32_t)tile * TILE;
+    const uint32_t n = dev_count(n_dev, n_cap);
 
     K key[IPT];
     uint32_t val[IPT];
@@ -166,7 +183,7 @@ __global__ void __launch_bounds__(kThreads) k_onesweep(const K* __restrict__ key
         }
     }
     __syncthreads();
-    uint32_t count = n - base < (uint32_t)TILE ? n - base : (uint32_t)TILE;
+    uint32_t count = base >= n ? 0u : (n - base < (uint32_t)TILE ? n - base : (uint32_t)TILE);
     for (uint32_t j = tid; j < count; j += kThreads) {
         K k = s_keys[j];
         unsigned d = unsigned((k >> shift) & 0xFF);
@@ -191,32 +208,32 @@ inline void plan(Workspace& ws, uint32_t n, int passes, K** k_alt, uint32_t** v_
 }
 
 // Sort (keys_in, vals_in or identity if NULL) by bits [begin_bit, begin_bit+8*passes).
+// n_cap sizes the grids; the actual count is *n_dev when n_dev != NULL.
 // The result lands in (keys_out, vals_out); keys_in/vals_in are not modified.
 // The histogram/status/ticket block must be contiguous (as laid out by plan()).
 template <typename K>
 inline cudaError_t sort_pairs(const K* keys_in, const uint32_t* vals_in, K* keys_out,
-                              uint32_t* vals_out, uint32_t n, int begin_bit, int passes,
-                              K* k_tmp, uint32_t* v_tmp, uint32_t* hist, uint32_t* status,
-                              uint32_t* tickets, size_t meta_bytes, cudaStream_t st) {
-    if (n == 0) return cudaSuccess;
+                              uint32_t* vals_out, uint32_t n_cap, const uint32_t* n_dev,
+                              int begin_bit, int passes, K* k_tmp, uint32_t* v_tmp, uint32_t* hist,
+                              uint32_t* status, uint32_t* tickets, size_t meta_bytes,
+                              cudaStream_t st) {
+    if (n_cap == 0) return cudaSuccess;
     cudaError_t e = cudaMemsetAsync(hist, 0, meta_bytes, st);
     if (e != cudaSuccess) return e;
-    int hist_blocks = (int)ceil_div(n, kThreads * 8);
+    int hist_blocks = (int)ceil_div(n_cap, kThreads * 8);
     if (hist_blocks > 1184) hist_blocks = 1184;
-    k_histogram<K><<<hist_blocks, kThreads, 0, st>>>(keys_in, n, begin_bit, passes, hist);
+    k_histogram<K><<<hist_blocks, kThreads, 0, st>>>(keys_in, n_cap, n_dev, begin_bit, passes, hist);
     k_scan_hist<<<1, kBins, 0, st>>>(hist, passes);
-    const int tiles = (int)ceil_div(n, tile_items<K>());
+    const int tiles = (int)ceil_div(n_cap, tile_items<K>());
     // ping-pong so that the last pass writes into keys_out/vals_out
     const K* ksrc = keys_in;
     const uint32_t* vsrc = vals_in;
     for (int p = 0; p < passes; ++p) {
-        bool last = p == passes - 1;
         bool to_out = ((passes - 1 - p) % 2) == 0;
         K* kdst = to_out ? keys_out : k_tmp;
         uint32_t* vdst = to_out ? vals_out : v_tmp;
-        (void)last;
-        k_onesweep<K><<<tiles, kThreads, 0, st>>>(ksrc, vsrc, kdst, vdst, n, begin_bit + 8 * p,
-                                                  hist + p * kBins,
+        k_onesweep<K><<<tiles, kThreads, 0, st>>>(ksrc, vsrc, kdst, vdst, n_cap, n_dev,
+                                                  begin_bit + 8 * p, hist + p * kBins,
                                                   status + (size_t)p * tiles * kBins, tickets + p);
         ksrc = kdst;
         vsrc = vdst;

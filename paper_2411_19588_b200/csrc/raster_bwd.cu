@@ -4,25 +4,29 @@
 // and fixed-order merge of backward_render (:278-344), and backward_medium
 // (:261-275).
 //
-// One CTA per tile, one thread per pixel, walking the tile list BACK to
-// front over exactly the prefix the forward consumed (per-pixel `last`).
-// Transmittance is recovered as T_i = T_{i+1} / (1 - alpha_i) from the
-// stored final transmittance, and the suffix sum_{j>i} w_j (G . c_j) of the
-// reference's reverse cumsum (:149) is carried as one scalar per pixel, so no
-// per-pair state is stored.  Alpha and its gates are recomputed with the
-// forward's exact arithmetic, hence identical decisions.
+// One CTA per tile, kPix vertically strided pixels per thread, walking the
+// tile list BACK to front over exactly the prefix the forward consumed
+// (per-pixel `last`).  Transmittance is recovered as T_i = T_{i+1}/(1-alpha_i)
+// from the stored final transmittance, and the suffix sum_{j>i} w_j (G . c_j)
+// of the reference's reverse cumsum (:149) is carried as one scalar per
+// pixel, so no per-pair state is stored.  Alpha and its gates are recomputed
+// with the forward's exact arithmetic, hence identical decisions.
 //
 // The 9 per-(pixel, Gaussian) partials (dpower, dpower*dx, dpower*dy,
-// dpower*dx^2, dpower*dx*dy, dpower*dy^2, w*G) are reduced across the warp
-// with a transposed butterfly (14 shuffles instead of 45), accumulated over
-// the CTA's 8 warps in shared memory, chained through the conic once per
-// (tile, Gaussian) and only then sent to HBM with 9 atomics.
+// dpower*dx^2, dpower*dx*dy, dpower*dy^2, w*G) are first summed over the
+// thread's kPix pixels, then across the warp with a transposed butterfly
+// (14 shuffles instead of 45), accumulated over the CTA's warps in shared
+// memory, chained through the conic once per (tile, Gaussian) and only then
+// sent to HBM with 9 atomics.
+#include <cstdlib>
+
 #include "raster_common.cuh"
 
 namespace uws {
 namespace {
 
-constexpr int kWarps = kRasterThreads / 32;
+constexpr int kBatch = 256;
+constexpr float kLn2 = 0.69314718055994531f;
 
 struct BwdArgs {
     const uws_splat* splat;
@@ -42,7 +46,7 @@ struct BwdArgs {
 
 // Reduce v[0..7] across the warp; returns the full sum of value index
 // ((lane>>4)&1)*4 + ((lane>>3)&1)*2 + ((lane>>2)&1) (valid in every lane).
-__device__ __forceinline__ float butterfly8(float v[8], int lane) {
+__device__ __forceinline__ float butterfly8(const float v[8], int lane) {
     const bool b4 = lane & 16, b3 = lane & 8, b2 = lane & 4;
     float h[4];
 #pragma unroll
@@ -65,55 +69,67 @@ __device__ __forceinline__ float butterfly8(float v[8], int lane) {
     return r;
 }
 
-__global__ void __launch_bounds__(kRasterThreads, 3) k_raster_bwd(BwdArgs a) {
-    __shared__ StageA sA[kRasterThreads];
-    __shared__ StageB sB[kRasterThreads];
-    __shared__ StageC sC[kRasterThreads];
-    __shared__ int sRow[kRasterThreads];
-    __shared__ float sAcc[9][kRasterThreads];
+template <int kPix>
+__global__ void __launch_bounds__(kRasterThreads / kPix, 3 * kPix) k_raster_bwd(BwdArgs a) {
+    constexpr int kThreads = kRasterThreads / kPix;
+    constexpr int kWarps = kThreads / 32;
+    constexpr int kRowStep = kTile / kPix;
+    __shared__ StageA sA[kBatch];
+    __shared__ StageB sB[kBatch];
+    __shared__ StageC sC[kBatch];
+    __shared__ float sAcc[9][kBatch];
     __shared__ float sMed[kWarps][9];
     __shared__ int sMaxLast;
 
     const int tile = blockIdx.x;
     const int ty = tile / a.gx, tx = tile - ty * a.gx;
     const int ox = tx * kTile, oy = ty * kTile;
-    const int lx = threadIdx.x & (kTile - 1), ly = threadIdx.x / kTile;
-    const int px = ox + lx, py = oy + ly;
-    const bool inside = px < a.width && py < a.height;
-    const float fx = (float)lx + 0.5f, fy = (float)ly + 0.5f;
+    const int lx = threadIdx.x & (kTile - 1), ly0 = threadIdx.x / kTile;
+    const float fx = (float)lx + 0.5f;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int start = a.offsets[tile], end = a.offsets[tile + 1];
+    (void)end;
 
     if (threadIdx.x == 0) sMaxLast = 0;
-#pragma unroll
-    for (int v = 0; v < 9; ++v) sAcc[v][threadIdx.x] = 0.f;
+    for (int i = threadIdx.x; i < 9 * kBatch; i += kThreads) (&sAcc[0][0])[i] = 0.f;
 
-    float G[3] = {0.f, 0.f, 0.f};
+    float G[kPix][3], T[kPix], S[kPix], fy[kPix];
+    int mylast[kPix];
     float med[9];
 #pragma unroll
     for (int v = 0; v < 9; ++v) med[v] = 0.f;
-    float T = 1.f;
-    int mylast = 0;
-    if (inside) {
-        const int pix = py * a.width + px;
-        T = a.final_T[pix];
-        mylast = a.last[pix];
-        if (a.medium) {
-            const float d = a.depth[pix];
-            const float z = 2.0f / (1.0f + expf(-(float)kLogisticRate * d)) - 1.0f;
+    int maxl = 0;
 #pragma unroll
-            for (int ch = 0; ch < 3; ++ch) {
-                const float dl = a.dL[3 * pix + ch];
-                const float att = expf(-a.medium[ch] * z);
-                const float ebs = expf(-a.medium[6 + ch] * z);
-                G[ch] = dl * att;
-                med[ch] = dl * a.color_clean[3 * pix + ch] * (-z) * att;   // d attenuation
-                med[3 + ch] = dl * (1.0f - ebs);                             // d water_color
-                med[6 + ch] = dl * a.medium[3 + ch] * z * ebs;               // d backscatter
+    for (int p = 0; p < kPix; ++p) {
+        const int ly = ly0 + p * kRowStep;
+        fy[p] = (float)ly + 0.5f;
+        S[p] = 0.f;
+        T[p] = 1.f;
+        mylast[p] = 0;
+        G[p][0] = G[p][1] = G[p][2] = 0.f;
+        const int px = ox + lx, py = oy + ly;
+        if (px < a.width && py < a.height) {
+            const int pix = py * a.width + px;
+            T[p] = a.final_T[pix];
+            mylast[p] = a.last[pix];
+            maxl = max(maxl, mylast[p]);
+            if (a.medium) {
+                const float d = a.depth[pix];
+                const float z = 2.0f / (1.0f + expf(-(float)kLogisticRate * d)) - 1.0f;
+#pragma unroll
+                for (int ch = 0; ch < 3; ++ch) {
+                    const float dl = a.dL[3 * pix + ch];
+                    const float att = expf(-a.medium[ch] * z);
+                    const float ebs = expf(-a.medium[6 + ch] * z);
+                    G[p][ch] = dl * att;
+                    med[ch] += dl * a.color_clean[3 * pix + ch] * (-z) * att;   // d attenuation
+                    med[3 + ch] += dl * (1.0f - ebs);                            // d water_color
+                    med[6 + ch] += dl * a.medium[3 + ch] * z * ebs;              // d backscatter
+                }
+            } else {
+#pragma unroll
+                for (int ch = 0; ch < 3; ++ch) G[p][ch] = a.dL[3 * pix + ch];
             }
-        } else {
-#pragma unroll
-            for (int ch = 0; ch < 3; ++ch) G[ch] = a.dL[3 * pix + ch];
         }
     }
     if (a.medium) {
@@ -124,7 +140,7 @@ __global__ void __launch_bounds__(kRasterThreads, 3) k_raster_bwd(BwdArgs a) {
         }
     }
     __syncthreads();
-    if (mylast > 0) atomicMax(&sMaxLast, mylast);
+    if (maxl > 0) atomicMax(&sMaxLast, maxl);
     if (a.medium && threadIdx.x < 9) {
         float s = 0.f;
 #pragma unroll
@@ -134,60 +150,62 @@ __global__ void __launch_bounds__(kRasterThreads, 3) k_raster_bwd(BwdArgs a) {
     __syncthreads();
     const int maxlast = sMaxLast;
 
-    float S = 0.f;  // sum over later contributors of w_j (G . c_j)
-    for (int bend = start + maxlast; bend > start; bend -= kRasterThreads) {
-        const int bstart = max(start, bend - kRasterThreads);
+    for (int bend = start + maxlast; bend > start; bend -= kBatch) {
+        const int bstart = max(start, bend - kBatch);
         const int nb = bend - bstart;
         __syncthreads();
-        if (threadIdx.x < nb) {
-            const int row = a.entries[bstart + threadIdx.x];
-            float dep;
-            stage_entry(a.splat, row, ox, oy, sA[threadIdx.x], sB[threadIdx.x], sC[threadIdx.x], dep);
-            sRow[threadIdx.x] = row;
+#pragma unroll
+        for (int s = 0; s < kBatch / kThreads; ++s) {
+            const int i = threadIdx.x + s * kThreads;
+            if (i < nb) stage_entry(a.splat, a.entries[bstart + i], ox, oy, sA[i], sB[i], sC[i]);
         }
         __syncthreads();
         for (int k = nb - 1; k >= 0; --k) {
             const int jrel = bstart - start + k;
             float v[9];
+#pragma unroll
+            for (int i = 0; i < 9; ++i) v[i] = 0.f;
             bool hit = false;
-            if (jrel < mylast) {
-                const StageA A = sA[k];
-                const StageB B = sB[k];
-                const float dx = fx - A.mx, dy = fy - A.my;
-                const float power = -0.5f * (A.ca * dx * dx + B.cc * dy * dy) - A.cb * dx * dy;
-                if (power >= B.skip) {
-                    const float araw = B.op * __expf(power);
-                    if (araw >= kFloorHi || floor_pass(araw, a.splat, a.exact, sRow[k], px, py)) {
-                        hit = true;
-                        const float alpha = fminf(araw, kClampF);
-                        const float inv_om = __frcp_rn(1.0f - alpha);
-                        const float Ti = T * inv_om;
-                        const float w = alpha * Ti;
-                        const StageC C = sC[k];
-                        const float U = G[0] * B.r + G[1] * C.g + G[2] * C.b;
-                        const float dalpha = U * Ti - S * inv_om;
-                        S += w * U;
-                        T = Ti;
-                        const float dp = below_clamp(araw, a.splat, a.exact, sRow[k], px, py)
-                                             ? dalpha * araw
-                                             : 0.f;
-                        v[0] = dp;
-                        v[1] = dp * dx;
-                        v[2] = dp * dy;
-                        v[3] = v[1] * dx;
-                        v[4] = v[1] * dy;
-                        v[5] = v[2] * dy;
-                        v[6] = w * G[0];
-                        v[7] = w * G[1];
-                        v[8] = w * G[2];
-                    }
-                }
+            const StageA A = sA[k];
+            const StageB B = sB[k];
+            const float dx = fx - A.mx;
+            const float tA = A.A * dx;
+#pragma unroll
+            for (int p = 0; p < kPix; ++p) {
+                if (jrel >= mylast[p]) continue;
+                const float dy = fy[p] - A.my;
+                const float power = dx * fmaf(A.B, dy, tA) + B.C * dy * dy;
+                if (power < B.skip) continue;
+                const float araw = B.op * ex2_ftz(power);
+                const int py = oy + ly0 + p * kRowStep;
+                if (araw < kFloorHi && !floor_pass(araw, a.splat, a.exact, sC[k].row, ox + lx, py))
+                    continue;
+                hit = true;
+                const float alpha = fminf(araw, kClampF);
+                const float inv_om = __frcp_rn(1.0f - alpha);
+                const float Ti = T[p] * inv_om;
+                const float w = alpha * Ti;
+                const StageC& C = sC[k];
+                const float U = G[p][0] * C.r + G[p][1] * C.g + G[p][2] * C.b;
+                const float dalpha = U * Ti - S[p] * inv_om;
+                S[p] = fmaf(w, U, S[p]);
+                T[p] = Ti;
+                const float dp = (araw < kClampLo || below_clamp(araw, a.splat, a.exact, C.row,
+                                                                 ox + lx, py))
+                                     ? dalpha * araw
+                                     : 0.f;
+                const float dpx = dp * dx, dpy = dp * dy;
+                v[0] += dp;
+                v[1] += dpx;
+                v[2] += dpy;
+                v[3] = fmaf(dpx, dx, v[3]);
+                v[4] = fmaf(dpx, dy, v[4]);
+                v[5] = fmaf(dpy, dy, v[5]);
+                v[6] = fmaf(w, G[p][0], v[6]);
+                v[7] = fmaf(w, G[p][1], v[7]);
+                v[8] = fmaf(w, G[p][2], v[8]);
             }
             if (!__any_sync(0xffffffffu, hit)) continue;
-            if (!hit) {
-#pragma unroll
-                for (int i = 0; i < 9; ++i) v[i] = 0.f;
-            }
             const float r8 = butterfly8(v, lane);
             const float r9 = warp_sum(v[8]);
             if ((lane & 3) == 0) {
@@ -197,8 +215,7 @@ __global__ void __launch_bounds__(kRasterThreads, 3) k_raster_bwd(BwdArgs a) {
             if (lane == 0) atomicAdd(&sAcc[8][k], r9);
         }
         __syncthreads();
-        if (threadIdx.x < nb) {
-            const int k = threadIdx.x;
+        for (int k = threadIdx.x; k < nb; k += kThreads) {
             float s[9];
             bool any = false;
 #pragma unroll
@@ -208,21 +225,32 @@ __global__ void __launch_bounds__(kRasterThreads, 3) k_raster_bwd(BwdArgs a) {
                 any |= s[i] != 0.f;
             }
             if (any) {
-                const StageA A = sA[k];
-                const StageB B = sB[k];
-                float* g = a.screen + (size_t)sRow[k] * 9;
-                atomicAdd(g + 0, s[0]);                          // d_logit (before (1-s))
-                atomicAdd(g + 1, A.ca * s[1] + A.cb * s[2]);     // d_mean2d x
-                atomicAdd(g + 2, A.cb * s[1] + B.cc * s[2]);     // d_mean2d y
-                atomicAdd(g + 3, -0.5f * s[3]);                  // d_conic a
-                atomicAdd(g + 4, -s[4]);                         // d_conic b
-                atomicAdd(g + 5, -0.5f * s[5]);                  // d_conic c
-                atomicAdd(g + 6, s[6]);                          // d_color
+                // natural-units conic from the log2-scaled staged values
+                const float ca = sA[k].A * (-2.0f * kLn2);
+                const float cb = sA[k].B * (-kLn2);
+                const float cc = sB[k].C * (-2.0f * kLn2);
+                float* g = a.screen + (size_t)sC[k].row * 9;
+                atomicAdd(g + 0, s[0]);                      // d_logit (before (1-s))
+                atomicAdd(g + 1, ca * s[1] + cb * s[2]);     // d_mean2d x
+                atomicAdd(g + 2, cb * s[1] + cc * s[2]);     // d_mean2d y
+                atomicAdd(g + 3, -0.5f * s[3]);              // d_conic a
+                atomicAdd(g + 4, -s[4]);                     // d_conic b
+                atomicAdd(g + 5, -0.5f * s[5]);              // d_conic c
+                atomicAdd(g + 6, s[6]);                      // d_color
                 atomicAdd(g + 7, s[7]);
                 atomicAdd(g + 8, s[8]);
             }
         }
     }
+}
+
+int bwd_pix() {
+    static int pix = [] {
+        const char* e = getenv("UWS_BWD_PIX");
+        int v = e ? atoi(e) : 4;
+        return (v == 2 || v == 8) ? v : 4;
+    }();
+    return pix;
 }
 
 }  // namespace
@@ -256,7 +284,12 @@ extern "C" int uws_raster_bwd(const uws_projected* proj, const int32_t* offsets,
     a.dL = dL_dC;
     a.screen = screen_grads;
     a.medium_acc = medium_acc;
-    k_raster_bwd<<<a.gx * gy, kRasterThreads, 0, as_stream(stream)>>>(a);
+    cudaStream_t st = as_stream(stream);
+    switch (bwd_pix()) {
+        case 2: k_raster_bwd<2><<<a.gx * gy, kRasterThreads / 2, 0, st>>>(a); break;
+        case 8: k_raster_bwd<8><<<a.gx * gy, kRasterThreads / 8, 0, st>>>(a); break;
+        default: k_raster_bwd<4><<<a.gx * gy, kRasterThreads / 4, 0, st>>>(a); break;
+    }
     UWS_CHECK_LAUNCH("k_raster_bwd");
     return UWS_OK;
 }

@@ -5,29 +5,48 @@
 // rasterizer.py:163-169, backward.py:151) are decided with float32 and, when
 // alpha_raw falls inside a +-kGuard relative band around a threshold,
 // re-decided from the float64 record exactly as the reference computes it.
+//
+// Staged record layout (per tile-list entry, shared memory): the conic is
+// pre-scaled by -0.5*log2(e) (and -log2(e) for the cross term) so that
+//     alpha_raw = opacity * 2^(dx*(A*dx + B*dy) + C*dy*dy)
+// costs 2 FADD + 5 FMUL/FFMA + 1 MUFU.EX2 per pair, and the mean is stored
+// relative to the tile origin (computed in float64 -> exact local offsets).
 #pragma once
 
 #include "common.cuh"
 
 namespace uws {
 
-constexpr int kRasterThreads = kTile * kTile;  // one thread per pixel
+constexpr int kRasterThreads = kTile * kTile;  // pixels per tile
+constexpr float kLog2e = 1.4426950408889634f;
 
-// Staged record of one tile-list entry (tile-local mean for exact offsets).
 struct __align__(16) StageA {
-    float mx, my, ca, cb;  // mean relative to the tile origin, conic a, b
+    float mx, my, A, B;  // tile-local mean; -0.5*ca*log2e, -cb*log2e
 };
 struct __align__(16) StageB {
-    float cc, op, skip, r;  // conic c, opacity, log-threshold for early reject, red
+    float C, op, skip, depth;  // -0.5*cc*log2e, opacity, log2-domain reject threshold, depth
 };
-struct __align__(8) StageC {
-    float g, b;
+struct __align__(16) StageC {
+    float r, g, b;
+    int row;
 };
+
+__device__ __forceinline__ float ex2_ftz(float x) {
+    float y;
+    asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+    return y;
+}
+
+__device__ __forceinline__ float lg2_ftz(float x) {
+    float y;
+    asm("lg2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+    return y;
+}
 
 // float64 alpha_raw exactly as the reference evaluates it (rasterizer.py:159-163)
 __device__ __forceinline__ double alpha_raw_f64(const uws_splat* __restrict__ splat,
-                                                const double* __restrict__ exact, int row, int px,
-                                                int py) {
+                                             const double* __restrict__ exact, int row, int px,
+                                             int py) {
     const double mx = splat[row].mx, my = splat[row].my;
     const double4 e = reinterpret_cast<const double4*>(exact)[row];
     double dx = __dsub_rn((double)px + 0.5, mx);
@@ -37,12 +56,19 @@ __device__ __forceinline__ double alpha_raw_f64(const uws_splat* __restrict__ sp
     return __dmul_rn(e.w, exp(power));
 }
 
+// Out-of-line copy for loops that must stay free of float64 code.
+static __device__ __noinline__ double alpha_raw_f64_cold(const uws_splat* __restrict__ splat,
+                                                         const double* __restrict__ exact, int row,
+                                                         int px, int py) {
+    return alpha_raw_f64(splat, exact, row, px, py);
+}
+
 // Gate decision for alpha_raw >= 1/255 given the float32 estimate.
 __device__ __forceinline__ bool floor_pass(float araw, const uws_splat* splat, const double* exact,
                                            int row, int px, int py) {
     if (araw >= kFloorHi) return true;
     if (araw < kFloorLo) return false;
-    return alpha_raw_f64(splat, exact, row, px, py) >= kFloor;
+    return alpha_raw_f64_cold(splat, exact, row, px, py) >= kFloor;
 }
 
 // Gate decision for alpha_raw < 0.99 (backward mask).
@@ -50,30 +76,30 @@ __device__ __forceinline__ bool below_clamp(float araw, const uws_splat* splat, 
                                             int row, int px, int py) {
     if (araw < kClampLo) return true;
     if (araw >= kClampHi) return false;
-    return alpha_raw_f64(splat, exact, row, px, py) < kClamp;
+    return alpha_raw_f64_cold(splat, exact, row, px, py) < kClamp;
 }
 
 // Stage entry `row` of a tile whose origin is (ox, oy).
 __device__ __forceinline__ void stage_entry(const uws_splat* __restrict__ splat, int row, int ox,
-                                            int oy, StageA& a, StageB& b, StageC& c, float& depth) {
+                                            int oy, StageA& a, StageB& b, StageC& c) {
     const float4* p = reinterpret_cast<const float4*>(splat + row);
     float4 w0 = __ldg(p), w1 = __ldg(p + 1), w2 = __ldg(p + 2);
-    double mx, my;
-    mx = __hiloint2double(__float_as_int(w0.y), __float_as_int(w0.x));
-    my = __hiloint2double(__float_as_int(w0.w), __float_as_int(w0.z));
+    double mx = __hiloint2double(__float_as_int(w0.y), __float_as_int(w0.x));
+    double my = __hiloint2double(__float_as_int(w0.w), __float_as_int(w0.z));
     a.mx = (float)(mx - (double)ox);
     a.my = (float)(my - (double)oy);
-    a.ca = w1.x;
-    a.cb = w1.y;
-    b.cc = w1.z;
+    a.A = (-0.5f * kLog2e) * w1.x;
+    a.B = (-kLog2e) * w1.y;
+    b.C = (-0.5f * kLog2e) * w1.z;
     b.op = w1.w;
-    // alpha_raw < floor_lo  <=>  power < log(floor_lo / op); keep a margin so
-    // float32 log/exp error can only send borderline pairs to the full test
-    b.skip = __logf(kFloorLo / w1.w) - 1e-3f;
-    b.r = w2.x;
+    // alpha_raw < floor_lo  <=>  power2 < log2(floor_lo / op); the margin keeps
+    // float32 lg2/ex2 error from rejecting a pair the full test would keep
+    b.skip = lg2_ftz(kFloorLo / w1.w) - 2e-3f;
+    b.depth = w2.w;
+    c.r = w2.x;
     c.g = w2.y;
     c.b = w2.z;
-    depth = w2.w;
+    c.row = row;
 }
 
 }  // namespace uws

@@ -4,18 +4,24 @@
 // per-tile blend _composite_block (:148-178) and apply_water (:244-251) with
 // logistic_remap (medium.py:26-29).
 //
-// One CTA per 16x16 tile, one thread per pixel.  The tile's depth-sorted list
-// is streamed through shared memory in batches of 256 records (each thread
-// stages one record with three 16-byte loads); every thread then walks the
-// batch front to back.  A pixel stops once its transmittance drops below
-// 1e-4 -- the contributor that crosses the threshold is still blended, as in
-// the reference -- and the CTA leaves as soon as all 256 pixels are done.
-// The per-pixel consumed-prefix length is written out so the backward kernel
+// One CTA per 16x16 tile, PIX vertically strided pixels per thread.  The
+// tile's depth-sorted list is streamed through shared memory in batches of
+// 256 records; every thread walks the batch front to back.  The walk is a
+// tight loop that only leaves to a slow path when a pair's alpha lands in
+// the float64 guard band of the 1/255 floor (rare), so the hot loop carries
+// no float64 code.  A pixel stops once its transmittance drops below 1e-4 --
+// the contributor that crosses the threshold is still blended, as in the
+// reference -- and the CTA leaves as soon as all its pixels are done.  The
+// per-pixel consumed-prefix length is written out so the backward kernel
 // visits exactly the same pairs.
+#include <cstdlib>
+
 #include "raster_common.cuh"
 
 namespace uws {
 namespace {
+
+constexpr int kBatch = 256;
 
 struct FwdArgs {
     const uws_splat* splat;
@@ -28,95 +34,152 @@ struct FwdArgs {
     uws_raster_out out;
 };
 
-__global__ void __launch_bounds__(kRasterThreads, 3) k_raster_fwd(FwdArgs a) {
-    __shared__ StageA sA[kRasterThreads];
-    __shared__ StageB sB[kRasterThreads];
-    __shared__ StageC sC[kRasterThreads];
-    __shared__ float sD[kRasterThreads];
-    __shared__ int sRow[kRasterThreads];
+struct PixState {
+    float T, cr, cg, cb, dsum, wsum;
+    int count, last;
+    bool done;
+};
+
+__device__ __forceinline__ void blend(PixState& s, float araw, const float4& c, float depth,
+                                      int idx) {
+    const float alpha = fminf(araw, kClampF);
+    const float w = alpha * s.T;
+    s.cr = fmaf(w, c.x, s.cr);
+    s.cg = fmaf(w, c.y, s.cg);
+    s.cb = fmaf(w, c.z, s.cb);
+    s.dsum = fmaf(w, depth, s.dsum);
+    s.wsum += w;
+    s.T = s.T * (1.0f - alpha);
+    ++s.count;
+    s.last = idx;
+    if (!(s.T >= kTStopF)) s.done = true;
+}
+
+template <int PIX>
+__global__ void __launch_bounds__(kRasterThreads / PIX, (PIX == 1 ? 3 : 4 * PIX / 2)) k_raster_fwd(FwdArgs a) {
+    constexpr int THREADS = kRasterThreads / PIX;
+    constexpr int ROWSTEP = kTile / PIX;
+    __shared__ float4 sP0[kBatch];  // mx, my, A, B
+    __shared__ float4 sP1[kBatch];  // C, op, skip, depth
+    __shared__ float4 sP2[kBatch];  // r, g, b, row
 
     const int tile = blockIdx.x;
     const int ty = tile / a.gx, tx = tile - ty * a.gx;
     const int ox = tx * kTile, oy = ty * kTile;
-    const int lx = threadIdx.x & (kTile - 1), ly = threadIdx.x / kTile;
-    const int px = ox + lx, py = oy + ly;
-    const bool inside = px < a.width && py < a.height;
-    const float fx = (float)lx + 0.5f, fy = (float)ly + 0.5f;
+    const int lx = threadIdx.x & (kTile - 1), ly0 = threadIdx.x / kTile;
+    const float fx = (float)lx + 0.5f;
+
+    PixState ps[PIX];
+    float fy[PIX];
+    bool inside[PIX];
+    bool all_done = true;
+#pragma unroll
+    for (int p = 0; p < PIX; ++p) {
+        const int ly = ly0 + p * ROWSTEP;
+        fy[p] = (float)ly + 0.5f;
+        inside[p] = (ox + lx) < a.width && (oy + ly) < a.height;
+        ps[p] = PixState{1.0f, 0.f, 0.f, 0.f, 0.f, 0.f, 0, 0, !inside[p]};
+        all_done &= ps[p].done;
+    }
 
     const int start = a.offsets[tile], end = a.offsets[tile + 1];
-    float T = 1.0f, cr = 0.f, cg = 0.f, cb = 0.f, dsum = 0.f, wsum = 0.f;
-    int count = 0, last = 0;
-    bool done = !inside;
-
-    for (int base = start; base < end; base += kRasterThreads) {
-        if (__syncthreads_count(done) == kRasterThreads) break;
-        const int j = base + threadIdx.x;
-        if (j < end) {
-            const int row = a.entries[j];
-            stage_entry(a.splat, row, ox, oy, sA[threadIdx.x], sB[threadIdx.x], sC[threadIdx.x],
-                        sD[threadIdx.x]);
-            sRow[threadIdx.x] = row;
-        }
-        __syncthreads();
-        const int n = min(kRasterThreads, end - base);
-        if (!done) {
-            for (int k = 0; k < n; ++k) {
-                const StageA A = sA[k];
-                const float dx = fx - A.mx, dy = fy - A.my;
-                const StageB B = sB[k];
-                const float power = -0.5f * (A.ca * dx * dx + B.cc * dy * dy) - A.cb * dx * dy;
-                if (power < B.skip) continue;
-                const float araw = B.op * __expf(power);
-                if (araw < kFloorHi && !floor_pass(araw, a.splat, a.exact, sRow[k], px, py)) continue;
-                const float alpha = fminf(araw, kClampF);
-                const float w = alpha * T;
-                const StageC C = sC[k];
-                cr += w * B.r;
-                cg += w * C.g;
-                cb += w * C.b;
-                dsum += w * sD[k];
-                wsum += w;
-                T = T * (1.0f - alpha);
-                ++count;
-                last = base - start + k + 1;
-                if (!(T >= kTStopF)) {
-                    done = true;
-                    break;
-                }
+    for (int base = start; base < end; base += kBatch) {
+        if (__syncthreads_count(all_done) == THREADS) break;
+#pragma unroll
+        for (int s = 0; s < kBatch / THREADS; ++s) {
+            const int i = threadIdx.x + s * THREADS;
+            if (base + i < end) {
+                StageA sa;
+                StageB sb;
+                StageC sc;
+                stage_entry(a.splat, a.entries[base + i], ox, oy, sa, sb, sc);
+                sP0[i] = make_float4(sa.mx, sa.my, sa.A, sa.B);
+                sP1[i] = make_float4(sb.C, sb.op, sb.skip, sb.depth);
+                sP2[i] = make_float4(sc.r, sc.g, sc.b, __int_as_float(sc.row));
             }
         }
-    }
-    if (!inside) return;
-    const int pix = py * a.width + px;
-    const float depth = count > 0 ? dsum / wsum : a.far_plane;
-    a.out.depth[pix] = depth;
-    a.out.weight[pix] = wsum;
-    a.out.final_T[pix] = T;
-    a.out.count[pix] = count;
-    if (a.out.last) a.out.last[pix] = last;
-    if (a.medium == nullptr) {
-        a.out.color[3 * pix + 0] = cr;
-        a.out.color[3 * pix + 1] = cg;
-        a.out.color[3 * pix + 2] = cb;
-        if (a.out.color_clean) {
-            a.out.color_clean[3 * pix + 0] = cr;
-            a.out.color_clean[3 * pix + 1] = cg;
-            a.out.color_clean[3 * pix + 2] = cb;
-        }
-        return;
-    }
-    // underwater epilogue: z = logistic(depth); C*exp(-Bd z) + Binf (1 - exp(-Bb z))
-    const float z = 2.0f / (1.0f + expf(-(float)kLogisticRate * depth)) - 1.0f;
-    const float c3[3] = {cr, cg, cb};
+        __syncthreads();
+        if (all_done) continue;
+        const int n = min(kBatch, end - base);
+        const int rel = base - start + 1;
 #pragma unroll
-    for (int ch = 0; ch < 3; ++ch) {
-        const float att = expf(-a.medium[ch] * z);
-        const float bs = a.medium[3 + ch] * (1.0f - expf(-a.medium[6 + ch] * z));
-        a.out.color[3 * pix + ch] = c3[ch] * att + bs;
-        if (a.out.color_clean) a.out.color_clean[3 * pix + ch] = c3[ch];
-        if (a.out.attenuation) a.out.attenuation[3 * pix + ch] = att;
-        if (a.out.backscatter) a.out.backscatter[3 * pix + ch] = bs;
+        for (int p = 0; p < PIX; ++p) {
+            PixState& s = ps[p];
+            int k = 0;
+            while (!s.done && k < n) {
+                // hot loop: float32 only
+                for (; k < n; ++k) {
+                    const float4 p0 = sP0[k];
+                    const float4 p1 = sP1[k];
+                    const float dx = fx - p0.x, dy = fy[p] - p0.y;
+                    const float power = dx * fmaf(p0.w, dy, p0.z * dx) + p1.x * dy * dy;
+                    if (power < p1.z) continue;
+                    const float araw = p1.y * ex2_ftz(power);
+                    if (araw < kFloorHi) {
+                        if (araw >= kFloorLo) break;  // guard band -> slow path
+                        continue;
+                    }
+                    blend(s, araw, sP2[k], p1.w, rel + k);
+                    if (s.done) break;
+                }
+                if (s.done || k >= n) break;
+                // slow path: float64 decision of alpha_raw >= 1/255 for entry k
+                const float4 p0 = sP0[k];
+                const float4 p1 = sP1[k];
+                const float4 p2 = sP2[k];
+                const float dx = fx - p0.x, dy = fy[p] - p0.y;
+                const float araw = p1.y * ex2_ftz(dx * fmaf(p0.w, dy, p0.z * dx) + p1.x * dy * dy);
+                if (alpha_raw_f64(a.splat, a.exact, __float_as_int(p2.w), ox + lx,
+                                  oy + ly0 + p * ROWSTEP) >= kFloor)
+                    blend(s, araw, p2, p1.w, rel + k);
+                ++k;
+            }
+        }
+        all_done = true;
+#pragma unroll
+        for (int p = 0; p < PIX; ++p) all_done &= ps[p].done;
     }
+#pragma unroll
+    for (int p = 0; p < PIX; ++p) {
+        if (!inside[p]) continue;
+        const PixState& s = ps[p];
+        const int pix = (oy + ly0 + p * ROWSTEP) * a.width + ox + lx;
+        const float depth = s.count > 0 ? s.dsum / s.wsum : a.far_plane;
+        a.out.depth[pix] = depth;
+        a.out.weight[pix] = s.wsum;
+        a.out.final_T[pix] = s.T;
+        a.out.count[pix] = s.count;
+        if (a.out.last) a.out.last[pix] = s.last;
+        const float c3[3] = {s.cr, s.cg, s.cb};
+        if (a.medium == nullptr) {
+#pragma unroll
+            for (int ch = 0; ch < 3; ++ch) {
+                a.out.color[3 * pix + ch] = c3[ch];
+                if (a.out.color_clean) a.out.color_clean[3 * pix + ch] = c3[ch];
+            }
+            continue;
+        }
+        // underwater epilogue: z = logistic(depth); C*exp(-Bd z) + Binf (1 - exp(-Bb z))
+        const float z = 2.0f / (1.0f + expf(-(float)kLogisticRate * depth)) - 1.0f;
+#pragma unroll
+        for (int ch = 0; ch < 3; ++ch) {
+            const float att = expf(-a.medium[ch] * z);
+            const float bs = a.medium[3 + ch] * (1.0f - expf(-a.medium[6 + ch] * z));
+            a.out.color[3 * pix + ch] = c3[ch] * att + bs;
+            a.out.color_clean[3 * pix + ch] = c3[ch];
+            if (a.out.attenuation) a.out.attenuation[3 * pix + ch] = att;
+            if (a.out.backscatter) a.out.backscatter[3 * pix + ch] = bs;
+        }
+    }
+}
+
+int fwd_pix() {
+    static int pix = [] {
+        const char* e = getenv("UWS_FWD_PIX");
+        int v = e ? atoi(e) : 1;
+        return (v == 2 || v == 4) ? v : 1;
+    }();
+    return pix;
 }
 
 }  // namespace
@@ -144,7 +207,12 @@ extern "C" int uws_raster_fwd(const uws_projected* proj, const int32_t* offsets,
     a.far_plane = (float)cam->far_plane;
     a.medium = medium;
     a.out = *out;
-    k_raster_fwd<<<a.gx * gy, kRasterThreads, 0, as_stream(stream)>>>(a);
+    cudaStream_t st = as_stream(stream);
+    switch (fwd_pix()) {
+        case 2: k_raster_fwd<2><<<a.gx * gy, kRasterThreads / 2, 0, st>>>(a); break;
+        case 4: k_raster_fwd<4><<<a.gx * gy, kRasterThreads / 4, 0, st>>>(a); break;
+        default: k_raster_fwd<1><<<a.gx * gy, kRasterThreads, 0, st>>>(a); break;
+    }
     UWS_CHECK_LAUNCH("k_raster_fwd");
     return UWS_OK;
 }

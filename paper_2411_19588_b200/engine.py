@@ -1,0 +1,200 @@
+"""Device-resident training step without host synchronisation.
+
+The public functions (render / total_loss / backward_render /
+apply_gradients) mirror the reference API and therefore read sizes back to
+the host (K visible Gaussians, E tile entries) to allocate exact outputs.
+The training loop does not need that: :class:`StepEngine` owns persistent
+buffers for a fixed cloud size and image size, passes counts between kernels
+in device memory, and sizes the tile lists with a capacity.  A step is a
+fixed sequence of asynchronous launches --
+
+    per view:  preprocess -> depth sort + tile-row counts -> tile lists
+               -> forward compositing -> L1/D-SSIM loss -> backward
+               compositing -> projection backward (accumulating)
+    then:      [NCCL all-reduce of the flat gradient buffer]
+               -> fused Adam (skips itself on non-finite / overflow,
+                  accumulates the densification statistics, zeroes grads)
+
+-- followed by ONE small device-to-host read (loss values, flags, list
+sizes).  If a view's tile lists did not fit their capacity the kernels turn
+the whole step into a no-op on the device (Adam skipped); the engine grows
+the buffers to the reported sizes and runs the step again.  This is the
+loop body of pipeline.train (reference pipeline.py:170-193).
+"""
+
+from __future__ import annotations
+
+import ctypes
+import logging
+from dataclasses import dataclass
+from typing import Sequence
+
+import torch
+
+from . import _lib
+from .backward import GradientBuffer
+from .losses import total_loss_device
+from .optim import OptimConfig, apply_gradients_device, rollback_steps
+from .projection import ProjectedCloud, preprocess_into
+from .rasterizer import RenderOutput, TileBins, _alloc_output
+from .scene import Camera, TrainState
+
+log = logging.getLogger(__name__)
+
+# per-view stats record (float64 slots)
+_ST_LOSS = 0      # l1, d_ssim, l_bs, total, finite, reserved  (6)
+_ST_TOTALS = 6    # E, S as int64 (2 slots)
+_ST_OVF = 8       # overflow flag of this view (int32 in a float64 slot)
+_ST_SIZE = 10
+
+
+@dataclass
+class EngineStats:
+    l1: float
+    d_ssim: float
+    l_bs: float
+    total: float
+    views: int
+    skipped: bool
+    reruns: int
+    max_entries: int
+
+
+class StepEngine:
+    """Persistent-buffer, sync-free training step for one (cloud size, image size)."""
+
+    def __init__(self, state: TrainState, width: int, height: int, cfg: OptimConfig,
+                 spatial_scale: float = 1.0, max_views: int = 1, entry_capacity: int = 0,
+                 group=None):
+        import torch.distributed as dist
+        self.state = state
+        self.cfg = cfg
+        self.spatial_scale = spatial_scale
+        self.width, self.height = width, height
+        self.max_views = max_views
+        self.group = group
+        self.dist = dist if dist.is_available() and dist.is_initialized() else None
+        self.world = self.dist.get_world_size(group) if self.dist else 1
+        self.rank = self.dist.get_rank(group) if self.dist else 0
+        n = len(state.cloud)
+        dev = state.cloud.device
+        self.n, self.dev = n, dev
+        self.gx, self.gy = (width + 15) // 16, (height + 15) // 16
+        self.proj = ProjectedCloud(n, dev, with_geometry=False)
+        b = _lib.size_out()
+        _lib.call("uws_preprocess_workspace_size", n, ctypes.byref(b))
+        self.pre_ws = torch.empty(max(b.value, 1), dtype=torch.uint8, device=dev)
+        cb, eb = _lib.size_out(), _lib.size_out()
+        _lib.call("uws_bin_workspace_size", n, 0, self.gx, self.gy, ctypes.byref(cb),
+                  ctypes.byref(eb))
+        self.count_ws = torch.empty(max(cb.value, 1), dtype=torch.uint8, device=dev)
+        self.offsets = torch.zeros(self.gx * self.gy + 1, dtype=torch.int32, device=dev)
+        self._set_capacity(entry_capacity or 48 * n, (entry_capacity or 48 * n) // 4)
+        self.out = _alloc_output(height, width, dev, "underwater", False)
+        self.dL = torch.empty(height, width, 3, dtype=torch.float32, device=dev)
+        _lib.call("uws_loss_workspace_size", height, width, 3, ctypes.byref(b))
+        self.loss_ws = torch.empty(b.value, dtype=torch.uint8, device=dev)
+        self.screen = torch.zeros(max(n, 1), 9, dtype=torch.float32, device=dev)
+        self.med_acc = torch.zeros(9, dtype=torch.float64, device=dev)
+        self.grads = GradientBuffer(n, dev)
+        self.stats = torch.zeros(max_views * _ST_SIZE + 2, dtype=torch.float64, device=dev)
+        self.stats_host = torch.zeros_like(self.stats, device="cpu").pin_memory()
+
+    # -- capacity management ---------------------------------------------------
+    def _set_capacity(self, e_cap: int, s_cap: int):
+        self.e_cap = int(e_cap)
+        self.s_cap = int(max(s_cap, 1))
+        self.entries = torch.empty(max(self.e_cap, 1), dtype=torch.int32, device=self.dev)
+        cb, eb = _lib.size_out(), _lib.size_out()
+        _lib.call("uws_bin_workspace_size", self.n, self.s_cap, self.gx, self.gy, ctypes.byref(cb),
+                  ctypes.byref(eb))
+        self.emit_ws = torch.empty(max(eb.value, 1), dtype=torch.uint8, device=self.dev)
+
+    # -- one view: forward + loss + backward into self.grads -----------------------
+    def _view(self, cam: Camera, gt: torch.Tensor, slot: int):
+        st = _lib.stream_handle()
+        cloud, medium = self.state.cloud, self.state.medium
+        cc = cam.c_struct()
+        preprocess_into(self.proj, cloud, cam, self.pre_ws)
+        pc = self.proj.c_struct()
+        rec = self.stats[slot * _ST_SIZE:(slot + 1) * _ST_SIZE]
+        totals = rec[_ST_TOTALS:_ST_TOTALS + 2].view(torch.int64)
+        ovf = rec[_ST_OVF:_ST_OVF + 1].view(torch.int32)[:1]
+        _lib.call("uws_bin_count", ctypes.byref(pc), self.n, ctypes.byref(cc), _lib.ptr(totals),
+                  _lib.ptr(self.count_ws), self.count_ws.numel(), st)
+        _lib.call("uws_bin_emit", ctypes.byref(pc), self.n, self.e_cap, self.s_cap,
+                  ctypes.byref(cc), _lib.ptr(totals), _lib.ptr(self.offsets),
+                  _lib.ptr(self.entries), _lib.ptr(ovf), _lib.ptr(self.grads.nonfinite),
+                  _lib.ptr(self.count_ws), self.count_ws.numel(), _lib.ptr(self.emit_ws),
+                  self.emit_ws.numel(), st)
+        out = self.out
+        oc = out.c_struct()
+        _lib.call("uws_raster_fwd", ctypes.byref(pc), _lib.ptr(self.offsets),
+                  _lib.ptr(self.entries), ctypes.byref(cc), _lib.ptr(medium.flat),
+                  ctypes.byref(oc), st)
+        total_loss_device(out.color, gt, medium, self.cfg.lambda_ssim, self.cfg.lambda_guide,
+                          result=rec[_ST_LOSS:_ST_LOSS + 6], grad=self.dL, workspace=self.loss_ws,
+                          nonfinite=self.grads.nonfinite)
+        _lib.call("uws_raster_bwd", ctypes.byref(pc), _lib.ptr(self.offsets),
+                  _lib.ptr(self.entries), ctypes.byref(cc), _lib.ptr(medium.flat),
+                  ctypes.byref(oc), _lib.ptr(self.dL), _lib.ptr(self.screen),
+                  _lib.ptr(self.med_acc), st)
+        cl = cloud.c_struct()
+        guided = 1 if medium.has_guidance else 0
+        _lib.call("uws_preprocess_bwd", ctypes.byref(cl), ctypes.byref(cc), ctypes.byref(pc),
+                  self.n, _lib.ptr(self.screen), _lib.ptr(self.med_acc), _lib.ptr(medium.flat),
+                  guided, float(self.cfg.lambda_guide), _lib.ptr(self.grads.flat),
+                  _lib.ptr(self.grads.nonfinite), st)
+
+    def last_render(self) -> RenderOutput:
+        """Forward buffers of the most recent view (valid until the next step)."""
+        out = self.out
+        out.proj = self.proj
+        out.bins = TileBins(self.gx, self.gy, self.offsets, self.entries)
+        return out
+
+    def _launch(self, views: Sequence):
+        if len(views) > self.max_views:
+            raise ValueError(f"at most {self.max_views} views per step on this engine")
+        for i, (cam, gt) in enumerate(views):
+            self._view(Camera.from_any(cam), gt, i)
+        if self.dist is not None and self.world > 1:
+            # one NCCL all-reduce of [grads | medium | skip counter | pad]
+            self.dist.all_reduce(self.grads.flat, group=self.group)
+        # the skip counter is consumed (zeroed) by the Adam launch: keep a copy
+        self.stats[-1:].copy_(self.grads.nonfinite)
+        apply_gradients_device(self.state, self.grads, self.cfg, self.spatial_scale)
+        self.stats_host.copy_(self.stats, non_blocking=True)
+
+    def step(self, views: Sequence) -> EngineStats:
+        """One optimizer step over this rank's (camera, gt-on-device) views.
+
+        Loss values in the returned stats are this rank's view averages."""
+        reruns = 0
+        nv = len(views)
+        while True:
+            self._launch(views)
+            torch.cuda.current_stream().synchronize()
+            s = self.stats_host
+            skip_count = float(s[-1])
+            skipped = skip_count > 0
+            need_e = need_s = 0
+            for i in range(nv):
+                tot = s[i * _ST_SIZE + _ST_TOTALS:i * _ST_SIZE + _ST_TOTALS + 2].view(torch.int64)
+                need_e = max(need_e, int(tot[0]))
+                need_s = max(need_s, int(tot[1]))
+            if skipped:
+                rollback_steps(self.state)
+            if skip_count >= 65536.0 and reruns < 3:
+                # some rank's tile lists overflowed: every rank re-runs the step
+                if need_e > self.e_cap or need_s > self.s_cap:
+                    self._set_capacity(int(need_e * 1.25) + 1024, int(need_s * 1.25) + 1024)
+                reruns += 1
+                continue
+            break
+        loss = [sum(float(s[i * _ST_SIZE + j]) for i in range(nv)) / max(nv, 1) for j in range(4)]
+        if skipped:
+            log.warning("iteration %d: non-finite loss or gradients, skipping update",
+                        self.state.iteration)
+        return EngineStats(loss[0], loss[1], loss[2], loss[3], nv * self.world, skipped, reruns,
+                           need_e)

@@ -57,23 +57,27 @@ def _prep(a, b):
 
 
 def total_loss_device(rendered, gt, medium: Optional[MediumParams], lambda_ssim: float = 0.3,
-                      lambda_guide: float = 0.1):
-    """Kernel call; returns (result double[6] on device, dL_dC)."""
+                      lambda_guide: float = 0.1, result=None, grad=None, workspace=None,
+                      nonfinite=None):
+    """Kernel call; returns (result double[6] on device, dL_dC).  Optional
+    preallocated ``result``/``grad``/``workspace`` and a device ``nonfinite``
+    counter (incremented when the total is not finite) serve the engine."""
     a, b = _prep(rendered, gt)
     h, w = a.shape[0], a.shape[1]
     c = a.shape[2] if a.dim() == 3 else 1
     if h < SSIM_WINDOW or w < SSIM_WINDOW:
         raise DataError(f"image {(h, w)} smaller than the {SSIM_WINDOW}x{SSIM_WINDOW} window")
-    grad = torch.empty_like(a)
-    res = torch.empty(6, dtype=torch.float64, device=a.device)
-    nb = _lib.size_out()
-    _lib.call("uws_loss_workspace_size", h, w, c, ctypes.byref(nb))
-    ws = torch.empty(nb.value, dtype=torch.uint8, device=a.device)
+    grad = torch.empty_like(a) if grad is None else grad
+    res = torch.empty(6, dtype=torch.float64, device=a.device) if result is None else result
+    if workspace is None:
+        nb = _lib.size_out()
+        _lib.call("uws_loss_workspace_size", h, w, c, ctypes.byref(nb))
+        workspace = torch.empty(nb.value, dtype=torch.uint8, device=a.device)
     med = _lib.ptr(medium.flat) if medium is not None else 0
     guided = 1 if (medium is not None and medium.has_guidance) else 0
     _lib.call("uws_loss_fwd_bwd", _lib.ptr(a), _lib.ptr(b), h, w, c, med, guided,
               float(lambda_ssim), float(lambda_guide), _lib.ptr(grad), _lib.ptr(res),
-              _lib.ptr(ws), nb.value, _lib.stream_handle())
+              _lib.ptr(nonfinite), _lib.ptr(workspace), workspace.numel(), _lib.stream_handle())
     return res, grad
 
 

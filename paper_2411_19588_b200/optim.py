@@ -128,4 +128,27 @@ def apply_gradients(state: TrainState, buf, cfg: OptimConfig, spatial_scale: flo
     _lib.call("uws_adam_step", _lib.ptr(cloud.flat), _lib.ptr(state.exp_avg),
               _lib.ptr(state.exp_avg_sq), _lib.ptr(buf.flat), n, _lib.ptr(medium.flat),
               _lib.ptr(state.medium_exp_avg), _lib.ptr(state.medium_exp_avg_sq),
-              _lib.ptr(buf.medium), ctypes.byref(hp), _lib.stream_handle())
+              _lib.ptr(buf.medium), ctypes.byref(hp), 0, 0, 0, 0, _lib.stream_handle())
+
+
+def apply_gradients_device(state: TrainState, buf, cfg: OptimConfig, spatial_scale: float = 1.0,
+                           zero_grads: bool = True) -> _lib.AdamParamsC:
+    """Engine form: skip on device when buf.nonfinite > 0, accumulate the
+    densification statistics and leave ``buf`` zeroed.  Advances the step
+    counters; the caller rolls them back (``rollback_steps``) if the device
+    reported a skip."""
+    cloud, medium = state.cloud, state.medium
+    hp = adam_hparams(state, cfg, spatial_scale)
+    _lib.call("uws_adam_step", _lib.ptr(cloud.flat), _lib.ptr(state.exp_avg),
+              _lib.ptr(state.exp_avg_sq), _lib.ptr(buf.flat), len(cloud), _lib.ptr(medium.flat),
+              _lib.ptr(state.medium_exp_avg), _lib.ptr(state.medium_exp_avg_sq),
+              _lib.ptr(buf.medium), ctypes.byref(hp), _lib.ptr(buf.nonfinite),
+              _lib.ptr(state.grad_accum), _lib.ptr(state.obs_count), 1 if zero_grads else 0,
+              _lib.stream_handle())
+    return hp
+
+
+def rollback_steps(state: TrainState) -> None:
+    """Undo the step-counter advance of a skipped update (pipeline.py:182-189)."""
+    for slot in state.adam.values():
+        slot.step -= 1

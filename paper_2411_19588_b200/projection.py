@@ -47,13 +47,28 @@ class ProjectedCloud:
         self._cov2d = torch.empty(cap, 3, dtype=torch.float64, device=device) if with_geometry else None
         self._radius = torch.empty(cap, dtype=torch.float64, device=device) if with_geometry else None
         self._num_visible = torch.zeros(1, dtype=torch.int32, device=device)
-        self.k = 0
+        self._k = 0 if n_source == 0 else None   # host copy of K, read lazily
 
     def c_struct(self) -> _lib.ProjectedC:
         return _lib.ProjectedC(_lib.ptr(self._source_index), _lib.ptr(self._splat),
                                _lib.ptr(self._exact), _lib.ptr(self._depth), _lib.ptr(self._rect),
                                _lib.ptr(self._cov2d), _lib.ptr(self._radius),
                                _lib.ptr(self._num_visible))
+
+    @property
+    def k(self) -> int:
+        """Number of visible rows (one device-to-host read on first use)."""
+        if self._k is None:
+            self._k = int(self._num_visible.item())
+        return self._k
+
+    def invalidate(self):
+        """Forget the host copy of K (the buffers are being re-filled)."""
+        self._k = 0 if self.n_source == 0 else None
+
+    @property
+    def num_visible(self) -> torch.Tensor:
+        return self._num_visible
 
     def __len__(self) -> int:
         return self.k
@@ -100,20 +115,27 @@ class ProjectedCloud:
         return self.color <= 0.0
 
 
-def project_cloud(cloud: GaussianCloud, cam, with_geometry: bool = True) -> ProjectedCloud:
-    """Project every Gaussian, dropping those that cannot touch the image
-    (reference projection.py:100-199).  Synchronises once to read K."""
-    cam = Camera.from_any(cam)
-    proj = ProjectedCloud(len(cloud), cloud.device, with_geometry)
+def preprocess_into(proj: ProjectedCloud, cloud: GaussianCloud, cam, workspace=None) -> None:
+    """Run the preprocess kernel into an existing ProjectedCloud (no host sync)."""
+    proj.invalidate()
     if len(cloud) == 0:
-        return proj
-    ws_bytes = _lib.size_out()
-    _lib.call("uws_preprocess_workspace_size", len(cloud), ctypes.byref(ws_bytes))
-    ws = torch.empty(ws_bytes.value, dtype=torch.uint8, device=cloud.device)
+        proj._num_visible.zero_()
+        return
+    if workspace is None:
+        ws_bytes = _lib.size_out()
+        _lib.call("uws_preprocess_workspace_size", len(cloud), ctypes.byref(ws_bytes))
+        workspace = torch.empty(ws_bytes.value, dtype=torch.uint8, device=cloud.device)
     cl, cc, pc = cloud.c_struct(), cam.c_struct(), proj.c_struct()
     _lib.call("uws_preprocess_fwd", ctypes.byref(cl), ctypes.byref(cc), ctypes.byref(pc),
-              _lib.ptr(ws), ws_bytes.value, _lib.stream_handle())
-    proj.k = int(proj._num_visible.item())
+              _lib.ptr(workspace), workspace.numel(), _lib.stream_handle())
+
+
+def project_cloud(cloud: GaussianCloud, cam, with_geometry: bool = True) -> ProjectedCloud:
+    """Project every Gaussian, dropping those that cannot touch the image
+    (reference projection.py:100-199).  K is read from the device lazily."""
+    cam = Camera.from_any(cam)
+    proj = ProjectedCloud(len(cloud), cloud.device, with_geometry)
+    preprocess_into(proj, cloud, cam)
     return proj
 
 

@@ -45,7 +45,8 @@ def bin_and_sort(proj: ProjectedCloud, width: int, height: int,
                  tile_size: int = TILE_SIZE) -> TileBins:
     """Assign footprints to tiles and depth-sort each list (rasterizer.py:50-85).
 
-    Synchronises once to read the entry count E.
+    Standalone form: reads the entry counts once and allocates exactly.  The
+    training engine (engine.py) uses capacity buffers instead and never syncs.
     """
     if tile_size != TILE_SIZE:
         raise ValueError("the device kernels use 16x16 tiles")
@@ -54,23 +55,25 @@ def bin_and_sort(proj: ProjectedCloud, width: int, height: int,
     gx, gy = cam.grid
     dev = proj.device
     offsets = torch.zeros(gx * gy + 1, dtype=torch.int32, device=dev)
-    k = len(proj)
-    if k == 0:
+    k_cap = proj.n_source
+    if k_cap == 0:
         return TileBins(gx, gy, offsets, torch.empty(0, dtype=torch.int32, device=dev))
     cb, eb = _lib.size_out(), _lib.size_out()
-    _lib.call("uws_bin_workspace_size", k, 0, gx * gy, ctypes.byref(cb), ctypes.byref(eb))
+    _lib.call("uws_bin_workspace_size", k_cap, 0, gx, gy, ctypes.byref(cb), ctypes.byref(eb))
     count_ws = torch.empty(cb.value, dtype=torch.uint8, device=dev)
-    total = torch.zeros(1, dtype=torch.int64, device=dev)
+    totals = torch.zeros(2, dtype=torch.int64, device=dev)
+    overflow = torch.zeros(1, dtype=torch.int32, device=dev)
     pc, cc = proj.c_struct(), cam.c_struct()
     st = _lib.stream_handle()
-    _lib.call("uws_bin_count", ctypes.byref(pc), k, ctypes.byref(cc), _lib.ptr(total),
+    _lib.call("uws_bin_count", ctypes.byref(pc), k_cap, ctypes.byref(cc), _lib.ptr(totals),
               _lib.ptr(count_ws), cb.value, st)
-    e = int(total.item())
+    e, s = (int(v) for v in totals.tolist())
     entries = torch.empty(max(e, 1), dtype=torch.int32, device=dev)
-    _lib.call("uws_bin_workspace_size", k, e, gx * gy, ctypes.byref(cb), ctypes.byref(eb))
+    _lib.call("uws_bin_workspace_size", k_cap, s, gx, gy, ctypes.byref(cb), ctypes.byref(eb))
     emit_ws = torch.empty(eb.value, dtype=torch.uint8, device=dev)
-    _lib.call("uws_bin_emit", ctypes.byref(pc), k, e, ctypes.byref(cc), _lib.ptr(offsets),
-              _lib.ptr(entries), _lib.ptr(count_ws), cb.value, _lib.ptr(emit_ws), eb.value, st)
+    _lib.call("uws_bin_emit", ctypes.byref(pc), k_cap, e, s, ctypes.byref(cc), _lib.ptr(totals),
+              _lib.ptr(offsets), _lib.ptr(entries), _lib.ptr(overflow), 0, _lib.ptr(count_ws),
+              cb.value, _lib.ptr(emit_ws), eb.value, st)
     return TileBins(gx, gy, offsets, entries[:e])
 
 

@@ -107,63 +107,38 @@ def train_step(state: TrainState, cam, gt, cfg: OptimConfig, spatial_scale: floa
 
 
 class ViewShardedTrainer:
-    """Data-parallel training over camera views, one process per GPU."""
+    """Data-parallel training over camera views, one process per GPU.
 
-    def __init__(self, state: TrainState, cfg: OptimConfig, spatial_scale: float = 1.0,
-                 group=None):
-        import torch.distributed as dist
+    Every rank holds the full cloud and optimizer state; a batch of views is
+    split round-robin over the ranks, each rank renders and back-propagates
+    its views into one flat gradient buffer (StepEngine), the buffers are
+    summed with one NCCL all-reduce, and every rank applies the identical
+    fused Adam step.  No host synchronisation inside the step.
+    """
+
+    def __init__(self, state: TrainState, cfg: OptimConfig, width: int, height: int,
+                 spatial_scale: float = 1.0, views_per_rank: int = 1, group=None,
+                 entry_capacity: int = 0):
+        from .engine import StepEngine
         self.state = state
-        self.cfg = cfg
-        self.spatial_scale = spatial_scale
-        self.group = group
-        self.dist = dist if dist.is_available() and dist.is_initialized() else None
-        self.world = self.dist.get_world_size(group) if self.dist else 1
-        self.rank = self.dist.get_rank(group) if self.dist else 0
-        self.buf = GradientBuffer(len(state.cloud), state.cloud.device)
-        self.loss_acc = torch.zeros(6, dtype=torch.float64, device=state.cloud.device)
+        self.engine = StepEngine(state, width, height, cfg, spatial_scale,
+                                 max_views=views_per_rank, entry_capacity=entry_capacity,
+                                 group=group)
+        self.world, self.rank = self.engine.world, self.engine.rank
 
     def shard(self, views: Sequence) -> Sequence:
         """Views of this rank: round-robin over the global view list."""
         return shard_views(views, self.rank, self.world)
 
-    def local_pass(self, views: Sequence):
-        """Render + loss + backward of this rank's views into self.buf."""
-        st = self.state
-        self.buf.zero_()
-        self.loss_acc.zero_()
-        for cam, gt in views:
-            out = render(st.cloud, cam, medium=st.medium, mode="underwater")
-            res, dL = total_loss_device(out.color, gt, st.medium, self.cfg.lambda_ssim,
-                                        self.cfg.lambda_guide)
-            backward_render(out, dL, st.cloud, st.medium, self.cfg.lambda_guide, buf=self.buf)
-            self.loss_acc[:4] += res[:4]
-            self.loss_acc[4] += 1.0 - res[4]       # count of non-finite losses
-        self.loss_acc[5] = float(len(views))
-
-    def reduce(self):
-        """Sum gradients (and loss statistics) over ranks: one NCCL all-reduce each."""
-        if self.dist is not None and self.world > 1:
-            self.dist.all_reduce(self.buf.flat, group=self.group)
-            self.dist.all_reduce(self.loss_acc, group=self.group)
-
-    def step(self, views: Sequence, sharded: bool = False) -> StepStats:
-        """One optimizer step over a batch of (camera, gt) views.
-
-        ``views`` is the global batch (sharded here) unless ``sharded=True``.
-        """
+    def step(self, views: Sequence, sharded: bool = False):
+        """One optimizer step over a batch of (camera, gt) views; ``views`` is
+        the global batch (sharded here) unless ``sharded=True``.  Ground-truth
+        images may be host arrays or device tensors."""
         mine = views if sharded else self.shard(views)
-        self.local_pass(mine)
-        self.reduce()
-        finite = self.buf.all_finite_device().double()
-        vals = torch.cat([self.loss_acc, finite[None]]).tolist()
-        nviews = max(vals[5], 1.0)
-        stats = StepStats(vals[0] / nviews, vals[1] / nviews, vals[2] / nviews, vals[3] / nviews,
-                          int(vals[5]), False)
-        if vals[4] > 0 or vals[6] < 0.5:
-            log.warning("iteration %d: non-finite loss or gradients, skipping update",
-                        self.state.iteration)
-            stats.skipped = True
-            return stats
-        _accumulate_stats(self.state, self.buf)
-        apply_gradients(self.state, self.buf, self.cfg, self.spatial_scale)
-        return stats
+        dev = self.state.cloud.device
+        prepared = []
+        for cam, gt in mine:
+            if not (isinstance(gt, torch.Tensor) and gt.is_cuda):
+                gt = torch.as_tensor(gt, dtype=torch.float32).to(dev, non_blocking=True)
+            prepared.append((cam, gt.float()))
+        return self.engine.step(prepared)

@@ -43,14 +43,14 @@ def test_workspace_queries_and_argument_errors(lib):
     n = ctypes.c_size_t(0)
     assert lib.uws_preprocess_workspace_size(1000, ctypes.byref(n)) == 0 and n.value > 0
     a, b = ctypes.c_size_t(0), ctypes.c_size_t(0)
-    assert lib.uws_bin_workspace_size(1000, 5000, 64, ctypes.byref(a), ctypes.byref(b)) == 0
+    assert lib.uws_bin_workspace_size(1000, 5000, 8, 8, ctypes.byref(a), ctypes.byref(b)) == 0
     assert a.value > 0 and b.value > 0
     assert lib.uws_loss_workspace_size(32, 32, 3, ctypes.byref(n)) == 0
     # invalid arguments are rejected before touching the device
     assert lib.uws_preprocess_workspace_size(-1, ctypes.byref(n)) == _lib.UWS_EINVAL
     assert b"bad argument" in lib.uws_last_error()
-    assert lib.uws_loss_fwd_bwd(None, None, 4, 4, 3, None, 0, 0.3, 0.1, None, None, None, 0,
-                                None) == _lib.UWS_EINVAL
+    assert lib.uws_loss_fwd_bwd(None, None, 4, 4, 3, None, 0, 0.3, 0.1, None, None, None, None,
+                                0, None) == _lib.UWS_EINVAL
     with pytest.raises(ValueError):
         _lib.call("uws_preprocess_workspace_size", -5, ctypes.byref(n))
 
