@@ -99,6 +99,8 @@ typedef struct uws_adam_params {
     double lr[8];
     double bias1[8];
     double bias2[8];
+    double inv_bias1[8];   /* RN(1 / bias1): exact-division helper */
+    double inv_bias2[8];
     double beta1, beta2, one_minus_beta1, one_minus_beta2, eps;
 } uws_adam_params;
 
@@ -139,12 +141,27 @@ int uws_bin_emit(const uws_projected* proj, int64_t k_cap, int64_t e_cap, int64_
                  void* count_ws, size_t count_bytes, void* emit_ws, size_t emit_bytes,
                  void* stream);
 
+/* Row-list variant for the training/render hot path: after uws_bin_count,
+ * builds only the first level -- for every tile row, the depth-ordered rows
+ * whose rectangle spans it (row_start [tiles_y+1], row_items [s_cap]) --
+ * and no E-sized tile lists.  The *_rows compositing kernels derive each
+ * tile's list from its row list on the fly and stop at saturation.  Only
+ * S <= s_cap is checked (overflow / skip_counter as above). */
+int uws_bin_rows(const uws_projected* proj, int64_t k_cap, int64_t s_cap, const uws_camera* cam,
+                 const int64_t* totals, int32_t* row_start,
+                 void* row_items /* [s_cap] x 8 B: row, tile x0 | x1 << 16 */,
+                 int32_t* overflow, float* skip_counter, void* count_ws, size_t count_bytes,
+                 void* stream);
+
 /* ---- forward compositing + medium epilogue (replaces rasterizer.render's
  *      tile loop / _composite_block :148-178 / apply_water :244-251).
  *      medium: device float[9] = attenuation[3], water_color[3],
  *      backscatter[3]; NULL selects clean mode. ---------------------------- */
 int uws_raster_fwd(const uws_projected* proj, const int32_t* offsets, const int32_t* entries,
                    const uws_camera* cam, const float* medium, uws_raster_out* out, void* stream);
+int uws_raster_fwd_rows(const uws_projected* proj, const int32_t* row_start,
+                        const void* row_items, const uws_camera* cam, const float* medium,
+                        uws_raster_out* out, void* stream);
 
 /* ---- loss (replaces losses.total_loss :140-160 incl. l1 :40-49 and
  *      d_ssim :83-123).  rendered/gt: [H][W][C] float32.  medium: device
@@ -165,6 +182,10 @@ int uws_loss_fwd_bwd(const float* rendered, const float* gt, int32_t h, int32_t 
 int uws_raster_bwd(const uws_projected* proj, const int32_t* offsets, const int32_t* entries,
                    const uws_camera* cam, const float* medium, const uws_raster_out* fwd,
                    const float* dL_dC, float* screen_grads, double* medium_acc, void* stream);
+int uws_raster_bwd_rows(const uws_projected* proj, const int32_t* row_start,
+                        const void* row_items, const uws_camera* cam, const float* medium,
+                        const uws_raster_out* fwd, const float* dL_dC, float* screen_grads,
+                        double* medium_acc, void* stream);
 
 /* ---- projection backward (replaces backward._project_backward :184-258 and
  *      _quat_backward :166-181).  grads: float32 flat buffer laid out as

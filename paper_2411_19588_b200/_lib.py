@@ -45,6 +45,7 @@ class RasterOutC(ctypes.Structure):
 
 class AdamParamsC(ctypes.Structure):
     _fields_ = [("lr", c_double * 8), ("bias1", c_double * 8), ("bias2", c_double * 8),
+                ("inv_bias1", c_double * 8), ("inv_bias2", c_double * 8),
                 ("beta1", c_double), ("beta2", c_double), ("one_minus_beta1", c_double),
                 ("one_minus_beta2", c_double), ("eps", c_double)]
 
@@ -63,8 +64,13 @@ _SIGS = {
     "uws_bin_emit": (c_int, [POINTER(ProjectedC), c_int64, c_int64, c_int64, POINTER(CameraC),
                              c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p,
                              c_size_t, c_void_p, c_size_t, c_void_p]),
+    "uws_bin_rows": (c_int, [POINTER(ProjectedC), c_int64, c_int64, POINTER(CameraC), c_void_p,
+                             c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_size_t,
+                             c_void_p]),
     "uws_raster_fwd": (c_int, [POINTER(ProjectedC), c_void_p, c_void_p, POINTER(CameraC),
                                c_void_p, POINTER(RasterOutC), c_void_p]),
+    "uws_raster_fwd_rows": (c_int, [POINTER(ProjectedC), c_void_p, c_void_p, POINTER(CameraC),
+                                    c_void_p, POINTER(RasterOutC), c_void_p]),
     "uws_loss_workspace_size": (c_int, [c_int32, c_int32, c_int32, POINTER(c_size_t)]),
     "uws_loss_fwd_bwd": (c_int, [c_void_p, c_void_p, c_int32, c_int32, c_int32, c_void_p,
                                  c_int32, c_double, c_double, c_void_p, c_void_p, c_void_p,
@@ -72,6 +78,9 @@ _SIGS = {
     "uws_raster_bwd": (c_int, [POINTER(ProjectedC), c_void_p, c_void_p, POINTER(CameraC),
                                c_void_p, POINTER(RasterOutC), c_void_p, c_void_p, c_void_p,
                                c_void_p]),
+    "uws_raster_bwd_rows": (c_int, [POINTER(ProjectedC), c_void_p, c_void_p, POINTER(CameraC),
+                                    c_void_p, POINTER(RasterOutC), c_void_p, c_void_p, c_void_p,
+                                    c_void_p]),
     "uws_preprocess_bwd": (c_int, [POINTER(CloudC), POINTER(CameraC), POINTER(ProjectedC),
                                    c_int64, c_void_p, c_void_p, c_void_p, c_int32, c_double,
                                    c_void_p, c_void_p, c_void_p]),

@@ -21,6 +21,7 @@
 #include <cstdlib>
 
 #include "raster_common.cuh"
+#include "row_filter.cuh"
 
 namespace uws {
 namespace {
@@ -31,8 +32,10 @@ constexpr float kLn2 = 0.69314718055994531f;
 struct BwdArgs {
     const uws_splat* splat;
     const double* exact;
-    const int32_t* offsets;
+    const int32_t* offsets;      // tile lists (full binning) ...
     const int32_t* entries;
+    const int32_t* row_start;    // ... or tile-row lists filtered on the fly
+    const uint2* row_items;
     int width, height, gx;
     const float* medium;
     const float* color_clean;
@@ -69,15 +72,20 @@ __device__ __forceinline__ float butterfly8(const float v[8], int lane) {
     return r;
 }
 
-template <int kPix>
-__global__ void __launch_bounds__(kRasterThreads / kPix, 3 * kPix) k_raster_bwd(BwdArgs a) {
+constexpr int kMaxMarks = 128;  // recorded batch starts per tile (row-list source)
+
+template <int kPix, bool ROWS>
+__global__ void __launch_bounds__(kRasterThreads / kPix, kPix == 4 ? 10 : 3 * kPix) k_raster_bwd(BwdArgs a) {
     constexpr int kThreads = kRasterThreads / kPix;
     constexpr int kWarps = kThreads / 32;
     constexpr int kRowStep = kTile / kPix;
+    __shared__ int sRow[ROWS ? kBatch : 1];  // (filter writes only positions < nb <= kBatch)
+    __shared__ int sMarkCur[ROWS ? kMaxMarks : 1], sMarkSkip[ROWS ? kMaxMarks : 1];
+    __shared__ int sScan[kWarps];
     __shared__ StageA sA[kBatch];
     __shared__ StageB sB[kBatch];
     __shared__ StageC sC[kBatch];
-    __shared__ float sAcc[9][kBatch];
+    __shared__ float sAcc[9][kBatch + 1];  // +1: the 8 reducing lanes hit distinct banks
     __shared__ float sMed[kWarps][9];
     __shared__ int sMaxLast;
 
@@ -87,11 +95,10 @@ __global__ void __launch_bounds__(kRasterThreads / kPix, 3 * kPix) k_raster_bwd(
     const int lx = threadIdx.x & (kTile - 1), ly0 = threadIdx.x / kTile;
     const float fx = (float)lx + 0.5f;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    const int start = a.offsets[tile], end = a.offsets[tile + 1];
-    (void)end;
+    const int start = ROWS ? 0 : a.offsets[tile];
 
     if (threadIdx.x == 0) sMaxLast = 0;
-    for (int i = threadIdx.x; i < 9 * kBatch; i += kThreads) (&sAcc[0][0])[i] = 0.f;
+    for (int i = threadIdx.x; i < 9 * (kBatch + 1); i += kThreads) (&sAcc[0][0])[i] = 0.f;
 
     float G[kPix][3], T[kPix], S[kPix], fy[kPix];
     int mylast[kPix];
@@ -150,18 +157,66 @@ __global__ void __launch_bounds__(kRasterThreads / kPix, 3 * kPix) k_raster_bwd(
     __syncthreads();
     const int maxlast = sMaxLast;
 
-    for (int bend = start + maxlast; bend > start; bend -= kBatch) {
-        const int bstart = max(start, bend - kBatch);
-        const int nb = bend - bstart;
+    const int nbatch = (maxlast + kBatch - 1) / kBatch;
+    int rend = 0, stride = 1;
+    if (ROWS && nbatch > 0) {
+        // pass 1 over the row list: where does each batch of 256 tile entries start?
+        const int rs = a.row_start[ty];
+        rend = a.row_start[ty + 1];
+        stride = (nbatch + kMaxMarks - 1) / kMaxMarks;
+        int cnt = 0, cur = rs, b = 0;
+        if (nbatch == 1) {  // the common case: the whole prefix is one batch from the start
+            if (threadIdx.x == 0) {
+                sMarkCur[0] = rs;
+                sMarkSkip[0] = 0;
+            }
+            cnt = maxlast;
+        }
+        while (cnt < maxlast && cur < rend) {
+            const int t = filter_chunk<kThreads>(a.row_items, cur, rend, tx, nullptr, 0, 0,
+                                                 sScan);
+            while (b < nbatch && b * kBatch < cnt + t) {
+                if (threadIdx.x == 0) {
+                    sMarkCur[b / stride] = cur;
+                    sMarkSkip[b / stride] = b * kBatch - cnt;
+                }
+                b += stride;
+            }
+            cnt += t;
+            cur += kChunk;
+        }
         __syncthreads();
+    }
+
+    for (int bi = nbatch - 1; bi >= 0; --bi) {
+        const int lo = bi * kBatch;
+        const int nb = min(kBatch, maxlast - lo);
+        __syncthreads();
+        if (ROWS) {
+            // pass 2: re-collect this batch's rows from its recorded start
+            const int mk = bi / stride;
+            int cur = sMarkCur[mk];
+            int got = -(sMarkSkip[mk] + (bi - mk * stride) * kBatch);
+            while (got < nb) {
+                got += filter_chunk<kThreads>(a.row_items, cur, rend, tx, sRow, got, nb,
+                                              sScan);
+                cur += kChunk;
+            }
 #pragma unroll
-        for (int s = 0; s < kBatch / kThreads; ++s) {
-            const int i = threadIdx.x + s * kThreads;
-            if (i < nb) stage_entry(a.splat, a.entries[bstart + i], ox, oy, sA[i], sB[i], sC[i]);
+            for (int s = 0; s < kBatch / kThreads; ++s) {
+                const int i = threadIdx.x + s * kThreads;
+                if (i < nb) stage_entry(a.splat, sRow[i], ox, oy, sA[i], sB[i], sC[i]);
+            }
+        } else {
+#pragma unroll
+            for (int s = 0; s < kBatch / kThreads; ++s) {
+                const int i = threadIdx.x + s * kThreads;
+                if (i < nb) stage_entry(a.splat, a.entries[start + lo + i], ox, oy, sA[i], sB[i], sC[i]);
+            }
         }
         __syncthreads();
         for (int k = nb - 1; k >= 0; --k) {
-            const int jrel = bstart - start + k;
+            const int jrel = lo + k;
             float v[9];
 #pragma unroll
             for (int i = 0; i < 9; ++i) v[i] = 0.f;
@@ -285,11 +340,47 @@ extern "C" int uws_raster_bwd(const uws_projected* proj, const int32_t* offsets,
     a.screen = screen_grads;
     a.medium_acc = medium_acc;
     cudaStream_t st = as_stream(stream);
+    a.row_start = nullptr;
+    a.row_items = nullptr;
     switch (bwd_pix()) {
-        case 2: k_raster_bwd<2><<<a.gx * gy, kRasterThreads / 2, 0, st>>>(a); break;
-        case 8: k_raster_bwd<8><<<a.gx * gy, kRasterThreads / 8, 0, st>>>(a); break;
-        default: k_raster_bwd<4><<<a.gx * gy, kRasterThreads / 4, 0, st>>>(a); break;
+        case 2: k_raster_bwd<2, false><<<a.gx * gy, kRasterThreads / 2, 0, st>>>(a); break;
+        case 8: k_raster_bwd<8, false><<<a.gx * gy, kRasterThreads / 8, 0, st>>>(a); break;
+        default: k_raster_bwd<4, false><<<a.gx * gy, kRasterThreads / 4, 0, st>>>(a); break;
     }
     UWS_CHECK_LAUNCH("k_raster_bwd");
+    return UWS_OK;
+}
+
+extern "C" int uws_raster_bwd_rows(const uws_projected* proj, const int32_t* row_start,
+                                   const void* row_items, const uws_camera* cam,
+                                   const float* medium, const uws_raster_out* fwd,
+                                   const float* dL_dC, float* screen_grads, double* medium_acc,
+                                   void* stream) {
+    UWS_REQUIRE(proj && row_start && cam && fwd && dL_dC && screen_grads,
+                "uws_raster_bwd_rows: null argument");
+    UWS_REQUIRE(fwd->final_T && fwd->last, "uws_raster_bwd_rows: forward context missing");
+    UWS_REQUIRE(medium == nullptr || (fwd->color_clean && fwd->depth && medium_acc),
+                "uws_raster_bwd_rows: underwater backward needs color_clean, depth and medium_acc");
+    BwdArgs a;
+    a.splat = proj->splat;
+    a.exact = proj->exact;
+    a.offsets = nullptr;
+    a.entries = nullptr;
+    a.row_start = row_start;
+    a.row_items = (const uint2*)row_items;
+    a.width = cam->width;
+    a.height = cam->height;
+    a.gx = (int)ceil_div(cam->width, kTile);
+    const int gy = (int)ceil_div(cam->height, kTile);
+    a.medium = medium;
+    a.color_clean = fwd->color_clean;
+    a.depth = fwd->depth;
+    a.final_T = fwd->final_T;
+    a.last = fwd->last;
+    a.dL = dL_dC;
+    a.screen = screen_grads;
+    a.medium_acc = medium_acc;
+    k_raster_bwd<4, true><<<a.gx * gy, kRasterThreads / 4, 0, as_stream(stream)>>>(a);
+    UWS_CHECK_LAUNCH("k_raster_bwd_rows");
     return UWS_OK;
 }

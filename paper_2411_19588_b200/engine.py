@@ -8,15 +8,18 @@ buffers for a fixed cloud size and image size, passes counts between kernels
 in device memory, and sizes the tile lists with a capacity.  A step is a
 fixed sequence of asynchronous launches --
 
-    per view:  preprocess -> depth sort + tile-row counts -> tile lists
-               -> forward compositing -> L1/D-SSIM loss -> backward
-               compositing -> projection backward (accumulating)
+    per view:  preprocess -> depth sort + tile-row counts -> tile-row
+               lists -> forward compositing (each tile filters its row list
+               on the fly and stops at saturation: the E-entry tile lists of
+               bin_and_sort are never materialised) -> L1/D-SSIM loss ->
+               backward compositing (re-derives the same consumed prefix)
+               -> projection backward (accumulating)
     then:      [NCCL all-reduce of the flat gradient buffer]
                -> fused Adam (skips itself on non-finite / overflow,
                   accumulates the densification statistics, zeroes grads)
 
 -- followed by ONE small device-to-host read (loss values, flags, list
-sizes).  If a view's tile lists did not fit their capacity the kernels turn
+sizes).  If a view's row lists did not fit their capacity the kernels turn
 the whole step into a no-op on the device (Adam skipped); the engine grows
 the buffers to the reported sizes and runs the step again.  This is the
 loop body of pipeline.train (reference pipeline.py:170-193).
@@ -36,7 +39,7 @@ from .backward import GradientBuffer
 from .losses import total_loss_device
 from .optim import OptimConfig, apply_gradients_device, rollback_steps
 from .projection import ProjectedCloud, preprocess_into
-from .rasterizer import RenderOutput, TileBins, _alloc_output
+from .rasterizer import RenderOutput, _alloc_output
 from .scene import Camera, TrainState
 
 log = logging.getLogger(__name__)
@@ -88,8 +91,8 @@ class StepEngine:
         _lib.call("uws_bin_workspace_size", n, 0, self.gx, self.gy, ctypes.byref(cb),
                   ctypes.byref(eb))
         self.count_ws = torch.empty(max(cb.value, 1), dtype=torch.uint8, device=dev)
-        self.offsets = torch.zeros(self.gx * self.gy + 1, dtype=torch.int32, device=dev)
-        self._set_capacity(entry_capacity or 48 * n, (entry_capacity or 48 * n) // 4)
+        self.row_start = torch.zeros(self.gy + 1, dtype=torch.int32, device=dev)
+        self._set_capacity(entry_capacity or 12 * n)
         self.out = _alloc_output(height, width, dev, "underwater", False)
         self.dL = torch.empty(height, width, 3, dtype=torch.float32, device=dev)
         _lib.call("uws_loss_workspace_size", height, width, 3, ctypes.byref(b))
@@ -101,17 +104,15 @@ class StepEngine:
         self.stats_host = torch.zeros_like(self.stats, device="cpu").pin_memory()
 
     # -- capacity management ---------------------------------------------------
-    def _set_capacity(self, e_cap: int, s_cap: int):
-        self.e_cap = int(e_cap)
+    def _set_capacity(self, s_cap: int):
+        """Capacity of the tile-row lists (S = sum over visible Gaussians of
+        the tile rows their rectangle spans)."""
         self.s_cap = int(max(s_cap, 1))
-        self.entries = torch.empty(max(self.e_cap, 1), dtype=torch.int32, device=self.dev)
-        cb, eb = _lib.size_out(), _lib.size_out()
-        _lib.call("uws_bin_workspace_size", self.n, self.s_cap, self.gx, self.gy, ctypes.byref(cb),
-                  ctypes.byref(eb))
-        self.emit_ws = torch.empty(max(eb.value, 1), dtype=torch.uint8, device=self.dev)
+        # 8-byte items: row index, tile-column span x0 | x1 << 16
+        self.row_items = torch.empty(self.s_cap, 2, dtype=torch.int32, device=self.dev)
 
-    # -- one view: forward + loss + backward into self.grads -----------------------
-    def _view(self, cam: Camera, gt: torch.Tensor, slot: int):
+    # -- forward of one view (render path) ----------------------------------------
+    def _forward(self, cam: Camera, slot: int, mode: str = "underwater", train: bool = True):
         st = _lib.stream_handle()
         cloud, medium = self.state.cloud, self.state.medium
         cc = cam.c_struct()
@@ -122,21 +123,43 @@ class StepEngine:
         ovf = rec[_ST_OVF:_ST_OVF + 1].view(torch.int32)[:1]
         _lib.call("uws_bin_count", ctypes.byref(pc), self.n, ctypes.byref(cc), _lib.ptr(totals),
                   _lib.ptr(self.count_ws), self.count_ws.numel(), st)
-        _lib.call("uws_bin_emit", ctypes.byref(pc), self.n, self.e_cap, self.s_cap,
-                  ctypes.byref(cc), _lib.ptr(totals), _lib.ptr(self.offsets),
-                  _lib.ptr(self.entries), _lib.ptr(ovf), _lib.ptr(self.grads.nonfinite),
-                  _lib.ptr(self.count_ws), self.count_ws.numel(), _lib.ptr(self.emit_ws),
-                  self.emit_ws.numel(), st)
+        _lib.call("uws_bin_rows", ctypes.byref(pc), self.n, self.s_cap, ctypes.byref(cc),
+                  _lib.ptr(totals), _lib.ptr(self.row_start), _lib.ptr(self.row_items),
+                  _lib.ptr(ovf), _lib.ptr(self.grads.nonfinite) if train else 0,
+                  _lib.ptr(self.count_ws), self.count_ws.numel(), st)
         out = self.out
         oc = out.c_struct()
-        _lib.call("uws_raster_fwd", ctypes.byref(pc), _lib.ptr(self.offsets),
-                  _lib.ptr(self.entries), ctypes.byref(cc), _lib.ptr(medium.flat),
-                  ctypes.byref(oc), st)
+        med = _lib.ptr(medium.flat) if mode == "underwater" else 0
+        _lib.call("uws_raster_fwd_rows", ctypes.byref(pc), _lib.ptr(self.row_start),
+                  _lib.ptr(self.row_items), ctypes.byref(cc), med, ctypes.byref(oc), st)
+        return cc, pc, oc, rec
+
+    def render(self, cam, mode: str = "underwater") -> RenderOutput:
+        """Render-only path (no host sync before the caller reads the image).
+        Overflow of the row-list capacity is detected and the view re-run."""
+        cam = Camera.from_any(cam)
+        for _ in range(4):
+            self.stats.zero_()
+            self._forward(cam, 0, mode, train=False)
+            rec = self.stats[0:_ST_SIZE]
+            if int(rec[_ST_OVF:_ST_OVF + 1].view(torch.int32)[0]) == 0:
+                break
+            need_s = int(rec[_ST_TOTALS:_ST_TOTALS + 2].view(torch.int64)[1])
+            self._set_capacity(int(need_s * 1.25) + 1024)
+        self.out.mode = mode
+        return self.last_render()
+
+    # -- one view: forward + loss + backward into self.grads -----------------------
+    def _view(self, cam: Camera, gt: torch.Tensor, slot: int):
+        st = _lib.stream_handle()
+        cloud, medium = self.state.cloud, self.state.medium
+        cc, pc, oc, rec = self._forward(cam, slot)
+        out = self.out
         total_loss_device(out.color, gt, medium, self.cfg.lambda_ssim, self.cfg.lambda_guide,
                           result=rec[_ST_LOSS:_ST_LOSS + 6], grad=self.dL, workspace=self.loss_ws,
                           nonfinite=self.grads.nonfinite)
-        _lib.call("uws_raster_bwd", ctypes.byref(pc), _lib.ptr(self.offsets),
-                  _lib.ptr(self.entries), ctypes.byref(cc), _lib.ptr(medium.flat),
+        _lib.call("uws_raster_bwd_rows", ctypes.byref(pc), _lib.ptr(self.row_start),
+                  _lib.ptr(self.row_items), ctypes.byref(cc), _lib.ptr(medium.flat),
                   ctypes.byref(oc), _lib.ptr(self.dL), _lib.ptr(self.screen),
                   _lib.ptr(self.med_acc), st)
         cl = cloud.c_struct()
@@ -147,10 +170,11 @@ class StepEngine:
                   _lib.ptr(self.grads.nonfinite), st)
 
     def last_render(self) -> RenderOutput:
-        """Forward buffers of the most recent view (valid until the next step)."""
+        """Forward buffers of the most recent view (valid until the next step).
+        ``bins`` is None: the engine never materialises full tile lists."""
         out = self.out
         out.proj = self.proj
-        out.bins = TileBins(self.gx, self.gy, self.offsets, self.entries)
+        out.bins = None
         return out
 
     def _launch(self, views: Sequence):
@@ -181,14 +205,14 @@ class StepEngine:
             need_e = need_s = 0
             for i in range(nv):
                 tot = s[i * _ST_SIZE + _ST_TOTALS:i * _ST_SIZE + _ST_TOTALS + 2].view(torch.int64)
-                need_e = max(need_e, int(tot[0]))
-                need_s = max(need_s, int(tot[1]))
+                need_e = max(need_e, int(tot[0]))   # tile entries (reported only)
+                need_s = max(need_s, int(tot[1]))   # row-list items (capacity)
             if skipped:
                 rollback_steps(self.state)
             if skip_count >= 65536.0 and reruns < 3:
                 # some rank's tile lists overflowed: every rank re-runs the step
-                if need_e > self.e_cap or need_s > self.s_cap:
-                    self._set_capacity(int(need_e * 1.25) + 1024, int(need_s * 1.25) + 1024)
+                if need_s > self.s_cap:
+                    self._set_capacity(int(need_s * 1.25) + 1024)
                 reruns += 1
                 continue
             break

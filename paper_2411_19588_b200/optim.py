@@ -112,6 +112,8 @@ def adam_hparams(state: TrainState, cfg: OptimConfig, spatial_scale: float = 1.0
         hp.lr[j] = lr
         hp.bias1[j] = 1 - BETA1 ** step
         hp.bias2[j] = 1 - BETA2 ** step
+        hp.inv_bias1[j] = 1.0 / hp.bias1[j]
+        hp.inv_bias2[j] = 1.0 / hp.bias2[j]
     hp.beta1, hp.beta2 = BETA1, BETA2
     hp.one_minus_beta1, hp.one_minus_beta2 = 1 - BETA1, 1 - BETA2
     hp.eps = EPS

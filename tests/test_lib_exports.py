@@ -61,4 +61,4 @@ def test_struct_layouts_match_header():
     assert ctypes.sizeof(_lib.CloudC) == 6 * 8
     assert ctypes.sizeof(_lib.ProjectedC) == 8 * 8
     assert ctypes.sizeof(_lib.RasterOutC) == 9 * 8
-    assert ctypes.sizeof(_lib.AdamParamsC) == 29 * 8
+    assert ctypes.sizeof(_lib.AdamParamsC) == 45 * 8
