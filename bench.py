@@ -20,6 +20,7 @@ same workload, extrapolated to a full step.
 from __future__ import annotations
 
 import argparse
+import glob
 import json
 import os
 import statistics
@@ -64,6 +65,26 @@ def view_eye(rank):
 
 def gt_image(seed=0):
     return np.random.default_rng(seed).uniform(0, 1, (H, W, 3)).astype(np.float32)
+
+
+def kernel_traffic(stage):
+    """DRAM bytes (read + write) per launch of the stage's dominant kernel, from the committed
+    `ncu --set full` capture summary under profiles/ (None when no capture is on file)."""
+    kern = {"uws_raster_bwd": "k_raster_bwd", "uws_raster_fwd": "k_raster_fwd",
+            "uws_preprocess_fwd": "k_preprocess", "uws_preprocess_bwd": "k_preprocess_bwd",
+            "uws_adam_step": "k_adam_cloud", "uws_loss_fwd_bwd": "k_ssim"}.get(stage)
+    if kern is None:
+        return None
+    caps = sorted(glob.glob(os.path.join(ROOT, "profiles", "r*", "kernel_traffic*.json")))
+    if not caps:
+        return None
+    try:
+        data = json.load(open(caps[-1]))
+    except (OSError, ValueError):
+        return None
+    tot = [v["dram_bytes"] for k, v in data.items()
+           if k.split("<")[0].split("::")[-1] == kern or (kern == "k_ssim" and "k_ssim" in k)]
+    return {"bytes": sum(tot), "source": os.path.relpath(caps[-1], ROOT)} if tot else None
 
 
 # ----------------------------------------------------------------------------
@@ -252,6 +273,7 @@ def run_gpu(args):
     m_tile = (offs[1:] - offs[:-1])[tid]
     p_pix = int(torch.where(term, last, m_tile).sum().item())
     per_step = {k: v / args.steps for k, v in stages.items()}
+    canon = {k: k.replace("_rows", "") for k in per_step}  # row-list variants: same work
     total_stage = sum(per_step.values())
     fwd_flops = 30.0 * p_pix
     bwd_flops = 60.0 * p_pix
@@ -270,38 +292,41 @@ def run_gpu(args):
         "uws_preprocess_fwd": 56 * N_GAUSS + 48 * k_vis,
         "uws_bin_count": 24 * k_vis,
         "uws_bin_emit": 20 * e_ent,
+        "uws_bin_rows": 24 * k_vis,
         "uws_loss_fwd_bwd": 36 * W * H,
         "uws_preprocess_bwd": 36 * k_vis + 112 * N_GAUSS,
         "uws_adam_step": 392 * N_GAUSS,
     }
     stage_roofline = {}
     for k, v in per_step.items():
-        if k in hbm_bytes and v > 0:
-            gbs = hbm_bytes[k] / (v / 1e3) / 1e9
+        if canon[k] in hbm_bytes and v > 0:
+            gbs = hbm_bytes[canon[k]] / (v / 1e3) / 1e9
             stage_roofline[k] = {"bound": "hbm", "achieved_gbs": round(gbs, 1),
                                  "frac": round(gbs / hbm_peak, 4), "ms": round(v, 4)}
-    for k, fl in (("uws_raster_fwd", fwd_flops), ("uws_raster_bwd", bwd_flops)):
-        if k in per_step and per_step[k] > 0:
+    for k in per_step:
+        fl = {"uws_raster_fwd": fwd_flops, "uws_raster_bwd": bwd_flops}.get(canon[k])
+        if fl is not None and per_step[k] > 0:
             tf = fl / (per_step[k] / 1e3) / 1e12
             stage_roofline[k] = {"bound": "fp32", "achieved_tflops": round(tf, 3),
                                  "frac": round(tf / fp32_peak, 4), "ms": round(per_step[k], 4)}
     dom = stage_roofline.get(dominant, {})
-    if dominant in ("uws_raster_fwd", "uws_raster_bwd"):
-        fl = bwd_flops if dominant == "uws_raster_bwd" else fwd_flops
+    traffic = kernel_traffic(canon.get(dominant))
+    if canon.get(dominant) in ("uws_raster_fwd", "uws_raster_bwd"):
+        fl = bwd_flops if canon[dominant] == "uws_raster_bwd" else fwd_flops
         achieved = fl / (per_step[dominant] / 1e3) / 1e12
         roofline = {"bound": "fp32", "kernel": dominant, "achieved": round(achieved, 3),
                     "peak": round(fp32_peak, 1), "unit": "TFLOP/s",
-                    "frac": round(achieved / fp32_peak, 4), "traffic": None,
+                    "frac": round(achieved / fp32_peak, 4), "traffic": traffic,
                     "peak_source": "nominal FP32 non-tensor 148 SM x 128 lanes x 2 x 1.965 GHz "
                                    "(no FP32 figure in MEASURED_PEAKS.json; no tensor cores on "
                                    "this path)",
                     "work": f"{fl / 1e9:.2f} GFLOP per launch (SURVEY 8d: "
-                            f"{'60' if dominant.endswith('bwd') else '30'} flop x P_pix={p_pix})"}
-    elif dominant in hbm_bytes:
-        gbs = hbm_bytes[dominant] / (per_step[dominant] / 1e3) / 1e9
+                            f"{'60' if canon[dominant].endswith('bwd') else '30'} flop x P_pix={p_pix})"}
+    elif canon.get(dominant) in hbm_bytes:
+        gbs = hbm_bytes[canon[dominant]] / (per_step[dominant] / 1e3) / 1e9
         roofline = {"bound": "hbm", "kernel": dominant, "achieved": round(gbs, 1),
                     "peak": hbm_peak, "unit": "GB/s", "frac": round(gbs / hbm_peak, 4),
-                    "traffic": None}
+                    "traffic": traffic}
     else:
         roofline = {"bound": "hbm", "kernel": dominant, "achieved": None, "peak": hbm_peak,
                     "unit": "GB/s", "frac": None, "traffic": None}

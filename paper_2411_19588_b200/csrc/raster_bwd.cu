@@ -18,16 +18,18 @@
 // (14 shuffles instead of 45), accumulated over the CTA's warps in shared
 // memory, chained through the conic once per (tile, Gaussian) and only then
 // sent to HBM with 9 atomics.
-#include <cstdlib>
-
 #include "raster_common.cuh"
 #include "row_filter.cuh"
 
 namespace uws {
 namespace {
 
-constexpr int kBatch = 256;
+constexpr int kBatch = 128;
 constexpr float kLn2 = 0.69314718055994531f;
+constexpr int kPix = 4;                          // pixels per thread
+constexpr int kThreads = kRasterThreads / kPix;  // 64
+constexpr int kWarps = kThreads / 32;            // 2
+constexpr int kBandRows = kTile / kWarps;        // each warp owns an 8-row band of the tile
 
 struct BwdArgs {
     const uws_splat* splat;
@@ -74,31 +76,33 @@ __device__ __forceinline__ float butterfly8(const float v[8], int lane) {
 
 constexpr int kMaxMarks = 128;  // recorded batch starts per tile (row-list source)
 
-template <int kPix, bool ROWS>
-__global__ void __launch_bounds__(kRasterThreads / kPix, kPix == 4 ? 10 : 3 * kPix) k_raster_bwd(BwdArgs a) {
-    constexpr int kThreads = kRasterThreads / kPix;
-    constexpr int kWarps = kThreads / 32;
-    constexpr int kRowStep = kTile / kPix;
+template <bool ROWS>
+__global__ void __launch_bounds__(kThreads, 10) k_raster_bwd(BwdArgs a) {
     __shared__ int sRow[ROWS ? kBatch : 1];  // (filter writes only positions < nb <= kBatch)
     __shared__ int sMarkCur[ROWS ? kMaxMarks : 1], sMarkSkip[ROWS ? kMaxMarks : 1];
     __shared__ int sScan[kWarps];
     __shared__ StageA sA[kBatch];
     __shared__ StageB sB[kBatch];
     __shared__ StageC sC[kBatch];
-    __shared__ float sAcc[9][kBatch + 1];  // +1: the 8 reducing lanes hit distinct banks
+    __shared__ float4 sD[kBatch];                  // pre-filter box (stage_extent)
+    __shared__ float sAcc[kWarps][9][kBatch + 1];  // per-warp partials; +1: the 8 storing lanes hit distinct banks
+    __shared__ int sHit[kWarps][kBatch];           // sAcc[w][.][k] valid
     __shared__ float sMed[kWarps][9];
     __shared__ int sMaxLast;
 
     const int tile = blockIdx.x;
     const int ty = tile / a.gx, tx = tile - ty * a.gx;
     const int ox = tx * kTile, oy = ty * kTile;
-    const int lx = threadIdx.x & (kTile - 1), ly0 = threadIdx.x / kTile;
-    const float fx = (float)lx + 0.5f;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int lx = lane & (kTile - 1);
+    const int ly0 = warp * kBandRows + (lane >> 4);  // pixel p sits on row ly0 + 2p
+    const float fx = (float)lx + 0.5f;
+    const float band_lo = (float)(warp * kBandRows) + 0.5f;
+    const float band_hi = band_lo + (float)(kBandRows - 1);
     const int start = ROWS ? 0 : a.offsets[tile];
 
     if (threadIdx.x == 0) sMaxLast = 0;
-    for (int i = threadIdx.x; i < 9 * (kBatch + 1); i += kThreads) (&sAcc[0][0])[i] = 0.f;
+    for (int i = threadIdx.x; i < kWarps * kBatch; i += kThreads) (&sHit[0][0])[i] = 0;
 
     float G[kPix][3], T[kPix], S[kPix], fy[kPix];
     int mylast[kPix];
@@ -108,7 +112,7 @@ __global__ void __launch_bounds__(kRasterThreads / kPix, kPix == 4 ? 10 : 3 * kP
     int maxl = 0;
 #pragma unroll
     for (int p = 0; p < kPix; ++p) {
-        const int ly = ly0 + p * kRowStep;
+        const int ly = ly0 + 2 * p;
         fy[p] = (float)ly + 0.5f;
         S[p] = 0.f;
         T[p] = 1.f;
@@ -146,8 +150,9 @@ __global__ void __launch_bounds__(kRasterThreads / kPix, kPix == 4 ? 10 : 3 * kP
             if (lane == 0) sMed[warp][v] = s;
         }
     }
+    const int wmax = __reduce_max_sync(0xffffffffu, maxl);  // this warp's consumed prefix
     __syncthreads();
-    if (maxl > 0) atomicMax(&sMaxLast, maxl);
+    if (lane == 0 && wmax > 0) atomicMax(&sMaxLast, wmax);
     if (a.medium && threadIdx.x < 9) {
         float s = 0.f;
 #pragma unroll
@@ -160,7 +165,7 @@ __global__ void __launch_bounds__(kRasterThreads / kPix, kPix == 4 ? 10 : 3 * kP
     const int nbatch = (maxlast + kBatch - 1) / kBatch;
     int rend = 0, stride = 1;
     if (ROWS && nbatch > 0) {
-        // pass 1 over the row list: where does each batch of 256 tile entries start?
+        // pass 1 over the row list: where does each batch of tile entries start?
         const int rs = a.row_start[ty];
         rend = a.row_start[ty + 1];
         stride = (nbatch + kMaxMarks - 1) / kMaxMarks;
@@ -202,82 +207,96 @@ __global__ void __launch_bounds__(kRasterThreads / kPix, kPix == 4 ? 10 : 3 * kP
                                               sScan);
                 cur += kChunk;
             }
+        }
 #pragma unroll
-            for (int s = 0; s < kBatch / kThreads; ++s) {
-                const int i = threadIdx.x + s * kThreads;
-                if (i < nb) stage_entry(a.splat, sRow[i], ox, oy, sA[i], sB[i], sC[i]);
-            }
-        } else {
-#pragma unroll
-            for (int s = 0; s < kBatch / kThreads; ++s) {
-                const int i = threadIdx.x + s * kThreads;
-                if (i < nb) stage_entry(a.splat, a.entries[start + lo + i], ox, oy, sA[i], sB[i], sC[i]);
+        for (int s = 0; s < kBatch / kThreads; ++s) {
+            const int i = threadIdx.x + s * kThreads;
+            if (i < nb) {
+                stage_entry(a.splat, ROWS ? sRow[i] : a.entries[start + lo + i], ox, oy, sA[i],
+                            sB[i], sC[i]);
+                sD[i] = stage_extent(sA[i], sB[i]);
             }
         }
         __syncthreads();
-        for (int k = nb - 1; k >= 0; --k) {
+        // back to front over the entries this warp's pixels consumed
+        for (int k = min(nb, wmax - lo) - 1; k >= 0; --k) {
+            const float4 D = sD[k];
+            if (D.y < band_lo || D.x > band_hi) continue;  // misses this warp's band (uniform)
             const int jrel = lo + k;
             float v[9];
 #pragma unroll
             for (int i = 0; i < 9; ++i) v[i] = 0.f;
             bool hit = false;
-            const StageA A = sA[k];
-            const StageB B = sB[k];
-            const float dx = fx - A.mx;
-            const float tA = A.A * dx;
+            if (fx >= D.z && fx <= D.w) {  // column inside the box
+                const StageA A = sA[k];
+                const StageB B = sB[k];
+                const float dx = fx - A.mx;
+                const float tA = A.A * dx;
 #pragma unroll
-            for (int p = 0; p < kPix; ++p) {
-                if (jrel >= mylast[p]) continue;
-                const float dy = fy[p] - A.my;
-                const float power = dx * fmaf(A.B, dy, tA) + B.C * dy * dy;
-                if (power < B.skip) continue;
-                const float araw = B.op * ex2_ftz(power);
-                const int py = oy + ly0 + p * kRowStep;
-                if (araw < kFloorHi && !floor_pass(araw, a.splat, a.exact, sC[k].row, ox + lx, py))
-                    continue;
-                hit = true;
-                const float alpha = fminf(araw, kClampF);
-                const float inv_om = __frcp_rn(1.0f - alpha);
-                const float Ti = T[p] * inv_om;
-                const float w = alpha * Ti;
-                const StageC& C = sC[k];
-                const float U = G[p][0] * C.r + G[p][1] * C.g + G[p][2] * C.b;
-                const float dalpha = U * Ti - S[p] * inv_om;
-                S[p] = fmaf(w, U, S[p]);
-                T[p] = Ti;
-                const float dp = (araw < kClampLo || below_clamp(araw, a.splat, a.exact, C.row,
-                                                                 ox + lx, py))
-                                     ? dalpha * araw
-                                     : 0.f;
-                const float dpx = dp * dx, dpy = dp * dy;
-                v[0] += dp;
-                v[1] += dpx;
-                v[2] += dpy;
-                v[3] = fmaf(dpx, dx, v[3]);
-                v[4] = fmaf(dpx, dy, v[4]);
-                v[5] = fmaf(dpy, dy, v[5]);
-                v[6] = fmaf(w, G[p][0], v[6]);
-                v[7] = fmaf(w, G[p][1], v[7]);
-                v[8] = fmaf(w, G[p][2], v[8]);
+                for (int p = 0; p < kPix; ++p) {
+                    if (jrel >= mylast[p]) continue;
+                    const float dy = fy[p] - A.my;
+                    const float power = dx * fmaf(A.B, dy, tA) + B.C * dy * dy;
+                    if (power < B.skip) continue;
+                    const float araw = B.op * ex2_ftz(power);
+                    if (araw < kFloorLo) continue;
+                    bool unclamped = araw < kClampLo;
+                    if (araw < kFloorHi || (!unclamped && araw < kClampHi)) {
+                        // guard band: re-decide both gates from the float64 record
+                        const double e = alpha_raw_f64_cold(a.splat, a.exact, sC[k].row, ox + lx,
+                                                            oy + ly0 + 2 * p);
+                        if (!(e >= kFloor)) continue;
+                        unclamped = e < kClamp;
+                    }
+                    hit = true;
+                    const float alpha = fminf(araw, kClampF);
+                    const float inv_om = rcp_ftz(1.0f - alpha);
+                    const float Ti = T[p] * inv_om;
+                    const float w = alpha * Ti;
+                    const StageC& C = sC[k];
+                    const float U = G[p][0] * C.r + G[p][1] * C.g + G[p][2] * C.b;
+                    const float dalpha = U * Ti - S[p] * inv_om;
+                    S[p] = fmaf(w, U, S[p]);
+                    T[p] = Ti;
+                    const float dp = unclamped ? dalpha * araw : 0.f;
+                    const float dpx = dp * dx, dpy = dp * dy;
+                    v[0] += dp;
+                    v[1] += dpx;
+                    v[2] += dpy;
+                    v[3] = fmaf(dpx, dx, v[3]);
+                    v[4] = fmaf(dpx, dy, v[4]);
+                    v[5] = fmaf(dpy, dy, v[5]);
+                    v[6] = fmaf(w, G[p][0], v[6]);
+                    v[7] = fmaf(w, G[p][1], v[7]);
+                    v[8] = fmaf(w, G[p][2], v[8]);
+                }
             }
             if (!__any_sync(0xffffffffu, hit)) continue;
             const float r8 = butterfly8(v, lane);
             const float r9 = warp_sum(v[8]);
             if ((lane & 3) == 0) {
                 const int idx = ((lane >> 4) & 1) * 4 + ((lane >> 3) & 1) * 2 + ((lane >> 2) & 1);
-                atomicAdd(&sAcc[idx][k], r8);
+                sAcc[warp][idx][k] = r8;
             }
-            if (lane == 0) atomicAdd(&sAcc[8][k], r9);
+            if (lane == 0) {
+                sAcc[warp][8][k] = r9;
+                sHit[warp][k] = 1;
+            }
         }
         __syncthreads();
         for (int k = threadIdx.x; k < nb; k += kThreads) {
             float s[9];
+#pragma unroll
+            for (int i = 0; i < 9; ++i) s[i] = 0.f;
             bool any = false;
 #pragma unroll
-            for (int i = 0; i < 9; ++i) {
-                s[i] = sAcc[i][k];
-                sAcc[i][k] = 0.f;
-                any |= s[i] != 0.f;
+            for (int w = 0; w < kWarps; ++w) {  // fixed order: deterministic per tile
+                if (sHit[w][k]) {
+                    any = true;
+                    sHit[w][k] = 0;
+#pragma unroll
+                    for (int i = 0; i < 9; ++i) s[i] += sAcc[w][i][k];
+                }
             }
             if (any) {
                 // natural-units conic from the log2-scaled staged values
@@ -297,15 +316,6 @@ __global__ void __launch_bounds__(kRasterThreads / kPix, kPix == 4 ? 10 : 3 * kP
             }
         }
     }
-}
-
-int bwd_pix() {
-    static int pix = [] {
-        const char* e = getenv("UWS_BWD_PIX");
-        int v = e ? atoi(e) : 4;
-        return (v == 2 || v == 8) ? v : 4;
-    }();
-    return pix;
 }
 
 }  // namespace
@@ -339,14 +349,9 @@ extern "C" int uws_raster_bwd(const uws_projected* proj, const int32_t* offsets,
     a.dL = dL_dC;
     a.screen = screen_grads;
     a.medium_acc = medium_acc;
-    cudaStream_t st = as_stream(stream);
     a.row_start = nullptr;
     a.row_items = nullptr;
-    switch (bwd_pix()) {
-        case 2: k_raster_bwd<2, false><<<a.gx * gy, kRasterThreads / 2, 0, st>>>(a); break;
-        case 8: k_raster_bwd<8, false><<<a.gx * gy, kRasterThreads / 8, 0, st>>>(a); break;
-        default: k_raster_bwd<4, false><<<a.gx * gy, kRasterThreads / 4, 0, st>>>(a); break;
-    }
+    k_raster_bwd<false><<<a.gx * gy, kThreads, 0, as_stream(stream)>>>(a);
     UWS_CHECK_LAUNCH("k_raster_bwd");
     return UWS_OK;
 }
@@ -380,7 +385,7 @@ extern "C" int uws_raster_bwd_rows(const uws_projected* proj, const int32_t* row
     a.dL = dL_dC;
     a.screen = screen_grads;
     a.medium_acc = medium_acc;
-    k_raster_bwd<4, true><<<a.gx * gy, kRasterThreads / 4, 0, as_stream(stream)>>>(a);
+    k_raster_bwd<true><<<a.gx * gy, kThreads, 0, as_stream(stream)>>>(a);
     UWS_CHECK_LAUNCH("k_raster_bwd_rows");
     return UWS_OK;
 }

@@ -79,6 +79,29 @@ __device__ __forceinline__ bool below_clamp(float araw, const uws_splat* splat, 
     return alpha_raw_f64_cold(splat, exact, row, px, py) < kClamp;
 }
 
+__device__ __forceinline__ float rcp_ftz(float x) {
+    float y;
+    asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+    return y;
+}
+
+// Conservative tile-local box {ylo, yhi, xlo, xhi} of the region where the
+// staged pair test `power >= skip` can hold: for the positive-definite form
+// q = a dx^2 + b dx dy + c dy^2 <= Q (a = -A, b = -B, c = -C, Q = -skip) the
+// extents are |dy| <= sqrt(4aQ / (4ac - b^2)), |dx| <= sqrt(4cQ / (4ac - b^2)).
+// A relative + absolute margin keeps it a strict superset of what the float32
+// per-pixel test accepts; it is only a pre-filter.
+__device__ __forceinline__ float4 stage_extent(const StageA& s, const StageB& t) {
+    const float a = -s.A, b = -s.B, c = -t.C, Q = -t.skip;
+    if (Q < 0.f) return make_float4(1e30f, -1e30f, 1e30f, -1e30f);  // nothing passes
+    const float det4 = 4.f * a * c - b * b;
+    if (!(det4 > 0.f) || !(a > 0.f) || !(c > 0.f) || !(Q >= 0.f))
+        return make_float4(-1e30f, 1e30f, -1e30f, 1e30f);  // degenerate/NaN: no pre-filter
+    const float ey = sqrtf(4.f * a * Q / det4) * 1.001f + 0.01f;
+    const float ex = sqrtf(4.f * c * Q / det4) * 1.001f + 0.01f;
+    return make_float4(s.my - ey, s.my + ey, s.mx - ex, s.mx + ex);
+}
+
 // Stage entry `row` of a tile whose origin is (ox, oy).
 __device__ __forceinline__ void stage_entry(const uws_splat* __restrict__ splat, int row, int ox,
                                             int oy, StageA& a, StageB& b, StageC& c) {
