@@ -14,8 +14,6 @@
 // reference -- and the CTA leaves as soon as all its pixels are done.  The
 // per-pixel consumed-prefix length is written out so the backward kernel
 // visits exactly the same pairs.
-#include <cstdlib>
-
 #include "raster_common.cuh"
 #include "row_filter.cuh"
 
@@ -23,6 +21,10 @@ namespace uws {
 namespace {
 
 constexpr int kBatch = 256;
+constexpr int kThreads = kRasterThreads;       // one pixel per thread
+constexpr int kWarps = kThreads / 32;          // 8
+constexpr int kBandRows = kTile / kWarps;      // each warp owns a 2-row band of the tile
+constexpr int kListPad = 4;                    // per-warp lists are walked 4 entries at a time
 
 struct FwdArgs {
     const uws_splat* splat;
@@ -37,55 +39,42 @@ struct FwdArgs {
     uws_raster_out out;
 };
 
-struct PixState {
-    float T, cr, cg, cb, dsum, wsum;
-    int count, last;
-    bool done;
-};
-
-__device__ __forceinline__ void blend(PixState& s, float araw, const float4& c, float depth,
-                                      int idx) {
-    const float alpha = fminf(araw, kClampF);
-    const float w = alpha * s.T;
-    s.cr = fmaf(w, c.x, s.cr);
-    s.cg = fmaf(w, c.y, s.cg);
-    s.cb = fmaf(w, c.z, s.cb);
-    s.dsum = fmaf(w, depth, s.dsum);
-    s.wsum += w;
-    s.T = s.T * (1.0f - alpha);
-    ++s.count;
-    s.last = idx;
-    if (!(s.T >= kTStopF)) s.done = true;
+// Bit b set <=> the staged box [ylo, yhi] reaches a pixel centre of band b.
+__device__ __forceinline__ unsigned band_mask(float ylo, float yhi) {
+    // band b covers centres 2b + 0.5 .. 2b + 1.5
+    const float lo = fmaxf(ceilf((ylo - 1.5f) * 0.5f), 0.f);
+    const float hi = fminf(floorf((yhi - 0.5f) * 0.5f), (float)(kWarps - 1));
+    if (!(lo <= hi)) return (ylo != ylo || yhi != yhi) ? 0xffu : 0u;  // NaN box: no pre-filter
+    const unsigned l = (unsigned)lo, h = (unsigned)hi;
+    return ((2u << h) - 1u) & ~((1u << l) - 1u);
 }
 
-template <int PIX, bool ROWS>
-__global__ void __launch_bounds__(kRasterThreads / PIX, (PIX == 1 ? 3 : 4 * PIX / 2)) k_raster_fwd(FwdArgs a) {
-    constexpr int THREADS = kRasterThreads / PIX;
-    constexpr int ROWSTEP = kTile / PIX;
-    static_assert(!ROWS || THREADS == kBatch, "row-list source needs one thread per batch slot");
-    __shared__ float4 sP0[kBatch];  // mx, my, A, B
-    __shared__ float4 sP1[kBatch];  // C, op, skip, depth
-    __shared__ float4 sP2[kBatch];  // r, g, b, row
+template <bool ROWS>
+__global__ void __launch_bounds__(kThreads, 4) k_raster_fwd(FwdArgs a) {
+    __shared__ float4 sP0[kBatch + 1];  // mx, my, A, B          (+1: sentinel that never passes)
+    __shared__ float4 sP1[kBatch + 1];  // C, op, skip, depth
+    __shared__ float4 sP2[kBatch + 1];  // r, g, b, row
+    __shared__ unsigned char sMask[kBatch];
+    __shared__ __align__(8) unsigned short sList[kWarps][kBatch + kListPad];
     __shared__ int sRow[ROWS ? kBatch + kChunk : 1];
-    __shared__ int sScan[THREADS / 32];
+    __shared__ int sScan[kWarps];
 
     const int tile = blockIdx.x;
     const int ty = tile / a.gx, tx = tile - ty * a.gx;
     const int ox = tx * kTile, oy = ty * kTile;
-    const int lx = threadIdx.x & (kTile - 1), ly0 = threadIdx.x / kTile;
-    const float fx = (float)lx + 0.5f;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int lx = lane & (kTile - 1), ly = warp * kBandRows + (lane >> 4);
+    const float fx = (float)lx + 0.5f, fy = (float)ly + 0.5f;
+    const int px = ox + lx, py = oy + ly;
+    const bool inside = px < a.width && py < a.height;
 
-    PixState ps[PIX];
-    float fy[PIX];
-    bool inside[PIX];
-    bool all_done = true;
-#pragma unroll
-    for (int p = 0; p < PIX; ++p) {
-        const int ly = ly0 + p * ROWSTEP;
-        fy[p] = (float)ly + 0.5f;
-        inside[p] = (ox + lx) < a.width && (oy + ly) < a.height;
-        ps[p] = PixState{1.0f, 0.f, 0.f, 0.f, 0.f, 0.f, 0, 0, !inside[p]};
-        all_done &= ps[p].done;
+    // pixel state; T = 0 marks a pixel outside the image as finished
+    float T = inside ? 1.0f : 0.0f, cr = 0.f, cg = 0.f, cb = 0.f, dsum = 0.f, wsum = 0.f;
+    int count = 0, last = 0;
+    if (threadIdx.x == 0) {
+        sP0[kBatch] = make_float4(0.f, 0.f, 0.f, 0.f);
+        sP1[kBatch] = make_float4(0.f, 0.f, __int_as_float(0x7f800000), 0.f);  // skip = +inf
+        sP2[kBatch] = make_float4(0.f, 0.f, 0.f, 0.f);
     }
 
     int start = 0, end = 0, cur = 0, nst = 0;
@@ -98,146 +87,132 @@ __global__ void __launch_bounds__(kRasterThreads / PIX, (PIX == 1 ? 3 : 4 * PIX 
     }
     int base = 0;  // tile-list entries consumed so far
     while (true) {
-        if (__syncthreads_count(all_done) == THREADS) break;
+        if (__syncthreads_count(!(T >= kTStopF)) == kThreads) break;
         int n;
+        int row = -1;
         if (ROWS) {
             // fill the staging list with >= 256 rows of this tile (or all that remain)
             while (nst < kBatch && cur < end) {
-                nst += filter_chunk<THREADS>(a.row_items, cur, end, tx, sRow, nst,
-                                             kBatch + kChunk, sScan);
+                nst += filter_chunk<kThreads>(a.row_items, cur, end, tx, sRow, nst,
+                                              kBatch + kChunk, sScan);
                 cur += kChunk;
             }
             n = min(nst, kBatch);
             if (n == 0) break;
-            if (threadIdx.x < n) {
-                StageA sa;
-                StageB sb;
-                StageC sc;
-                stage_entry(a.splat, sRow[threadIdx.x], ox, oy, sa, sb, sc);
-                sP0[threadIdx.x] = make_float4(sa.mx, sa.my, sa.A, sa.B);
-                sP1[threadIdx.x] = make_float4(sb.C, sb.op, sb.skip, sb.depth);
-                sP2[threadIdx.x] = make_float4(sc.r, sc.g, sc.b, __int_as_float(sc.row));
-            }
+            if (threadIdx.x < n) row = sRow[threadIdx.x];
         } else {
             if (start + base >= end) break;
             n = min(kBatch, end - start - base);
-#pragma unroll
-            for (int s = 0; s < kBatch / THREADS; ++s) {
-                const int i = threadIdx.x + s * THREADS;
-                if (i < n) {
-                    StageA sa;
-                    StageB sb;
-                    StageC sc;
-                    stage_entry(a.splat, a.entries[start + base + i], ox, oy, sa, sb, sc);
-                    sP0[i] = make_float4(sa.mx, sa.my, sa.A, sa.B);
-                    sP1[i] = make_float4(sb.C, sb.op, sb.skip, sb.depth);
-                    sP2[i] = make_float4(sc.r, sc.g, sc.b, __int_as_float(sc.row));
-                }
-            }
+            if (threadIdx.x < n) row = a.entries[start + base + threadIdx.x];
+        }
+        if (row >= 0) {
+            StageA sa;
+            StageB sb;
+            StageC sc;
+            stage_entry(a.splat, row, ox, oy, sa, sb, sc);
+            sP0[threadIdx.x] = make_float4(sa.mx, sa.my, sa.A, sa.B);
+            sP1[threadIdx.x] = make_float4(sb.C, sb.op, sb.skip, sb.depth);
+            sP2[threadIdx.x] = make_float4(sc.r, sc.g, sc.b, __int_as_float(sc.row));
+            const float4 box = stage_extent(sa, sb);
+            sMask[threadIdx.x] = (unsigned char)band_mask(box.x, box.y);
         }
         __syncthreads();
-        if (!all_done) {
-            const int rel = base + 1;
+        // this warp's entries: those whose box reaches its band, in list order
+        int m = 0;
+        if (__any_sync(0xffffffffu, T >= kTStopF)) {
+            for (int c = 0; c < n; c += 32) {
+                const int i = c + lane;
+                const bool keep = i < n && ((sMask[i] >> warp) & 1u);
+                const unsigned bal = __ballot_sync(0xffffffffu, keep);
+                if (keep) sList[warp][m + __popc(bal & ((1u << lane) - 1u))] = (unsigned short)i;
+                m += __popc(bal);
+            }
+            if (lane < kListPad) sList[warp][m + lane] = (unsigned short)kBatch;  // sentinel pad
+            __syncwarp();
+        }
+        const int rel = base + 1;
+#pragma unroll 1
+        for (int j = 0; j < m && T >= kTStopF; j += kListPad) {
+            const ushort4 q = *reinterpret_cast<const ushort4*>(&sList[warp][j]);
+            const int idx[kListPad] = {q.x, q.y, q.z, q.w};
 #pragma unroll
-            for (int p = 0; p < PIX; ++p) {
-                PixState& s = ps[p];
-                int k = 0;
-                while (!s.done && k < n) {
-                    // hot loop: float32 only
-                    for (; k < n; ++k) {
-                        const float4 p0 = sP0[k];
-                        const float4 p1 = sP1[k];
-                        const float dx = fx - p0.x, dy = fy[p] - p0.y;
-                        const float power = dx * fmaf(p0.w, dy, p0.z * dx) + p1.x * dy * dy;
-                        if (power < p1.z) continue;
-                        const float araw = p1.y * ex2_ftz(power);
-                        if (araw < kFloorHi) {
-                            if (araw >= kFloorLo) break;  // guard band -> slow path
-                            continue;
-                        }
-                        blend(s, araw, sP2[k], p1.w, rel + k);
-                        if (s.done) break;
+            for (int u = 0; u < kListPad; ++u) {
+                const int i = idx[u];
+                const float4 p0 = sP0[i];
+                const float4 p1 = sP1[i];
+                const float dx = fx - p0.x, dy = fy - p0.y;
+                const float power = dx * fmaf(p0.w, dy, p0.z * dx) + p1.x * dy * dy;
+                if (power >= p1.z && T >= kTStopF) {
+                    const float araw = p1.y * ex2_ftz(power);
+                    bool ok = araw >= kFloorHi;
+                    if (!ok && araw >= kFloorLo)  // guard band: float64 decision (rare)
+                        ok = alpha_raw_f64_cold(a.splat, a.exact, __float_as_int(sP2[i].w), px,
+                                                py) >= kFloor;
+                    if (ok) {
+                        const float4 c = sP2[i];
+                        const float alpha = fminf(araw, kClampF);
+                        const float w = alpha * T;
+                        cr = fmaf(w, c.x, cr);
+                        cg = fmaf(w, c.y, cg);
+                        cb = fmaf(w, c.z, cb);
+                        dsum = fmaf(w, p1.w, dsum);
+                        wsum += w;
+                        T = T * (1.0f - alpha);
+                        ++count;
+                        last = rel + i;
                     }
-                    if (s.done || k >= n) break;
-                    // slow path: float64 decision of alpha_raw >= 1/255 for entry k
-                    const float4 p0 = sP0[k];
-                    const float4 p1 = sP1[k];
-                    const float4 p2 = sP2[k];
-                    const float dx = fx - p0.x, dy = fy[p] - p0.y;
-                    const float araw =
-                        p1.y * ex2_ftz(dx * fmaf(p0.w, dy, p0.z * dx) + p1.x * dy * dy);
-                    if (alpha_raw_f64(a.splat, a.exact, __float_as_int(p2.w), ox + lx,
-                                      oy + ly0 + p * ROWSTEP) >= kFloor)
-                        blend(s, araw, p2, p1.w, rel + k);
-                    ++k;
                 }
             }
-            all_done = true;
-#pragma unroll
-            for (int p = 0; p < PIX; ++p) all_done &= ps[p].done;
         }
         base += n;
         if (ROWS) {
             // keep the staged rows beyond this batch for the next one
             __syncthreads();
             const int rem = nst - n;
-            constexpr int KEEP = (kBatch + kChunk) / THREADS;
+            constexpr int KEEP = (kBatch + kChunk) / kThreads;
             int keep[KEEP];
 #pragma unroll
             for (int q = 0; q < KEEP; ++q) {
-                const int i = threadIdx.x + q * THREADS;
+                const int i = threadIdx.x + q * kThreads;
                 keep[q] = i < rem ? sRow[n + i] : 0;
             }
             __syncthreads();
 #pragma unroll
             for (int q = 0; q < KEEP; ++q) {
-                const int i = threadIdx.x + q * THREADS;
+                const int i = threadIdx.x + q * kThreads;
                 if (i < rem) sRow[i] = keep[q];
             }
             nst = rem;
         }
     }
-#pragma unroll
-    for (int p = 0; p < PIX; ++p) {
-        if (!inside[p]) continue;
-        const PixState& s = ps[p];
-        const int pix = (oy + ly0 + p * ROWSTEP) * a.width + ox + lx;
-        const float depth = s.count > 0 ? s.dsum / s.wsum : a.far_plane;
-        a.out.depth[pix] = depth;
-        a.out.weight[pix] = s.wsum;
-        a.out.final_T[pix] = s.T;
-        a.out.count[pix] = s.count;
-        if (a.out.last) a.out.last[pix] = s.last;
-        const float c3[3] = {s.cr, s.cg, s.cb};
-        if (a.medium == nullptr) {
-#pragma unroll
-            for (int ch = 0; ch < 3; ++ch) {
-                a.out.color[3 * pix + ch] = c3[ch];
-                if (a.out.color_clean) a.out.color_clean[3 * pix + ch] = c3[ch];
-            }
-            continue;
-        }
-        // underwater epilogue: z = logistic(depth); C*exp(-Bd z) + Binf (1 - exp(-Bb z))
-        const float z = 2.0f / (1.0f + expf(-(float)kLogisticRate * depth)) - 1.0f;
+    if (!inside) return;
+    const int pix = py * a.width + px;
+    const float depth = count > 0 ? dsum / wsum : a.far_plane;
+    a.out.depth[pix] = depth;
+    a.out.weight[pix] = wsum;
+    a.out.final_T[pix] = T;
+    a.out.count[pix] = count;
+    if (a.out.last) a.out.last[pix] = last;
+    const float c3[3] = {cr, cg, cb};
+    if (a.medium == nullptr) {
 #pragma unroll
         for (int ch = 0; ch < 3; ++ch) {
-            const float att = expf(-a.medium[ch] * z);
-            const float bs = a.medium[3 + ch] * (1.0f - expf(-a.medium[6 + ch] * z));
-            a.out.color[3 * pix + ch] = c3[ch] * att + bs;
-            a.out.color_clean[3 * pix + ch] = c3[ch];
-            if (a.out.attenuation) a.out.attenuation[3 * pix + ch] = att;
-            if (a.out.backscatter) a.out.backscatter[3 * pix + ch] = bs;
+            a.out.color[3 * pix + ch] = c3[ch];
+            if (a.out.color_clean) a.out.color_clean[3 * pix + ch] = c3[ch];
         }
+        return;
     }
-}
-
-int fwd_pix() {
-    static int pix = [] {
-        const char* e = getenv("UWS_FWD_PIX");
-        int v = e ? atoi(e) : 1;
-        return (v == 2 || v == 4) ? v : 1;
-    }();
-    return pix;
+    // underwater epilogue: z = logistic(depth); C*exp(-Bd z) + Binf (1 - exp(-Bb z))
+    const float z = 2.0f / (1.0f + expf(-(float)kLogisticRate * depth)) - 1.0f;
+#pragma unroll
+    for (int ch = 0; ch < 3; ++ch) {
+        const float att = expf(-a.medium[ch] * z);
+        const float bs = a.medium[3 + ch] * (1.0f - expf(-a.medium[6 + ch] * z));
+        a.out.color[3 * pix + ch] = c3[ch] * att + bs;
+        a.out.color_clean[3 * pix + ch] = c3[ch];
+        if (a.out.attenuation) a.out.attenuation[3 * pix + ch] = att;
+        if (a.out.backscatter) a.out.backscatter[3 * pix + ch] = bs;
+    }
 }
 
 }  // namespace
@@ -267,12 +242,7 @@ extern "C" int uws_raster_fwd(const uws_projected* proj, const int32_t* offsets,
     a.far_plane = (float)cam->far_plane;
     a.medium = medium;
     a.out = *out;
-    cudaStream_t st = as_stream(stream);
-    switch (fwd_pix()) {
-        case 2: k_raster_fwd<2, false><<<a.gx * gy, kRasterThreads / 2, 0, st>>>(a); break;
-        case 4: k_raster_fwd<4, false><<<a.gx * gy, kRasterThreads / 4, 0, st>>>(a); break;
-        default: k_raster_fwd<1, false><<<a.gx * gy, kRasterThreads, 0, st>>>(a); break;
-    }
+    k_raster_fwd<false><<<a.gx * gy, kThreads, 0, as_stream(stream)>>>(a);
     UWS_CHECK_LAUNCH("k_raster_fwd");
     return UWS_OK;
 }
@@ -299,7 +269,7 @@ extern "C" int uws_raster_fwd_rows(const uws_projected* proj, const int32_t* row
     a.far_plane = (float)cam->far_plane;
     a.medium = medium;
     a.out = *out;
-    k_raster_fwd<1, true><<<a.gx * gy, kRasterThreads, 0, as_stream(stream)>>>(a);
+    k_raster_fwd<true><<<a.gx * gy, kThreads, 0, as_stream(stream)>>>(a);
     UWS_CHECK_LAUNCH("k_raster_fwd_rows");
     return UWS_OK;
 }
