@@ -223,14 +223,15 @@ __global__ void __launch_bounds__(kThreads, 10) k_raster_bwd(BwdArgs a) {
             const float4 D = sD[k];
             if (D.y < band_lo || D.x > band_hi) continue;  // misses this warp's band (uniform)
             const int jrel = lo + k;
-            float v[9];
-#pragma unroll
-            for (int i = 0; i < 9; ++i) v[i] = 0.f;
+            // A thread's kPix pixels share one column, hence dx: the dx-weighted
+            // partials are formed once after the pixel loop from sum(dp) and sum(dp dy).
+            float sdp = 0.f, sdpy = 0.f, sdpyy = 0.f, wg0 = 0.f, wg1 = 0.f, wg2 = 0.f, dx = 0.f;
             bool hit = false;
             if (fx >= D.z && fx <= D.w) {  // column inside the box
                 const StageA A = sA[k];
                 const StageB B = sB[k];
-                const float dx = fx - A.mx;
+                const StageC C = sC[k];
+                dx = fx - A.mx;
                 const float tA = A.A * dx;
 #pragma unroll
                 for (int p = 0; p < kPix; ++p) {
@@ -241,9 +242,9 @@ __global__ void __launch_bounds__(kThreads, 10) k_raster_bwd(BwdArgs a) {
                     const float araw = B.op * ex2_ftz(power);
                     if (araw < kFloorLo) continue;
                     bool unclamped = araw < kClampLo;
-                    if (araw < kFloorHi || (!unclamped && araw < kClampHi)) {
+                    if (araw < kFloorHi || (araw >= kClampLo && araw < kClampHi)) {
                         // guard band: re-decide both gates from the float64 record
-                        const double e = alpha_raw_f64_cold(a.splat, a.exact, sC[k].row, ox + lx,
+                        const double e = alpha_raw_f64_cold(a.splat, a.exact, C.row, ox + lx,
                                                             oy + ly0 + 2 * p);
                         if (!(e >= kFloor)) continue;
                         unclamped = e < kClamp;
@@ -253,24 +254,22 @@ __global__ void __launch_bounds__(kThreads, 10) k_raster_bwd(BwdArgs a) {
                     const float inv_om = rcp_ftz(1.0f - alpha);
                     const float Ti = T[p] * inv_om;
                     const float w = alpha * Ti;
-                    const StageC& C = sC[k];
                     const float U = G[p][0] * C.r + G[p][1] * C.g + G[p][2] * C.b;
                     const float dalpha = U * Ti - S[p] * inv_om;
                     S[p] = fmaf(w, U, S[p]);
                     T[p] = Ti;
                     const float dp = unclamped ? dalpha * araw : 0.f;
-                    const float dpx = dp * dx, dpy = dp * dy;
-                    v[0] += dp;
-                    v[1] += dpx;
-                    v[2] += dpy;
-                    v[3] = fmaf(dpx, dx, v[3]);
-                    v[4] = fmaf(dpx, dy, v[4]);
-                    v[5] = fmaf(dpy, dy, v[5]);
-                    v[6] = fmaf(w, G[p][0], v[6]);
-                    v[7] = fmaf(w, G[p][1], v[7]);
-                    v[8] = fmaf(w, G[p][2], v[8]);
+                    const float dpy = dp * dy;
+                    sdp += dp;
+                    sdpy += dpy;
+                    sdpyy = fmaf(dpy, dy, sdpyy);
+                    wg0 = fmaf(w, G[p][0], wg0);
+                    wg1 = fmaf(w, G[p][1], wg1);
+                    wg2 = fmaf(w, G[p][2], wg2);
                 }
             }
+            const float sdpx = sdp * dx;
+            float v[9] = {sdp, sdpx, sdpy, sdpx * dx, sdpy * dx, sdpyy, wg0, wg1, wg2};
             if (!__any_sync(0xffffffffu, hit)) continue;
             const float r8 = butterfly8(v, lane);
             const float r9 = warp_sum(v[8]);
