@@ -76,8 +76,8 @@ __device__ __forceinline__ float butterfly8(const float v[8], int lane) {
 
 constexpr int kMaxMarks = 128;  // recorded batch starts per tile (row-list source)
 
-template <bool ROWS>
-__global__ void __launch_bounds__(kThreads, 10) k_raster_bwd(BwdArgs a) {
+template <bool ROWS, int MINB>
+__global__ void __launch_bounds__(kThreads, MINB) k_raster_bwd(BwdArgs a) {
     __shared__ int sRow[ROWS ? kBatch : 1];  // (filter writes only positions < nb <= kBatch)
     __shared__ int sMarkCur[ROWS ? kMaxMarks : 1], sMarkSkip[ROWS ? kMaxMarks : 1];
     __shared__ int sScan[kWarps];
@@ -350,7 +350,7 @@ extern "C" int uws_raster_bwd(const uws_projected* proj, const int32_t* offsets,
     a.medium_acc = medium_acc;
     a.row_start = nullptr;
     a.row_items = nullptr;
-    k_raster_bwd<false><<<a.gx * gy, kThreads, 0, as_stream(stream)>>>(a);
+    k_raster_bwd<false, 12><<<a.gx * gy, kThreads, 0, as_stream(stream)>>>(a);
     UWS_CHECK_LAUNCH("k_raster_bwd");
     return UWS_OK;
 }
@@ -384,7 +384,7 @@ extern "C" int uws_raster_bwd_rows(const uws_projected* proj, const int32_t* row
     a.dL = dL_dC;
     a.screen = screen_grads;
     a.medium_acc = medium_acc;
-    k_raster_bwd<true><<<a.gx * gy, kThreads, 0, as_stream(stream)>>>(a);
+    k_raster_bwd<true, 12><<<a.gx * gy, kThreads, 0, as_stream(stream)>>>(a);
     UWS_CHECK_LAUNCH("k_raster_bwd_rows");
     return UWS_OK;
 }
