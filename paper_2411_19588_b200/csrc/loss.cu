@@ -5,19 +5,26 @@
 // C1 = 0.01^2, C2 = 0.03^2, adjoint of the valid filter :68-74) and
 // guidance_loss (:126-137).
 //
-// Two tiled passes, each staging a (16+10) x (32+10) halo patch in shared
-// memory and filtering separably: (1) window moments -> SSIM map partial sums
-// and the three per-window derivative maps; (2) the adjoint filter of those
-// maps fused with the L1 subgradient -> dL/dC.  Partial sums are reduced in
-// a fixed order (deterministic) by a one-block finalize kernel.
+// Two tiled passes over 32x32 tiles with a 10-pixel halo staged in shared
+// memory, each filtering separably with register-blocked sliding sums (8
+// outputs per horizontal item, 4 per vertical item, taps in the constant
+// bank): (1) window moments -> SSIM map partial sums and the three
+// per-window derivative maps (planar, one plane per map and channel); (2) the
+// adjoint filter of those maps fused with the L1 subgradient -> dL/dC.  Partial
+// sums are reduced in a fixed order (deterministic) by a one-block finalize
+// kernel.
 #include "common.cuh"
 
 namespace uws {
 namespace {
 
-constexpr int kOW = 32, kOH = 16, kR = 5, kN = 11;
-constexpr int kPW = kOW + 2 * kR, kPH = kOH + 2 * kR;
+constexpr int kR = 5, kN = 11;
+constexpr int kT = 32;               // output tile edge
+constexpr int kP = kT + 2 * kR;      // staged patch edge (42)
+constexpr int kHR = 8;               // horizontal outputs per item
+constexpr int kVR = 4;               // vertical outputs per item
 constexpr int kThreads = 256;
+constexpr int kMaxC = 4;             // channels staged at once by the moments pass
 constexpr double kC1 = 0.01 * 0.01, kC2 = 0.03 * 0.03;
 
 __constant__ float c_taps[kN];
@@ -33,135 +40,238 @@ __device__ __forceinline__ float block_sum_f(float v, float* sred) {
     return s;
 }
 
-__global__ void __launch_bounds__(kThreads) k_ssim_moments(const float* __restrict__ img_a,
-                                                           const float* __restrict__ img_b, int H,
-                                                           int W, int C, float* __restrict__ t_mu,
-                                                           float* __restrict__ t_aa,
-                                                           float* __restrict__ t_ab,
-                                                           double* __restrict__ part_s) {
-    __shared__ float sa[kPH][kPW + 1], sb[kPH][kPW + 1];
-    __shared__ float hs[5][kPH][kOW + 1];
+// Pass 1.  Block = 32x32 valid windows (all channels); dynamic smem holds the
+// interleaved (a, b) patch [2][kP][kP*C + 1] and the horizontal moments
+// [5][kP][kT + 1] of the channel in flight.
+template <int CT>  // compile-time channel count (0: runtime C)
+__global__ void __launch_bounds__(kThreads, 3) k_ssim_moments(const float* __restrict__ img_a,
+                                                              const float* __restrict__ img_b,
+                                                              int H, int W, int C_,
+                                                              float* __restrict__ maps,
+                                                              double* __restrict__ part_s) {
+    const int C = CT > 0 ? CT : C_;
+    extern __shared__ float smem[];
+    const int pitch = kP * C + 1;
+    float* sa = smem;
+    float* sb = sa + kP * pitch;
+    float* hs = sb + kP * pitch;  // [5][kP][kT + 1]
     __shared__ float sred[kThreads / 32];
-    const int ch = blockIdx.z;
-    const int x0 = blockIdx.x * kOW, y0 = blockIdx.y * kOH;  // valid-window origin == image pixel
+    const int x0 = blockIdx.x * kT, y0 = blockIdx.y * kT;  // valid-window origin == image pixel
     const int VW = W - 2 * kR, VH = H - 2 * kR;
-    for (int i = threadIdx.x; i < kPH * kPW; i += kThreads) {
-        int r = i / kPW, c = i - r * kPW;
-        int gy = y0 + r, gx = x0 + c;
-        bool ok = gy < H && gx < W;
-        size_t o = ((size_t)gy * W + gx) * C + ch;
-        sa[r][c] = ok ? img_a[o] : 0.f;
-        sb[r][c] = ok ? img_b[o] : 0.f;
-    }
-    __syncthreads();
-    for (int i = threadIdx.x; i < kPH * kOW; i += kThreads) {
-        int r = i / kOW, c = i - r * kOW;
-        float m0 = 0, m1 = 0, m2 = 0, m3 = 0, m4 = 0;
-#pragma unroll
-        for (int t = 0; t < kN; ++t) {
-            float w = c_taps[t], xa = sa[r][c + t], xb = sb[r][c + t];
-            m0 += w * xa;
-            m1 += w * xb;
-            m2 += w * xa * xa;
-            m3 += w * xb * xb;
-            m4 += w * xa * xb;
-        }
-        hs[0][r][c] = m0; hs[1][r][c] = m1; hs[2][r][c] = m2; hs[3][r][c] = m3; hs[4][r][c] = m4;
+    const size_t plane = (size_t)VH * VW;
+    // stage rows of kP*C contiguous floats (coalesced)
+    const int rowlen = kP * C;
+    for (int i = threadIdx.x; i < kP * rowlen; i += kThreads) {
+        const int r = i / rowlen, q = i - r * rowlen;
+        const int gy = y0 + r, gx = x0 + q / C;
+        const bool ok = gy < H && gx < W;
+        const size_t o = ((size_t)gy * W + x0) * C + q;
+        sa[r * pitch + q] = ok ? __ldg(img_a + o) : 0.f;
+        sb[r * pitch + q] = ok ? __ldg(img_b + o) : 0.f;
     }
     __syncthreads();
     float ssum = 0.f;
-    for (int i = threadIdx.x; i < kOH * kOW; i += kThreads) {
-        int r = i / kOW, c = i - r * kOW;
-        int oy = y0 + r, ox = x0 + c;
-        if (oy >= VH || ox >= VW) continue;
-        float u1 = 0, u2 = 0, v1 = 0, v2 = 0, v12 = 0;
+    for (int ch = 0; ch < C; ++ch) {
+        // horizontal: item = (row, group of 8 columns)
+        for (int it = threadIdx.x; it < kP * (kT / kHR); it += kThreads) {
+            const int r = it >> 2, c0 = (it & 3) * kHR;
+            float m[5][kHR];
 #pragma unroll
-        for (int t = 0; t < kN; ++t) {
-            float w = c_taps[t];
-            u1 += w * hs[0][r + t][c];
-            u2 += w * hs[1][r + t][c];
-            v1 += w * hs[2][r + t][c];
-            v2 += w * hs[3][r + t][c];
-            v12 += w * hs[4][r + t][c];
+            for (int v = 0; v < 5; ++v)
+#pragma unroll
+                for (int j = 0; j < kHR; ++j) m[v][j] = 0.f;
+            const float* pa = sa + r * pitch + c0 * C + ch;
+            const float* pb = sb + r * pitch + c0 * C + ch;
+#pragma unroll
+            for (int q = 0; q < kHR + kN - 1; ++q) {
+                const float xa = pa[q * C], xb = pb[q * C];
+                const float aa = xa * xa, bb = xb * xb, ab = xa * xb;
+#pragma unroll
+                for (int j = 0; j < kHR; ++j) {
+                    const int t = q - j;
+                    if (t < 0 || t >= kN) continue;
+                    const float w = c_taps[t];
+                    m[0][j] = fmaf(w, xa, m[0][j]);
+                    m[1][j] = fmaf(w, xb, m[1][j]);
+                    m[2][j] = fmaf(w, aa, m[2][j]);
+                    m[3][j] = fmaf(w, bb, m[3][j]);
+                    m[4][j] = fmaf(w, ab, m[4][j]);
+                }
+            }
+#pragma unroll
+            for (int v = 0; v < 5; ++v)
+#pragma unroll
+                for (int j = 0; j < kHR; ++j) hs[(v * kP + r) * (kT + 1) + c0 + j] = m[v][j];
         }
-        const float A1 = 2.0f * u1 * u2 + (float)kC1;
-        const float A2 = 2.0f * (v12 - u1 * u2) + (float)kC2;
-        const float B1 = u1 * u1 + u2 * u2 + (float)kC1;
-        const float B2 = (v1 - u1 * u1) + (v2 - u2 * u2) + (float)kC2;
-        const float inv = 1.0f / (B1 * B2);
-        const float S = A1 * A2 * inv;
-        ssum += S;
-        size_t o = ((size_t)oy * VW + ox) * C + ch;
-        t_mu[o] = 2.0f * u2 * (A2 - A1) * inv - 2.0f * u1 * S * (1.0f / B1 - 1.0f / B2);
-        t_aa[o] = -S / B2;
-        t_ab[o] = 2.0f * A1 * inv;
+        __syncthreads();
+        // vertical: item = (column, group of 4 rows)
+        {
+            const int c = threadIdx.x & (kT - 1), r0 = (threadIdx.x >> 5) * kVR;
+            float u[5][kVR];
+#pragma unroll
+            for (int v = 0; v < 5; ++v)
+#pragma unroll
+                for (int j = 0; j < kVR; ++j) u[v][j] = 0.f;
+#pragma unroll
+            for (int q = 0; q < kVR + kN - 1; ++q) {
+                float h[5];
+#pragma unroll
+                for (int v = 0; v < 5; ++v) h[v] = hs[(v * kP + r0 + q) * (kT + 1) + c];
+#pragma unroll
+                for (int j = 0; j < kVR; ++j) {
+                    const int t = q - j;
+                    if (t < 0 || t >= kN) continue;
+                    const float w = c_taps[t];
+#pragma unroll
+                    for (int v = 0; v < 5; ++v) u[v][j] = fmaf(w, h[v], u[v][j]);
+                }
+            }
+            const int ox = x0 + c;
+#pragma unroll
+            for (int j = 0; j < kVR; ++j) {
+                const int oy = y0 + r0 + j;
+                if (oy >= VH || ox >= VW) continue;
+                const float u1 = u[0][j], u2 = u[1][j], v1 = u[2][j], v2 = u[3][j], v12 = u[4][j];
+                const float A1 = 2.0f * u1 * u2 + (float)kC1;
+                const float A2 = 2.0f * (v12 - u1 * u2) + (float)kC2;
+                const float B1 = u1 * u1 + u2 * u2 + (float)kC1;
+                const float B2 = (v1 - u1 * u1) + (v2 - u2 * u2) + (float)kC2;
+                const float inv = 1.0f / (B1 * B2);
+                const float S = A1 * A2 * inv;
+                ssum += S;
+                const size_t o = (size_t)oy * VW + ox;
+                maps[(0 * C + ch) * plane + o] =
+                    2.0f * u2 * (A2 - A1) * inv - 2.0f * u1 * S * (1.0f / B1 - 1.0f / B2);
+                maps[(1 * C + ch) * plane + o] = -S / B2;
+                maps[(2 * C + ch) * plane + o] = 2.0f * A1 * inv;
+            }
+        }
+        __syncthreads();  // hs reuse by the next channel
     }
     float bs = block_sum_f(ssum, sred);
-    if (threadIdx.x == 0)
-        part_s[((size_t)blockIdx.z * gridDim.y + blockIdx.y) * gridDim.x + blockIdx.x] = (double)bs;
+    if (threadIdx.x == 0) part_s[blockIdx.y * gridDim.x + blockIdx.x] = (double)bs;
 }
 
-__global__ void __launch_bounds__(kThreads) k_ssim_grad(const float* __restrict__ img_a,
-                                                        const float* __restrict__ img_b, int H, int W,
-                                                        int C, const float* __restrict__ t_mu,
-                                                        const float* __restrict__ t_aa,
-                                                        const float* __restrict__ t_ab,
-                                                        float k_ssim, float k_l1,
-                                                        float* __restrict__ grad,
-                                                        double* __restrict__ part_l1) {
-    __shared__ float sm[3][kPH][kPW + 1];
-    __shared__ float hs[3][kPH][kOW + 1];
+// Pass 2.  Block = 32x32 image pixels; per channel the three derivative maps
+// are staged with a 2R halo (zero outside the valid grid) and filtered by the
+// adjoint (= the same symmetric) window.
+template <int CT>
+__global__ void __launch_bounds__(kThreads, 3) k_ssim_grad(const float* __restrict__ img_a,
+                                                           const float* __restrict__ img_b, int H,
+                                                           int W, int C_,
+                                                           const float* __restrict__ maps,
+                                                           float k_ssim, float k_l1,
+                                                           float* __restrict__ grad,
+                                                           double* __restrict__ part_l1) {
+    __shared__ float sm[3][kP][kP + 1];
+    __shared__ float hs[3][kP][kT + 1];
     __shared__ float sred[kThreads / 32];
-    const int ch = blockIdx.z;
-    const int x0 = blockIdx.x * kOW, y0 = blockIdx.y * kOH;
+    const int C = CT > 0 ? CT : C_;
+    const int x0 = blockIdx.x * kT, y0 = blockIdx.y * kT;
     const int VW = W - 2 * kR, VH = H - 2 * kR;
-    // adj[y][x] = sum_{u,v} w_u w_v M[y+u-2R][x+v-2R], M zero outside the valid grid
-    for (int i = threadIdx.x; i < kPH * kPW; i += kThreads) {
-        int r = i / kPW, c = i - r * kPW;
-        int my = y0 + r - 2 * kR, mx = x0 + c - 2 * kR;
-        bool ok = my >= 0 && my < VH && mx >= 0 && mx < VW;
-        size_t o = ((size_t)my * VW + mx) * C + ch;
-        sm[0][r][c] = ok ? t_mu[o] : 0.f;
-        sm[1][r][c] = ok ? t_aa[o] : 0.f;
-        sm[2][r][c] = ok ? t_ab[o] : 0.f;
-    }
-    __syncthreads();
-    for (int i = threadIdx.x; i < kPH * kOW; i += kThreads) {
-        int r = i / kOW, c = i - r * kOW;
-        float m0 = 0, m1 = 0, m2 = 0;
-#pragma unroll
-        for (int t = 0; t < kN; ++t) {
-            float w = c_taps[t];
-            m0 += w * sm[0][r][c + t];
-            m1 += w * sm[1][r][c + t];
-            m2 += w * sm[2][r][c + t];
-        }
-        hs[0][r][c] = m0; hs[1][r][c] = m1; hs[2][r][c] = m2;
-    }
-    __syncthreads();
+    const size_t plane = (size_t)VH * VW;
     float l1sum = 0.f;
-    for (int i = threadIdx.x; i < kOH * kOW; i += kThreads) {
-        int r = i / kOW, c = i - r * kOW;
-        int y = y0 + r, x = x0 + c;
-        if (y >= H || x >= W) continue;
-        float g0 = 0, g1 = 0, g2 = 0;
+    for (int ch = 0; ch < C; ++ch) {
+        // adj[y][x] = sum_{u,v} w_u w_v M[y+u-2R][x+v-2R], M zero outside the valid grid
+        {
+            constexpr int kIt = (kP * kP + kThreads - 1) / kThreads;
+            float x[kIt][3];
 #pragma unroll
-        for (int t = 0; t < kN; ++t) {
-            float w = c_taps[t];
-            g0 += w * hs[0][r + t][c];
-            g1 += w * hs[1][r + t][c];
-            g2 += w * hs[2][r + t][c];
+            for (int k = 0; k < kIt; ++k) {  // all loads in flight before the stores
+                const int i = threadIdx.x + k * kThreads;
+                const int r = i / kP, c = i - r * kP;
+                const int my = y0 + r - 2 * kR, mx = x0 + c - 2 * kR;
+                const bool ok = i < kP * kP && my >= 0 && my < VH && mx >= 0 && mx < VW;
+                const size_t o = (size_t)my * VW + mx;
+#pragma unroll
+                for (int m = 0; m < 3; ++m)
+                    x[k][m] = ok ? __ldg(maps + (m * C + ch) * plane + o) : 0.f;
+            }
+#pragma unroll
+            for (int k = 0; k < kIt; ++k) {
+                const int i = threadIdx.x + k * kThreads;
+                const int r = i / kP, c = i - r * kP;
+                if (i < kP * kP) {
+#pragma unroll
+                    for (int m = 0; m < 3; ++m) sm[m][r][c] = x[k][m];
+                }
+            }
         }
-        size_t o = ((size_t)y * W + x) * C + ch;
-        float a = img_a[o], b = img_b[o];
-        float d = a - b;
-        float sg = (d > 0.f) ? 1.f : ((d < 0.f) ? -1.f : 0.f);
-        l1sum += fabsf(d);
-        grad[o] = k_ssim * (g0 + 2.0f * a * g1 + b * g2) + k_l1 * sg;
+        __syncthreads();
+        for (int it = threadIdx.x; it < kP * (kT / kHR); it += kThreads) {
+            const int r = it >> 2, c0 = (it & 3) * kHR;
+            float g[3][kHR];
+#pragma unroll
+            for (int m = 0; m < 3; ++m)
+#pragma unroll
+                for (int j = 0; j < kHR; ++j) g[m][j] = 0.f;
+#pragma unroll
+            for (int q = 0; q < kHR + kN - 1; ++q) {
+                float x[3];
+#pragma unroll
+                for (int m = 0; m < 3; ++m) x[m] = sm[m][r][c0 + q];
+#pragma unroll
+                for (int j = 0; j < kHR; ++j) {
+                    const int t = q - j;
+                    if (t < 0 || t >= kN) continue;
+                    const float w = c_taps[t];
+#pragma unroll
+                    for (int m = 0; m < 3; ++m) g[m][j] = fmaf(w, x[m], g[m][j]);
+                }
+            }
+#pragma unroll
+            for (int m = 0; m < 3; ++m)
+#pragma unroll
+                for (int j = 0; j < kHR; ++j) hs[m][r][c0 + j] = g[m][j];
+        }
+        __syncthreads();
+        {
+            const int c = threadIdx.x & (kT - 1), r0 = (threadIdx.x >> 5) * kVR;
+            const int x = x0 + c;
+            float pa[kVR], pb[kVR];
+#pragma unroll
+            for (int j = 0; j < kVR; ++j) {  // issue the image loads before the filter math
+                const int y = y0 + r0 + j;
+                const bool ok = y < H && x < W;
+                const size_t o = ((size_t)y * W + x) * C + ch;
+                pa[j] = ok ? __ldg(img_a + o) : 0.f;
+                pb[j] = ok ? __ldg(img_b + o) : 0.f;
+            }
+            float g[3][kVR];
+#pragma unroll
+            for (int m = 0; m < 3; ++m)
+#pragma unroll
+                for (int j = 0; j < kVR; ++j) g[m][j] = 0.f;
+#pragma unroll
+            for (int q = 0; q < kVR + kN - 1; ++q) {
+                float h[3];
+#pragma unroll
+                for (int m = 0; m < 3; ++m) h[m] = hs[m][r0 + q][c];
+#pragma unroll
+                for (int j = 0; j < kVR; ++j) {
+                    const int t = q - j;
+                    if (t < 0 || t >= kN) continue;
+                    const float w = c_taps[t];
+#pragma unroll
+                    for (int m = 0; m < 3; ++m) g[m][j] = fmaf(w, h[m], g[m][j]);
+                }
+            }
+#pragma unroll
+            for (int j = 0; j < kVR; ++j) {
+                const int y = y0 + r0 + j;
+                if (y >= H || x >= W) continue;
+                const size_t o = ((size_t)y * W + x) * C + ch;
+                const float a = pa[j], b = pb[j];
+                const float d = a - b;
+                const float sg = (d > 0.f) ? 1.f : ((d < 0.f) ? -1.f : 0.f);
+                l1sum += fabsf(d);
+                grad[o] = k_ssim * (g[0][j] + 2.0f * a * g[1][j] + b * g[2][j]) + k_l1 * sg;
+            }
+        }
+        __syncthreads();  // sm / hs reuse by the next channel
     }
     float bs = block_sum_f(l1sum, sred);
-    if (threadIdx.x == 0)
-        part_l1[((size_t)blockIdx.z * gridDim.y + blockIdx.y) * gridDim.x + blockIdx.x] = (double)bs;
+    if (threadIdx.x == 0) part_l1[blockIdx.y * gridDim.x + blockIdx.x] = (double)bs;
 }
 
 __global__ void __launch_bounds__(kThreads) k_loss_finalize(const double* __restrict__ part_s,
@@ -223,19 +333,16 @@ int ensure_taps() {
 }
 
 struct LossPlan {
-    float *t_mu, *t_aa, *t_ab;
+    float* maps;  // [3 maps][C][VH][VW]
     double *part_s, *part_l1;
     int n_s, n_l1;
 };
 
 void plan_loss(Workspace& ws, int h, int w, int c, LossPlan& p) {
     int vh = h - 2 * kR > 0 ? h - 2 * kR : 1, vw = w - 2 * kR > 0 ? w - 2 * kR : 1;
-    size_t nv = (size_t)vh * vw * c;
-    p.t_mu = ws.take<float>(nv);
-    p.t_aa = ws.take<float>(nv);
-    p.t_ab = ws.take<float>(nv);
-    p.n_s = (int)(ceil_div(vw, kOW) * ceil_div(vh, kOH) * c);
-    p.n_l1 = (int)(ceil_div(w, kOW) * ceil_div(h, kOH) * c);
+    p.maps = ws.take<float>((size_t)vh * vw * c * 3);
+    p.n_s = (int)(ceil_div(vw, kT) * ceil_div(vh, kT));
+    p.n_l1 = (int)(ceil_div(w, kT) * ceil_div(h, kT));
     p.part_s = ws.take<double>(p.n_s);
     p.part_l1 = ws.take<double>(p.n_l1);
 }
@@ -261,7 +368,7 @@ extern "C" int uws_loss_fwd_bwd(const float* rendered, const float* gt, int32_t 
                                 size_t workspace_bytes, void* stream) {
     UWS_REQUIRE(rendered && gt && dL_dC && result, "uws_loss_fwd_bwd: null argument");
     UWS_REQUIRE(h >= kN && w >= kN, "uws_loss_fwd_bwd: image smaller than the 11x11 window");
-    UWS_REQUIRE(c >= 1, "uws_loss_fwd_bwd: bad channel count");
+    UWS_REQUIRE(c >= 1 && c <= kMaxC, "uws_loss_fwd_bwd: channel count must be 1..4");
     int rc = ensure_taps();
     if (rc != UWS_OK) return rc;
     Workspace ws(workspace, workspace_bytes);
@@ -271,14 +378,31 @@ extern "C" int uws_loss_fwd_bwd(const float* rendered, const float* gt, int32_t 
     cudaStream_t st = as_stream(stream);
     const int vh = h - 2 * kR, vw = w - 2 * kR;
     const double n_px = (double)h * w * c, n_win = (double)vh * vw * c;
-    dim3 g1((unsigned)ceil_div(vw, kOW), (unsigned)ceil_div(vh, kOH), (unsigned)c);
-    k_ssim_moments<<<g1, kThreads, 0, st>>>(rendered, gt, h, w, c, p.t_mu, p.t_aa, p.t_ab, p.part_s);
+    const size_t smem1 = (size_t)(2 * kP * (kP * c + 1) + 5 * kP * (kT + 1)) * sizeof(float);
+    static bool attr_set = false;
+    if (!attr_set) {
+        const int mx = (int)(2 * kP * (kP * kMaxC + 1) + 5 * kP * (kT + 1)) * (int)sizeof(float);
+        UWS_CUDA(cudaFuncSetAttribute(k_ssim_moments<3>,
+                                      cudaFuncAttributeMaxDynamicSharedMemorySize, mx));
+        UWS_CUDA(cudaFuncSetAttribute(k_ssim_moments<0>,
+                                      cudaFuncAttributeMaxDynamicSharedMemorySize, mx));
+        attr_set = true;
+    }
+    dim3 g1((unsigned)ceil_div(vw, kT), (unsigned)ceil_div(vh, kT));
+    if (c == 3)
+        k_ssim_moments<3><<<g1, kThreads, smem1, st>>>(rendered, gt, h, w, c, p.maps, p.part_s);
+    else
+        k_ssim_moments<0><<<g1, kThreads, smem1, st>>>(rendered, gt, h, w, c, p.maps, p.part_s);
     UWS_CHECK_LAUNCH("k_ssim_moments");
-    dim3 g2((unsigned)ceil_div(w, kOW), (unsigned)ceil_div(h, kOH), (unsigned)c);
+    dim3 g2((unsigned)ceil_div(w, kT), (unsigned)ceil_div(h, kT));
     const float k_ssim = (float)(lambda_ssim * (-1.0 / n_win));
     const float k_l1 = (float)((1.0 - lambda_ssim) / n_px);
-    k_ssim_grad<<<g2, kThreads, 0, st>>>(rendered, gt, h, w, c, p.t_mu, p.t_aa, p.t_ab, k_ssim, k_l1,
-                                         dL_dC, p.part_l1);
+    if (c == 3)
+        k_ssim_grad<3><<<g2, kThreads, 0, st>>>(rendered, gt, h, w, c, p.maps, k_ssim, k_l1, dL_dC,
+                                                p.part_l1);
+    else
+        k_ssim_grad<0><<<g2, kThreads, 0, st>>>(rendered, gt, h, w, c, p.maps, k_ssim, k_l1, dL_dC,
+                                                p.part_l1);
     UWS_CHECK_LAUNCH("k_ssim_grad");
     k_loss_finalize<<<1, kThreads, 0, st>>>(p.part_s, p.n_s, p.part_l1, p.n_l1, n_px, n_win, medium,
                                             has_guidance, lambda_ssim, lambda_guide, result,
