@@ -9,8 +9,8 @@
 // in numpy's operation order; learning rates and bias corrections
 // 1 - beta^step come from the host exactly as Python computes them.  Given
 // the same float32 gradients the update is therefore bit-identical to the
-// reference.  One thread per Gaussian touches its 14 scalars (p, m, v read
-// and written, g read): 392 B/Gaussian of HBM traffic, coalesced per field.
+// reference.  Every scalar's p, m, v are read and written and g read (and
+// zeroed): 392 B/Gaussian of HBM traffic, coalesced.
 #include "common.cuh"
 
 namespace uws {
@@ -40,7 +40,16 @@ __device__ __forceinline__ void adam1(float& p, float& m, float& v, float g, con
                                 __dmul_rn(__dmul_rn(hp.one_minus_beta2, gd), gd));
     const double mh = div_by_const(mm, k.b1c, k.r1);
     const double vh = div_by_const(vv, k.b2c, k.r2);
-    const double upd = __dsub_rn((double)p, __ddiv_rn(__dmul_rn(k.lr, mh), __dadd_rn(__dsqrt_rn(vh), hp.eps)));
+    // Zero moments (Gaussians that never received a gradient) would send
+    // sqrt and the division down their out-of-line special-operand paths;
+    // their results are known exactly: sqrt(+0) = +0, and (+-0) / den = +-0
+    // for den = sqrt(vh) + eps > 0.
+    // (The substituted operands keep the unused branch on the inline fast path
+    // when the compiler evaluates both sides of the selects.)
+    const double num = __dmul_rn(k.lr, mh);
+    const double den = vh == 0.0 ? hp.eps : __dadd_rn(__dsqrt_rn(vh == 0.0 ? 1.0 : vh), hp.eps);
+    const double q = num == 0.0 ? num : __ddiv_rn(num == 0.0 ? 1.0 : num, den);
+    const double upd = __dsub_rn((double)p, q);
     p = (float)upd;
     m = (float)mm;
     v = (float)vv;
@@ -53,26 +62,58 @@ struct AdamCtl {
     int zero_grads;         // leave the gradient buffer zeroed for the next step
 };
 
-__global__ void __launch_bounds__(kThreads) k_adam_cloud(float* __restrict__ P, float* __restrict__ M,
+
+// Layout of the flat cloud buffers (scene.py field order): positions [0, 3n),
+// log_scales [3n, 6n), rotations [6n, 10n), sh [10n, 13n), opacity [13n, 14n);
+// the gradient buffer adds the densify statistics at [14n, 15n) and [15n, 16n).
+//
+// Blocks [0, nb_flat) run the elementwise update of the 10n non-rotation
+// scalars, kEpt per thread with every load issued before the FP64 math;
+// blocks [nb_flat, ...) take one Gaussian per thread: its quaternion (update +
+// normalize_rotations) and its densify statistics.
+template <int kEpt, int MINB>  // scalars per thread in the elementwise section; resident blocks
+__global__ void __launch_bounds__(kThreads, MINB) k_adam_cloud(float* __restrict__ P, float* __restrict__ M,
                                                          float* __restrict__ V,
                                                          float* __restrict__ Gr, int64_t n,
-                                                         uws_adam_params hp, AdamCtl ctl) {
-    const int64_t i = (int64_t)blockIdx.x * kThreads + threadIdx.x;
-    if (i >= n) return;
+                                                         int nb_flat, uws_adam_params hp,
+                                                         AdamCtl ctl) {
     const bool skip = ctl.skip && *ctl.skip > 0.0f;
-    if (skip) {
-        if (ctl.zero_grads) {
-            const int64_t base[5] = {0, 3 * n, 6 * n, 10 * n, 13 * n};
-            const int width[5] = {3, 3, 4, 3, 1};
+    if ((int)blockIdx.x < nb_flat) {
+        const int64_t n10 = 10 * n;
+        const int64_t t0 = (int64_t)blockIdx.x * kThreads * kEpt + threadIdx.x;
+        int64_t j[kEpt];
+        float p[kEpt], m[kEpt], v[kEpt], g[kEpt];
 #pragma unroll
-            for (int f = 0; f < 5; ++f)
-                for (int c = 0; c < width[f]; ++c) Gr[base[f] + i * width[f] + c] = 0.f;
-            Gr[14 * n + i] = 0.f;
-            Gr[15 * n + i] = 0.f;
+        for (int e = 0; e < kEpt; ++e) {
+            const int64_t t = t0 + e * kThreads;
+            j[e] = t < 6 * n ? t : t + 4 * n;  // skip the rotation block
+            if (t < n10 && !skip) {
+                p[e] = P[j[e]];
+                m[e] = M[j[e]];
+                v[e] = V[j[e]];
+                g[e] = Gr[j[e]];
+            }
+        }
+#pragma unroll
+        for (int e = 0; e < kEpt; ++e) {
+            const int64_t t = t0 + e * kThreads;
+            if (t >= n10) break;
+            if (!skip) {
+                const int f = j[e] < 3 * n ? 0 : (j[e] < 6 * n ? 1 : (j[e] < 13 * n ? 3 : 4));
+                const AdamK k{hp.lr[f], hp.bias1[f], hp.bias2[f], hp.inv_bias1[f],
+                              hp.inv_bias2[f]};
+                adam1(p[e], m[e], v[e], g[e], k, hp);
+                P[j[e]] = p[e];
+                M[j[e]] = m[e];
+                V[j[e]] = v[e];
+            }
+            if (ctl.zero_grads) Gr[j[e]] = 0.f;
         }
         return;
     }
-    if (ctl.grad_accum) {
+    const int64_t i = (int64_t)(blockIdx.x - nb_flat) * kThreads + threadIdx.x;
+    if (i >= n) return;
+    if (!skip && ctl.grad_accum) {
         ctl.grad_accum[i] += Gr[14 * n + i];
         ctl.obs_count[i] += (int32_t)Gr[15 * n + i];
     }
@@ -80,38 +121,39 @@ __global__ void __launch_bounds__(kThreads) k_adam_cloud(float* __restrict__ P, 
         Gr[14 * n + i] = 0.f;
         Gr[15 * n + i] = 0.f;
     }
-    const int64_t base[5] = {0, 3 * n, 6 * n, 10 * n, 13 * n};
-    const int width[5] = {3, 3, 4, 3, 1};
+    const int64_t o = 6 * n + 4 * i;
+    if (skip) {
+        if (ctl.zero_grads)
 #pragma unroll
-    for (int f = 0; f < 5; ++f) {
-        const AdamK k{hp.lr[f], hp.bias1[f], hp.bias2[f], hp.inv_bias1[f], hp.inv_bias2[f]};
-        float q[4];
-#pragma unroll
-        for (int c = 0; c < 4; ++c) {
-            if (c >= width[f]) break;
-            const int64_t o = base[f] + i * width[f] + c;
-            float p = P[o], m = M[o], v = V[o];
-            adam1(p, m, v, Gr[o], k, hp);
-            if (ctl.zero_grads) Gr[o] = 0.f;
-            q[c] = p;
-            M[o] = m;
-            V[o] = v;
-            if (f != 2) P[o] = p;
-        }
-        if (f == 2) {
-            // normalize_rotations: q / max(|q|, 1e-12) in float64, stored float32
-            const double a = q[0], b = q[1], c = q[2], d = q[3];
-            double nr = __dsqrt_rn(__dadd_rn(__dadd_rn(__dadd_rn(__dmul_rn(a, a), __dmul_rn(b, b)),
-                                                      __dmul_rn(c, c)),
-                                             __dmul_rn(d, d)));
-            nr = fmax(nr, 1e-12);
-            const int64_t o = base[2] + i * 4;
-            P[o + 0] = (float)__ddiv_rn(a, nr);
-            P[o + 1] = (float)__ddiv_rn(b, nr);
-            P[o + 2] = (float)__ddiv_rn(c, nr);
-            P[o + 3] = (float)__ddiv_rn(d, nr);
-        }
+            for (int c = 0; c < 4; ++c) Gr[o + c] = 0.f;
+        return;
     }
+    float p[4], m[4], v[4], g[4];
+#pragma unroll
+    for (int c = 0; c < 4; ++c) {
+        p[c] = P[o + c];
+        m[c] = M[o + c];
+        v[c] = V[o + c];
+        g[c] = Gr[o + c];
+    }
+    const AdamK k{hp.lr[2], hp.bias1[2], hp.bias2[2], hp.inv_bias1[2], hp.inv_bias2[2]};
+#pragma unroll
+    for (int c = 0; c < 4; ++c) {
+        adam1(p[c], m[c], v[c], g[c], k, hp);
+        M[o + c] = m[c];
+        V[o + c] = v[c];
+        if (ctl.zero_grads) Gr[o + c] = 0.f;
+    }
+    // normalize_rotations: q / max(|q|, 1e-12) in float64, stored float32
+    const double a = p[0], b = p[1], c = p[2], d = p[3];
+    double nr = __dsqrt_rn(__dadd_rn(__dadd_rn(__dadd_rn(__dmul_rn(a, a), __dmul_rn(b, b)),
+                                              __dmul_rn(c, c)),
+                                     __dmul_rn(d, d)));
+    nr = fmax(nr, 1e-12);
+    P[o + 0] = (float)__ddiv_rn(a, nr);
+    P[o + 1] = (float)__ddiv_rn(b, nr);
+    P[o + 2] = (float)__ddiv_rn(c, nr);
+    P[o + 3] = (float)__ddiv_rn(d, nr);
 }
 
 __global__ void k_adam_medium(float* __restrict__ P, float* __restrict__ M, float* __restrict__ V,
@@ -166,8 +208,11 @@ extern "C" int uws_adam_step(float* params, float* exp_avg, float* exp_avg_sq, f
     }
     if (n > 0) {
         UWS_REQUIRE(params && exp_avg && exp_avg_sq && grads, "uws_adam_step: null cloud buffer");
-        k_adam_cloud<<<(unsigned)ceil_div(n, kThreads), kThreads, 0, st>>>(params, exp_avg, exp_avg_sq,
-                                                                           grads, n, *hp, ctl);
+        constexpr int kEpt = 2;
+        const int nb_flat = (int)ceil_div(10 * n, kThreads * kEpt);
+        const int nb_rot = (int)ceil_div(n, kThreads);
+        k_adam_cloud<kEpt, 4><<<(unsigned)(nb_flat + nb_rot), kThreads, 0, st>>>(
+            params, exp_avg, exp_avg_sq, grads, n, nb_flat, *hp, ctl);
         UWS_CHECK_LAUNCH("k_adam_cloud");
     }
     if (medium_params && zero_grads) {
