@@ -155,14 +155,28 @@ __global__ void __launch_bounds__(kThreads) k_onesweep(const K* __restrict__ key
             st_volatile(&status[b], kStInc | cnt);
         } else {
             st_volatile(&status[(size_t)tile * kBins + b], kStAgg | cnt);
+            // look back kLook predecessors per round trip: sum aggregates up to
+            // the nearest inclusive prefix, re-poll from the first unpublished one
+            constexpr int kLook = 8;
             int j = tile - 1;
             while (true) {
-                uint32_t s = ld_volatile(&status[(size_t)j * kBins + b]);
-                uint32_t f = s >> 30;
-                if (f == 0) continue;
-                excl += s & kStMask;
-                if (f == 2) break;
-                --j;
+                uint32_t sv[kLook];
+#pragma unroll
+                for (int q = 0; q < kLook; ++q)
+                    sv[q] = j - q >= 0 ? ld_volatile(&status[(size_t)(j - q) * kBins + b]) : kStInc;
+                int used = 0;
+                bool done = false;
+#pragma unroll
+                for (int q = 0; q < kLook; ++q) {
+                    if (done || used < q) break;  // stop at the first gap
+                    const uint32_t f = sv[q] >> 30;
+                    if (f == 0) break;
+                    excl += sv[q] & kStMask;
+                    used = q + 1;
+                    if (f == 2) done = true;
+                }
+                if (done) break;
+                j -= used;
             }
             st_volatile(&status[(size_t)tile * kBins + b], kStInc | (excl + cnt));
         }
