@@ -30,6 +30,9 @@ constexpr int kPix = 4;                          // pixels per thread
 constexpr int kThreads = kRasterThreads / kPix;  // 64
 constexpr int kWarps = kThreads / 32;            // 2
 constexpr int kBandRows = kTile / kWarps;        // each warp owns an 8-row band of the tile
+// the clamp guard band as |araw - mid| < half (a slightly wider superset of [kClampLo, kClampHi))
+constexpr float kClampMid = 0.5f * (kClampLo + kClampHi);
+constexpr float kClampHalf = 0.51f * (kClampHi - kClampLo);
 
 struct BwdArgs {
     const uws_splat* splat;
@@ -242,7 +245,7 @@ __global__ void __launch_bounds__(kThreads, MINB) k_raster_bwd(BwdArgs a) {
                     const float araw = B.op * ex2_ftz(power);
                     if (araw < kFloorLo) continue;
                     bool unclamped = araw < kClampLo;
-                    if (araw < kFloorHi || (araw >= kClampLo && araw < kClampHi)) {
+                    if (araw < kFloorHi || fabsf(araw - kClampMid) < kClampHalf) {
                         // guard band: re-decide both gates from the float64 record
                         const double e = alpha_raw_f64_cold(a.splat, a.exact, C.row, ox + lx,
                                                             oy + ly0 + 2 * p);
