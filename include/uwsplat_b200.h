@@ -209,8 +209,10 @@ int uws_preprocess_bwd(const uws_cloud* cloud, const uws_camera* cam, const uws_
  *      floats (medium_grads = grads + 16n).  Optional step control for the
  *      device-resident training loop (pipeline.py:182-192): skip (device
  *      float) > 0 turns the update into a no-op; grad_accum/obs_count
- *      receive the densification statistics; zero_grads leaves the whole
- *      gradient buffer zeroed for the next step. --------------------- */
+ *      receive the densification statistics; zero_grads leaves the
+ *      gradient buffer zeroed for the next step except the skip counter
+ *      (medium_grads[9]), which stays set after a skip so that steps already
+ *      queued behind it skip as well, until the caller clears it. ------ */
 int uws_adam_step(float* params, float* exp_avg, float* exp_avg_sq, float* grads, int64_t n,
                   float* medium_params, float* medium_exp_avg, float* medium_exp_avg_sq,
                   float* medium_grads, const uws_adam_params* hp, const float* skip,

@@ -216,8 +216,11 @@ extern "C" int uws_adam_step(float* params, float* exp_avg, float* exp_avg_sq, f
         UWS_CHECK_LAUNCH("k_adam_cloud");
     }
     if (medium_params && zero_grads) {
-        // medium slots + counter/pad (16 floats) zeroed after every reader is done
-        UWS_CUDA(cudaMemsetAsync(medium_grads, 0, 16 * sizeof(float), st));
+        // medium slots and pad zeroed after every reader is done; the skip
+        // counter (slot 9) is left alone: non-zero it keeps skipping later
+        // steps until the host has handled the skip and cleared it
+        UWS_CUDA(cudaMemsetAsync(medium_grads, 0, 9 * sizeof(float), st));
+        UWS_CUDA(cudaMemsetAsync(medium_grads + 10, 0, 6 * sizeof(float), st));
     }
     return UWS_OK;
 }

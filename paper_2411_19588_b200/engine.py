@@ -32,6 +32,7 @@ import logging
 from dataclasses import dataclass
 from typing import Sequence
 
+import numpy as np
 import torch
 
 from . import _lib
@@ -100,8 +101,13 @@ class StepEngine:
         self.screen = torch.zeros(max(n, 1), 9, dtype=torch.float32, device=dev)
         self.med_acc = torch.zeros(9, dtype=torch.float64, device=dev)
         self.grads = GradientBuffer(n, dev)
-        self.stats = torch.zeros(max_views * _ST_SIZE + 2, dtype=torch.float64, device=dev)
-        self.stats_host = torch.zeros_like(self.stats, device="cpu").pin_memory()
+        # two in-flight step slots: stats record (device + pinned host copy + event) and
+        # device copies of host ground-truth images
+        self._slots = [_Slot(max_views, dev) for _ in range(2)]
+        self._render_stats = torch.zeros(_ST_SIZE + 2, dtype=torch.float64, device=dev)
+        self._k = 0
+        self._pending = None
+        self.copy_stream = torch.cuda.Stream(device=dev)
 
     # -- capacity management ---------------------------------------------------
     def _set_capacity(self, s_cap: int):
@@ -112,13 +118,14 @@ class StepEngine:
         self.row_items = torch.empty(self.s_cap, 2, dtype=torch.int32, device=self.dev)
 
     # -- forward of one view (render path) ----------------------------------------
-    def _forward(self, cam: Camera, slot: int, mode: str = "underwater", train: bool = True):
+    def _forward(self, cam: Camera, stats: torch.Tensor, view: int, mode: str = "underwater",
+                 train: bool = True):
         st = _lib.stream_handle()
         cloud, medium = self.state.cloud, self.state.medium
         cc = cam.c_struct()
         preprocess_into(self.proj, cloud, cam, self.pre_ws)
         pc = self.proj.c_struct()
-        rec = self.stats[slot * _ST_SIZE:(slot + 1) * _ST_SIZE]
+        rec = stats[view * _ST_SIZE:(view + 1) * _ST_SIZE]
         totals = rec[_ST_TOTALS:_ST_TOTALS + 2].view(torch.int64)
         ovf = rec[_ST_OVF:_ST_OVF + 1].view(torch.int32)[:1]
         _lib.call("uws_bin_count", ctypes.byref(pc), self.n, ctypes.byref(cc), _lib.ptr(totals),
@@ -139,9 +146,9 @@ class StepEngine:
         Overflow of the row-list capacity is detected and the view re-run."""
         cam = Camera.from_any(cam)
         for _ in range(4):
-            self.stats.zero_()
-            self._forward(cam, 0, mode, train=False)
-            rec = self.stats[0:_ST_SIZE]
+            self._render_stats.zero_()
+            self._forward(cam, self._render_stats, 0, mode, train=False)
+            rec = self._render_stats[0:_ST_SIZE]
             if int(rec[_ST_OVF:_ST_OVF + 1].view(torch.int32)[0]) == 0:
                 break
             need_s = int(rec[_ST_TOTALS:_ST_TOTALS + 2].view(torch.int64)[1])
@@ -150,10 +157,10 @@ class StepEngine:
         return self.last_render()
 
     # -- one view: forward + loss + backward into self.grads -----------------------
-    def _view(self, cam: Camera, gt: torch.Tensor, slot: int):
+    def _view(self, cam: Camera, gt: torch.Tensor, stats: torch.Tensor, view: int):
         st = _lib.stream_handle()
         cloud, medium = self.state.cloud, self.state.medium
-        cc, pc, oc, rec = self._forward(cam, slot)
+        cc, pc, oc, rec = self._forward(cam, stats, view)
         out = self.out
         total_loss_device(out.color, gt, medium, self.cfg.lambda_ssim, self.cfg.lambda_guide,
                           result=rec[_ST_LOSS:_ST_LOSS + 6], grad=self.dL, workspace=self.loss_ws,
@@ -177,48 +184,141 @@ class StepEngine:
         out.bins = None
         return out
 
-    def _launch(self, views: Sequence):
+    # -- ground truth staging -------------------------------------------------------
+    def _stage(self, views: Sequence, slot: "_Slot"):
+        """Device views for a step: host images are copied into the slot's
+        device buffers on the copy stream (overlapping the previous step's
+        kernels); device images are used in place."""
         if len(views) > self.max_views:
             raise ValueError(f"at most {self.max_views} views per step on this engine")
+        out = []
+        cs = self.copy_stream
+        cs.wait_event(slot.free)        # the slot's previous step no longer reads them
         for i, (cam, gt) in enumerate(views):
-            self._view(Camera.from_any(cam), gt, i)
+            cam = Camera.from_any(cam)
+            if isinstance(gt, torch.Tensor) and gt.is_cuda:
+                out.append((cam, gt.float()))
+                continue
+            src = gt if isinstance(gt, torch.Tensor) else torch.from_numpy(
+                np.ascontiguousarray(gt, dtype=np.float32))
+            buf = slot.gt_buffer(i, (self.height, self.width, 3))
+            with torch.cuda.stream(cs):
+                buf.copy_(src, non_blocking=True)
+            out.append((cam, buf))
+        slot.copied.record(cs)
+        return out
+
+    def _launch(self, slot: "_Slot"):
+        cur = torch.cuda.current_stream()
+        cur.wait_event(slot.copied)
+        for i, (cam, gt) in enumerate(slot.views):
+            self._view(cam, gt, slot.stats, i)
         if self.dist is not None and self.world > 1:
             # one NCCL all-reduce of [grads | medium | skip counter | pad]
             self.dist.all_reduce(self.grads.flat, group=self.group)
-        # the skip counter is consumed (zeroed) by the Adam launch: keep a copy
-        self.stats[-1:].copy_(self.grads.nonfinite)
+        # the skip counter is read by the Adam launch (and kept while non-zero): keep a copy
+        slot.stats[-1:].copy_(self.grads.nonfinite)
+        saved = self.state.iteration
+        self.state.iteration = slot.iteration
         apply_gradients_device(self.state, self.grads, self.cfg, self.spatial_scale)
-        self.stats_host.copy_(self.stats, non_blocking=True)
+        self.state.iteration = saved
+        slot.host.copy_(slot.stats, non_blocking=True)
+        slot.done.record(cur)
+        slot.free.record(cur)
 
-    def step(self, views: Sequence) -> EngineStats:
-        """One optimizer step over this rank's (camera, gt-on-device) views.
+    def _read(self, slot: "_Slot"):
+        slot.done.synchronize()
+        s = slot.host
+        nv = len(slot.views)
+        need_e = need_s = 0
+        for i in range(nv):
+            tot = s[i * _ST_SIZE + _ST_TOTALS:i * _ST_SIZE + _ST_TOTALS + 2].view(torch.int64)
+            need_e = max(need_e, int(tot[0]))   # tile entries (reported only)
+            need_s = max(need_s, int(tot[1]))   # row-list items (capacity)
+        return float(s[-1]), need_e, need_s
 
-        Loss values in the returned stats are this rank's view averages."""
-        reruns = 0
-        nv = len(views)
-        while True:
-            self._launch(views)
-            torch.cuda.current_stream().synchronize()
-            s = self.stats_host
-            skip_count = float(s[-1])
-            skipped = skip_count > 0
-            need_e = need_s = 0
-            for i in range(nv):
-                tot = s[i * _ST_SIZE + _ST_TOTALS:i * _ST_SIZE + _ST_TOTALS + 2].view(torch.int64)
-                need_e = max(need_e, int(tot[0]))   # tile entries (reported only)
-                need_s = max(need_s, int(tot[1]))   # row-list items (capacity)
-            if skipped:
-                rollback_steps(self.state)
-            if skip_count >= 65536.0 and reruns < 3:
-                # some rank's tile lists overflowed: every rank re-runs the step
-                if need_s > self.s_cap:
-                    self._set_capacity(int(need_s * 1.25) + 1024)
-                reruns += 1
-                continue
-            break
+    def _stats(self, slot: "_Slot", skipped: bool, reruns: int, need_e: int) -> EngineStats:
+        s, nv = slot.host, len(slot.views)
         loss = [sum(float(s[i * _ST_SIZE + j]) for i in range(nv)) / max(nv, 1) for j in range(4)]
         if skipped:
             log.warning("iteration %d: non-finite loss or gradients, skipping update",
-                        self.state.iteration)
+                        slot.iteration)
         return EngineStats(loss[0], loss[1], loss[2], loss[3], nv * self.world, skipped, reruns,
                            need_e)
+
+    def _finalize(self, slot: "_Slot") -> EngineStats:
+        """Read a launched step's record.  A step the device skipped (non-finite
+        values or a row-list overflow on any rank) leaves the skip counter set,
+        which also turns every later launched step into a no-op; the host then
+        undoes their step-counter advances, clears the counter, re-runs an
+        overflowed step with grown lists and re-launches the later step."""
+        skip_count, need_e, need_s = self._read(slot)
+        if skip_count == 0:
+            return self._stats(slot, False, 0, need_e)
+        nxt = self._pending if self._pending is not slot else None
+        torch.cuda.current_stream().synchronize()
+        rollback_steps(self.state)
+        if nxt is not None:
+            rollback_steps(self.state)
+        self.grads.nonfinite.zero_()
+        reruns = 0
+        while skip_count >= 65536.0 and reruns < 3:
+            if need_s > self.s_cap:
+                self._set_capacity(int(need_s * 1.25) + 1024)
+            reruns += 1
+            self._launch(slot)
+            skip_count, need_e, need_s = self._read(slot)
+            if skip_count > 0:
+                rollback_steps(self.state)
+                self.grads.nonfinite.zero_()
+        st = self._stats(slot, skip_count > 0, reruns, need_e)
+        if nxt is not None:
+            self._launch(nxt)
+        return st
+
+    # -- public stepping ---------------------------------------------------------------
+    def step_async(self, views: Sequence):
+        """Launch one optimizer step over this rank's (camera, gt) views without
+        waiting for it; ground-truth images may be host arrays (copied on a side
+        stream while the previous step runs) or device tensors.  Returns the
+        stats of the previously launched step (None for the first)."""
+        slot = self._slots[self._k % 2]
+        self._k += 1
+        slot.views = self._stage(views, slot)
+        slot.iteration = self.state.iteration
+        self._launch(slot)
+        prev, self._pending = self._pending, slot
+        return self._finalize(prev) if prev is not None else None
+
+    def flush(self):
+        """Wait for the last launched step and return its stats (None if none)."""
+        slot, self._pending = self._pending, None
+        return self._finalize(slot) if slot is not None else None
+
+    def step(self, views: Sequence) -> EngineStats:
+        """One optimizer step over this rank's views, synchronously.
+
+        Loss values in the returned stats are this rank's view averages."""
+        self.step_async(views)
+        return self.flush()
+
+
+class _Slot:
+    """Per in-flight step: stats record, its pinned host copy and events, and
+    device buffers for host ground-truth images."""
+
+    def __init__(self, max_views: int, dev):
+        self.stats = torch.zeros(max_views * _ST_SIZE + 2, dtype=torch.float64, device=dev)
+        self.host = torch.zeros_like(self.stats, device="cpu").pin_memory()
+        self.done = torch.cuda.Event()
+        self.copied = torch.cuda.Event()
+        self.free = torch.cuda.Event()
+        self.gt = []
+        self.views = []
+        self.iteration = 0
+        self._dev = dev
+
+    def gt_buffer(self, i: int, shape):
+        while len(self.gt) <= i:
+            self.gt.append(torch.empty(shape, dtype=torch.float32, device=self._dev))
+        return self.gt[i]

@@ -135,10 +135,14 @@ class ViewShardedTrainer:
         the global batch (sharded here) unless ``sharded=True``.  Ground-truth
         images may be host arrays or device tensors."""
         mine = views if sharded else self.shard(views)
-        dev = self.state.cloud.device
-        prepared = []
-        for cam, gt in mine:
-            if not (isinstance(gt, torch.Tensor) and gt.is_cuda):
-                gt = torch.as_tensor(gt, dtype=torch.float32).to(dev, non_blocking=True)
-            prepared.append((cam, gt.float()))
-        return self.engine.step(prepared)
+        return self.engine.step(mine)
+
+    def step_async(self, views: Sequence, sharded: bool = False):
+        """Pipelined form of :meth:`step`: launches this step (host images are
+        copied on a side stream while the previous step's kernels run) and
+        returns the stats of the previous one; :meth:`flush` returns the last."""
+        mine = views if sharded else self.shard(views)
+        return self.engine.step_async(mine)
+
+    def flush(self):
+        return self.engine.flush()
