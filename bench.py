@@ -261,6 +261,32 @@ def run_gpu(args):
     ms_e2e, _ = timed(step_e2e, args.steps)
     trainer.flush()
 
+    # render FPS (BASELINE.json's second metric): the forward alone -- preprocess,
+    # depth sort, tile-row lists, compositing with the medium epilogue -- per frame
+    # through StepEngine.render (one host read of the overflow flag per frame), at C3
+    # and at C5's 1M Gaussians @ 3840x2160
+    render_fps = {}
+    for name, (rw, rh) in (("C3 1M 1920x1080", (W, H)), ("C5 1M 3840x2160", (3840, 2160))):
+        eng = trainer.engine if (rw, rh) == (W, H) else uw.StepEngine(state, rw, rh, cfg)
+        rcam = uw.Camera.look_at(view_eye(rank), (0, 0, 12), width=rw, height=rh,
+                                 fx=1.2 * rw, fy=1.2 * rw)
+        for _ in range(3):
+            eng.render(rcam)
+        nfr = max(args.steps, 10)
+        barrier()
+        t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        t0.record()
+        for _ in range(nfr):
+            eng.render(rcam)
+        t1.record()
+        barrier()
+        fms = t0.elapsed_time(t1) / nfr
+        render_fps[name] = {"fps": round(1e3 / fms, 1), "ms_per_frame": round(fms, 4),
+                            "mpix_per_s": round(rw * rh / fms / 1e3, 1)}
+        if eng is not trainer.engine:
+            del eng
+    torch.cuda.empty_cache()
+
     px_step = W * H * world
     value = px_step * args.steps / (ms / 1e3) / 1e6
     e2e = px_step * args.steps / (ms_e2e / 1e3) / 1e6
@@ -352,6 +378,7 @@ def run_gpu(args):
                 "h2d_bytes_per_step": H * W * 3 * 4,
                 "d2h_bytes_per_step": 4 + 8 + 7 * 8},
         "gpu_launches": int(launches),
+        "render_fps": render_fps,
         "roofline": roofline,
         "stages_ms": {k: round(v, 4) for k, v in per_step.items()},
         "stage_share": stage_share,
