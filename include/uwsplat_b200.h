@@ -218,6 +218,27 @@ int uws_adam_step(float* params, float* exp_avg, float* exp_avg_sq, float* grads
                   float* medium_grads, const uws_adam_params* hp, const float* skip,
                   float* grad_accum, int32_t* obs_count, int32_t zero_grads, void* stream);
 
+/* ---- densification (replaces optim.densify_and_prune :132-198 and
+ *      reset_opacities :201-207).  Two phases around one host read: classify
+ *      writes totals[3] = {n_keep, n_clone, n_split} (device int64) so the
+ *      caller can size the new buffers and draw the split samples
+ *      ([2][n_split][3] float64, standard normal, from its own generator, in
+ *      the reference's order); apply writes the new cloud / moments
+ *      (n_keep + n_clone + 2 n_split rows; moment buffers must be zeroed by the
+ *      caller: only kept rows are written).  Same workspace for both. ---- */
+int uws_densify_workspace_size(int64_t n, size_t* bytes);
+int uws_densify_classify(const float* params, int64_t n, const float* grad_accum,
+                         const int32_t* obs_count, double grad_threshold, double size_threshold,
+                         double min_opacity, int64_t* totals, void* workspace,
+                         size_t workspace_bytes, void* stream);
+int uws_densify_apply(const float* params, const float* exp_avg, const float* exp_avg_sq,
+                      int64_t n, const void* workspace, size_t workspace_bytes,
+                      const double* samples, double log_split_factor, int64_t n_keep,
+                      int64_t n_clone, int64_t n_split, float* new_params, float* new_exp_avg,
+                      float* new_exp_avg_sq, void* stream);
+int uws_reset_opacities(float* params, float* exp_avg, float* exp_avg_sq, int64_t n, float value,
+                        void* stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -672,3 +672,52 @@ def clamp_medium(att, wat, bsc):
     return (np.maximum(att, np.float32(0.0)).astype(np.float32),
             np.clip(wat, 0.0, 1.0).astype(np.float32),
             np.clip(bsc, 0.0, 5.0).astype(np.float32))
+
+
+def densify_and_prune(arrays, m, v, grad_accum, obs_count, extent, rng,
+                      grad_threshold=0.0002, percent_dense=0.01, min_opacity=0.1,
+                      split_scale_factor=1.6):
+    """Clone / split / prune (optim.py:132-198) on plain arrays.
+
+    ``arrays``/``m``/``v`` map the five cloud fields to (n, ...) float32 arrays.
+    Returns (new_arrays, new_m, new_v, (clones, splits, pruned)); nothing
+    changes when the cloud would be emptied (optim.py:160-161).
+    """
+    n = arrays["positions"].shape[0]
+    denom = np.maximum(obs_count.astype(np.float64), 1.0)                       # :143
+    mean_grad = grad_accum.astype(np.float64) / denom                           # :144
+    candidate = (mean_grad > grad_threshold) & (obs_count > 0)                  # :145
+    max_scale = np.exp(arrays["log_scales"].astype(np.float64)).max(axis=1)     # :147
+    small = max_scale <= percent_dense * extent                                 # :148
+    prune = _sigmoid(arrays["opacity_logits"]) < min_opacity                    # :153-154
+    clone = candidate & small & ~prune                                          # :149, 155
+    split = candidate & ~small & ~prune                                         # :150, 156
+    keep = ~(prune | split)                                                     # :157
+    if not keep.any() and not split.any():
+        return arrays, m, v, (0, 0, 0)
+    fields = ("positions", "log_scales", "rotations", "sh_coeffs", "opacity_logits")
+    parts = {f: [arrays[f][keep], arrays[f][clone]] for f in fields}            # :161-166
+    n_split = int(split.sum())
+    if n_split:                                                                 # :168-182
+        idx = np.nonzero(split)[0]
+        R = rotmat_from_quat(arrays["rotations"][idx])
+        s = np.exp(arrays["log_scales"][idx].astype(np.float64))
+        samples = rng.standard_normal((2, n_split, 3))
+        for half in range(2):
+            vec = samples[half] * s
+            offs = np.empty((n_split, 3))
+            for r in range(3):   # einsum("nij,nj->ni"): ((R0 v0 + R1 v1) + R2 v2)
+                offs[:, r] = (R[:, r, 0] * vec[:, 0] + R[:, r, 1] * vec[:, 1]) + R[:, r, 2] * vec[:, 2]
+            parts["positions"].append(
+                (arrays["positions"][idx].astype(np.float64) + offs).astype(np.float32))
+            parts["log_scales"].append((arrays["log_scales"][idx].astype(np.float64)
+                                        - np.log(split_scale_factor)).astype(np.float32))
+            for f in ("rotations", "sh_coeffs", "opacity_logits"):
+                parts[f].append(arrays[f][idx])
+    new = {f: np.concatenate(parts[f]).astype(np.float32) for f in fields}     # :184-186
+    n_added = int(clone.sum()) + 2 * n_split                                    # :190-195
+    new_m = {f: np.concatenate([m[f][keep], np.zeros((n_added,) + m[f].shape[1:], np.float32)])
+             for f in fields}
+    new_v = {f: np.concatenate([v[f][keep], np.zeros((n_added,) + v[f].shape[1:], np.float32)])
+             for f in fields}
+    return new, new_m, new_v, (int(clone.sum()), n_split, int(prune.sum()))

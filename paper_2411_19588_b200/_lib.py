@@ -9,7 +9,8 @@ from __future__ import annotations
 
 import ctypes
 import os
-from ctypes import POINTER, c_char_p, c_double, c_int, c_int16, c_int32, c_int64, c_size_t, c_void_p
+from ctypes import (POINTER, c_char_p, c_double, c_float, c_int, c_int16, c_int32, c_int64,
+                    c_size_t, c_void_p)
 
 import torch
 
@@ -87,6 +88,13 @@ _SIGS = {
     "uws_adam_step": (c_int, [c_void_p, c_void_p, c_void_p, c_void_p, c_int64, c_void_p,
                               c_void_p, c_void_p, c_void_p, POINTER(AdamParamsC), c_void_p,
                               c_void_p, c_void_p, c_int32, c_void_p]),
+    "uws_densify_workspace_size": (c_int, [c_int64, POINTER(c_size_t)]),
+    "uws_densify_classify": (c_int, [c_void_p, c_int64, c_void_p, c_void_p, c_double, c_double,
+                                     c_double, c_void_p, c_void_p, c_size_t, c_void_p]),
+    "uws_densify_apply": (c_int, [c_void_p, c_void_p, c_void_p, c_int64, c_void_p, c_size_t,
+                                  c_void_p, c_double, c_int64, c_int64, c_int64, c_void_p,
+                                  c_void_p, c_void_p, c_void_p]),
+    "uws_reset_opacities": (c_int, [c_void_p, c_void_p, c_void_p, c_int64, c_float, c_void_p]),
 }
 
 EXPORTED = tuple(_SIGS)

@@ -80,10 +80,31 @@ class StepEngine:
         self.dist = dist if dist.is_available() and dist.is_initialized() else None
         self.world = self.dist.get_world_size(group) if self.dist else 1
         self.rank = self.dist.get_rank(group) if self.dist else 0
-        n = len(state.cloud)
         dev = state.cloud.device
-        self.n, self.dev = n, dev
+        self.dev = dev
         self.gx, self.gy = (width + 15) // 16, (height + 15) // 16
+        self.row_start = torch.zeros(self.gy + 1, dtype=torch.int32, device=dev)
+        self.out = _alloc_output(height, width, dev, "underwater", False)
+        self.dL = torch.empty(height, width, 3, dtype=torch.float32, device=dev)
+        b = _lib.size_out()
+        _lib.call("uws_loss_workspace_size", height, width, 3, ctypes.byref(b))
+        self.loss_ws = torch.empty(b.value, dtype=torch.uint8, device=dev)
+        self.med_acc = torch.zeros(9, dtype=torch.float64, device=dev)
+        self._entry_capacity = entry_capacity
+        self._alloc(len(state.cloud))
+        # two in-flight step slots: stats record (device + pinned host copy + event) and
+        # device copies of host ground-truth images
+        self._slots = [_Slot(max_views, dev) for _ in range(2)]
+        self._render_stats = torch.zeros(_ST_SIZE + 2, dtype=torch.float64, device=dev)
+        self._k = 0
+        self._pending = None
+        self.copy_stream = torch.cuda.Stream(device=dev)
+
+    def _alloc(self, n: int):
+        """Buffers sized by the number of Gaussians (re-done after densification)."""
+        dev = self.dev
+        self.n = n
+        self.generation = self.state.cloud.generation
         self.proj = ProjectedCloud(n, dev, with_geometry=False)
         b = _lib.size_out()
         _lib.call("uws_preprocess_workspace_size", n, ctypes.byref(b))
@@ -92,22 +113,18 @@ class StepEngine:
         _lib.call("uws_bin_workspace_size", n, 0, self.gx, self.gy, ctypes.byref(cb),
                   ctypes.byref(eb))
         self.count_ws = torch.empty(max(cb.value, 1), dtype=torch.uint8, device=dev)
-        self.row_start = torch.zeros(self.gy + 1, dtype=torch.int32, device=dev)
-        self._set_capacity(entry_capacity or 12 * n)
-        self.out = _alloc_output(height, width, dev, "underwater", False)
-        self.dL = torch.empty(height, width, 3, dtype=torch.float32, device=dev)
-        _lib.call("uws_loss_workspace_size", height, width, 3, ctypes.byref(b))
-        self.loss_ws = torch.empty(b.value, dtype=torch.uint8, device=dev)
+        self._set_capacity(self._entry_capacity or 12 * n)
         self.screen = torch.zeros(max(n, 1), 9, dtype=torch.float32, device=dev)
-        self.med_acc = torch.zeros(9, dtype=torch.float64, device=dev)
         self.grads = GradientBuffer(n, dev)
-        # two in-flight step slots: stats record (device + pinned host copy + event) and
-        # device copies of host ground-truth images
-        self._slots = [_Slot(max_views, dev) for _ in range(2)]
-        self._render_stats = torch.zeros(_ST_SIZE + 2, dtype=torch.float64, device=dev)
-        self._k = 0
-        self._pending = None
-        self.copy_stream = torch.cuda.Stream(device=dev)
+
+    def _sync_cloud(self):
+        """Follow a topology change of the cloud (densify_and_prune)."""
+        cloud = self.state.cloud
+        if len(cloud) != self.n or cloud.generation != self.generation:
+            if self._pending is not None:
+                raise RuntimeError("the cloud changed while a step was in flight: call "
+                                   "flush() before densify_and_prune")
+            self._alloc(len(cloud))
 
     # -- capacity management ---------------------------------------------------
     def _set_capacity(self, s_cap: int):
@@ -145,6 +162,8 @@ class StepEngine:
         """Render-only path (no host sync before the caller reads the image).
         Overflow of the row-list capacity is detected and the view re-run."""
         cam = Camera.from_any(cam)
+        if self._pending is None:
+            self._sync_cloud()
         for _ in range(4):
             self._render_stats.zero_()
             self._forward(cam, self._render_stats, 0, mode, train=False)
@@ -256,6 +275,9 @@ class StepEngine:
         if skip_count == 0:
             return self._stats(slot, False, 0, need_e)
         nxt = self._pending if self._pending is not slot else None
+        if self.state.cloud.generation != self.generation:
+            raise RuntimeError("a skipped step cannot be re-run after the cloud changed: "
+                               "call flush() before densify_and_prune")
         torch.cuda.current_stream().synchronize()
         rollback_steps(self.state)
         if nxt is not None:
@@ -282,6 +304,7 @@ class StepEngine:
         waiting for it; ground-truth images may be host arrays (copied on a side
         stream while the previous step runs) or device tensors.  Returns the
         stats of the previously launched step (None for the first)."""
+        self._sync_cloud()
         slot = self._slots[self._k % 2]
         self._k += 1
         slot.views = self._stage(views, slot)

@@ -154,3 +154,61 @@ def rollback_steps(state: TrainState) -> None:
     """Undo the step-counter advance of a skipped update (pipeline.py:182-189)."""
     for slot in state.adam.values():
         slot.step -= 1
+
+
+def densify_and_prune(state: TrainState, cfg: OptimConfig, scene_extent: float, rng):
+    """Clone/split high-gradient Gaussians, prune transparent ones, on the device
+    (reference optim.py:132-198; same arguments, return value and random draws).
+
+    One host read of the three counts sizes the new buffers; the split samples
+    come from ``rng.standard_normal((2, n_split, 3))`` exactly as in the
+    reference so a shared seed reproduces its cloud.  Returns
+    (clones, splits, pruned).  A StepEngine driving this state must be
+    flushed first (``engine.flush()``): it resizes itself on its next step.
+    """
+    import numpy as np
+    cloud = state.cloud
+    n = len(cloud)
+    if n == 0:
+        return 0, 0, 0
+    dev = cloud.device
+    st = _lib.stream_handle()
+    b = _lib.size_out()
+    _lib.call("uws_densify_workspace_size", n, ctypes.byref(b))
+    ws = torch.empty(max(b.value, 1), dtype=torch.uint8, device=dev)
+    totals = torch.zeros(3, dtype=torch.int64, device=dev)
+    _lib.call("uws_densify_classify", _lib.ptr(cloud.flat), n, _lib.ptr(state.grad_accum),
+              _lib.ptr(state.obs_count), float(cfg.densify_grad_threshold),
+              float(cfg.percent_dense * scene_extent), float(cfg.min_opacity), _lib.ptr(totals),
+              _lib.ptr(ws), ws.numel(), st)
+    n_keep, n_clone, n_split = (int(v) for v in totals.cpu())
+    n_prune = n - n_keep - n_split
+    if n_keep == 0 and n_split == 0:
+        return 0, 0, 0  # refuse to empty the cloud (optim.py:160-161)
+    samples = None
+    if n_split:
+        draw = np.ascontiguousarray(rng.standard_normal((2, n_split, 3)), dtype=np.float64)
+        samples = torch.from_numpy(draw).to(dev)
+    n_new = n_keep + n_clone + 2 * n_split
+    flat = torch.empty(14 * n_new, dtype=torch.float32, device=dev)
+    m = torch.zeros(14 * n_new, dtype=torch.float32, device=dev)
+    v = torch.zeros(14 * n_new, dtype=torch.float32, device=dev)
+    _lib.call("uws_densify_apply", _lib.ptr(cloud.flat), _lib.ptr(state.exp_avg),
+              _lib.ptr(state.exp_avg_sq), n, _lib.ptr(ws), ws.numel(),
+              _lib.ptr(samples) if samples is not None else 0,
+              float(np.log(cfg.split_scale_factor)), n_keep, n_clone, n_split, _lib.ptr(flat),
+              _lib.ptr(m), _lib.ptr(v), st)
+    cloud._replace_flat(flat, n_new)
+    state._replace_moments(m, v)
+    state.reset_densify_stats()
+    return n_clone, n_split, n_prune
+
+
+def reset_opacities(state: TrainState, cfg: OptimConfig) -> None:
+    """Set every opacity logit to logit(reset value) and clear its moments
+    (reference optim.py:201-207), on the device."""
+    import numpy as np
+    target = math.log(cfg.opacity_reset_value / (1 - cfg.opacity_reset_value))
+    _lib.call("uws_reset_opacities", _lib.ptr(state.cloud.flat), _lib.ptr(state.exp_avg),
+              _lib.ptr(state.exp_avg_sq), len(state.cloud), float(np.float32(target)),
+              _lib.stream_handle())

@@ -111,6 +111,14 @@ class GaussianCloud:
         for name, v in flat_views(self._flat, self._n).items():
             object.__setattr__(self, "_v_" + name, v)
 
+    def _replace_flat(self, flat: torch.Tensor, n: int):
+        """Adopt a new flat parameter buffer of n Gaussians (densification);
+        bumps ``generation`` like the reference (optim.py:187)."""
+        object.__setattr__(self, "_flat", flat)
+        object.__setattr__(self, "_n", n)
+        self._bind()
+        self.generation += 1
+
     # field access mirrors the reference attributes; assignment copies in place
     # when the shape is unchanged, otherwise the flat buffer is rebuilt
     def __getattr__(self, name):
@@ -346,6 +354,16 @@ class TrainState:
                                        self.medium_exp_avg_sq[3 * j:3 * j + 3])
         self.grad_accum = torch.zeros(n, dtype=torch.float32, device=dev)
         self.obs_count = torch.zeros(n, dtype=torch.int32, device=dev)
+
+    def _replace_moments(self, exp_avg: torch.Tensor, exp_avg_sq: torch.Tensor):
+        """Adopt new moment buffers for the cloud's current size; the step
+        counters are kept (optim.py:190-195)."""
+        n = len(self.cloud)
+        self.exp_avg, self.exp_avg_sq = exp_avg, exp_avg_sq
+        mv, vv = flat_views(self.exp_avg, n), flat_views(self.exp_avg_sq, n)
+        for name in CLOUD_FIELDS:
+            slot = self.adam[name]
+            slot.m, slot.v = mv[name], vv[name]
 
     def reset_densify_stats(self):
         n = len(self.cloud)

@@ -6,6 +6,8 @@ rectangles, sorted entries, tile ranges) must match exactly; the float64
 oracle must reproduce float64 reference values to ~1e-12.
 """
 
+import os
+
 import numpy as np
 import pytest
 
@@ -144,3 +146,20 @@ def test_opaque_scene_crossing_contributor():
     tf = g.d["out_final_transmittance"]
     assert (tf < 1e-4).all()
     np.testing.assert_allclose(g.d["out_weight"] + tf, 1.0, atol=1e-13)
+
+
+def test_densify_matches_reference():
+    """oracle.densify_and_prune == reference densify_and_prune (same generator seed)."""
+    d = np.load(os.path.join(os.path.dirname(__file__), "golden", "densify.npz"))
+    f5 = ("positions", "log_scales", "rotations", "sh_coeffs", "opacity_logits")
+    arrays = {f: d["in_" + f] for f in f5}
+    m = {f: d["in_m_" + f] for f in f5}
+    v = {f: d["in_v_" + f] for f in f5}
+    new, nm, nv, counts = O.densify_and_prune(arrays, m, v, d["in_grad_accum"], d["in_obs_count"],
+                                              float(d["extent"]),
+                                              np.random.default_rng(int(d["seed"])))
+    assert counts == tuple(int(c) for c in d["counts"])
+    for f in f5:
+        np.testing.assert_array_equal(new[f], d["out_" + f], err_msg=f)
+        np.testing.assert_array_equal(nm[f], d["out_m_" + f], err_msg=f)
+        np.testing.assert_array_equal(nv[f], d["out_v_" + f], err_msg=f)
