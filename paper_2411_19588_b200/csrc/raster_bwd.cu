@@ -236,21 +236,25 @@ __global__ void __launch_bounds__(kThreads, MINB) k_raster_bwd(BwdArgs a) {
                 const StageC C = sC[k];
                 dx = fx - A.mx;
                 const float tA = A.A * dx;
+                const float skipv = B.hi - kSkipDelta;
 #pragma unroll
                 for (int p = 0; p < kPix; ++p) {
                     if (jrel >= mylast[p]) continue;
                     const float dy = fy[p] - A.my;
                     const float power = dx * fmaf(A.B, dy, tA) + B.C * dy * dy;
-                    if (power < B.skip) continue;
+                    if (power < skipv) continue;
                     const float araw = B.op * ex2_ftz(power);
-                    if (araw < kFloorLo) continue;
                     bool unclamped = araw < kClampLo;
-                    if (araw < kFloorHi || fabsf(araw - kClampMid) < kClampHalf) {
-                        // guard band: re-decide both gates from the float64 record
-                        const double e = alpha_raw_f64_cold(a.splat, a.exact, C.row, ox + lx,
-                                                            oy + ly0 + 2 * p);
-                        if (!(e >= kFloor)) continue;
-                        unclamped = e < kClamp;
+                    if (power < B.hi || fabsf(araw - kClampMid) < kClampHalf) {
+                        // near a gate (rare): the full decision from alpha_raw, with
+                        // both gates re-decided from the float64 record in the guard bands
+                        if (araw < kFloorLo) continue;
+                        if (araw < kFloorHi || fabsf(araw - kClampMid) < kClampHalf) {
+                            const double e = alpha_raw_f64_cold(a.splat, a.exact, C.row, ox + lx,
+                                                                oy + ly0 + 2 * p);
+                            if (!(e >= kFloor)) continue;
+                            unclamped = e < kClamp;
+                        }
                     }
                     hit = true;
                     const float alpha = fminf(araw, kClampF);

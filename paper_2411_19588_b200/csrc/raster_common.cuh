@@ -24,8 +24,16 @@ struct __align__(16) StageA {
     float mx, my, A, B;  // tile-local mean; -0.5*ca*log2e, -cb*log2e
 };
 struct __align__(16) StageB {
-    float C, op, skip, depth;  // -0.5*cc*log2e, opacity, log2-domain reject threshold, depth
+    float C, op, hi, depth;  // -0.5*cc*log2e, opacity, log2-domain sure-pass threshold, depth
 };
+
+// power >= hi       : alpha_raw is certainly >= kFloorHi (passes the 1/255 floor)
+// power <  hi - kSkipDelta : alpha_raw is certainly <  kFloorLo (rejected)
+// in between (a ~0.3% band of alpha_raw around 1/255): decide from alpha_raw as
+// before, with the float64 re-evaluation inside the guard band.
+// hi = lg2(kFloorHi/op) + 2e-3 and the old reject threshold lg2(kFloorLo/op) - 2e-3
+// differ by log2(kFloorHi/kFloorLo) + 4e-3 = 0.0040866; the constant rounds up.
+constexpr float kSkipDelta = 0.0041f;
 struct __align__(16) StageC {
     float r, g, b;
     int row;
@@ -86,13 +94,13 @@ __device__ __forceinline__ float rcp_ftz(float x) {
 }
 
 // Conservative tile-local box {ylo, yhi, xlo, xhi} of the region where the
-// staged pair test `power >= skip` can hold: for the positive-definite form
-// q = a dx^2 + b dx dy + c dy^2 <= Q (a = -A, b = -B, c = -C, Q = -skip) the
+// staged pair test `power >= hi - kSkipDelta` can hold: for the positive-definite form
+// q = a dx^2 + b dx dy + c dy^2 <= Q (a = -A, b = -B, c = -C, Q = kSkipDelta - hi) the
 // extents are |dy| <= sqrt(4aQ / (4ac - b^2)), |dx| <= sqrt(4cQ / (4ac - b^2)).
 // A relative + absolute margin keeps it a strict superset of what the float32
 // per-pixel test accepts; it is only a pre-filter.
 __device__ __forceinline__ float4 stage_extent(const StageA& s, const StageB& t) {
-    const float a = -s.A, b = -s.B, c = -t.C, Q = -t.skip;
+    const float a = -s.A, b = -s.B, c = -t.C, Q = -(t.hi - kSkipDelta);
     if (Q < 0.f) return make_float4(1e30f, -1e30f, 1e30f, -1e30f);  // nothing passes
     const float det4 = 4.f * a * c - b * b;
     if (!(det4 > 0.f) || !(a > 0.f) || !(c > 0.f) || !(Q >= 0.f))
@@ -115,9 +123,9 @@ __device__ __forceinline__ void stage_entry(const uws_splat* __restrict__ splat,
     a.B = (-kLog2e) * w1.y;
     b.C = (-0.5f * kLog2e) * w1.z;
     b.op = w1.w;
-    // alpha_raw < floor_lo  <=>  power2 < log2(floor_lo / op); the margin keeps
-    // float32 lg2/ex2 error from rejecting a pair the full test would keep
-    b.skip = lg2_ftz(kFloorLo / w1.w) - 2e-3f;
+    // alpha_raw >= floor_hi  <=  power2 >= log2(floor_hi / op) + margin; the
+    // margin (0.14% of alpha_raw) dwarfs the float32 lg2/ex2 error
+    b.hi = lg2_ftz(kFloorHi / w1.w) + 2e-3f;
     b.depth = w2.w;
     c.r = w2.x;
     c.g = w2.y;

@@ -52,7 +52,7 @@ __device__ __forceinline__ unsigned band_mask(float ylo, float yhi) {
 template <bool ROWS>
 __global__ void __launch_bounds__(kThreads, 4) k_raster_fwd(FwdArgs a) {
     __shared__ float4 sP0[kBatch + 1];  // mx, my, A, B          (+1: sentinel that never passes)
-    __shared__ float4 sP1[kBatch + 1];  // C, op, skip, depth
+    __shared__ float4 sP1[kBatch + 1];  // C, op, hi, depth
     __shared__ float4 sP2[kBatch + 1];  // r, g, b, row
     __shared__ unsigned char sMask[kBatch];
     __shared__ __align__(8) unsigned short sList[kWarps][kBatch + kListPad];
@@ -73,7 +73,7 @@ __global__ void __launch_bounds__(kThreads, 4) k_raster_fwd(FwdArgs a) {
     int count = 0, last = 0;
     if (threadIdx.x == 0) {
         sP0[kBatch] = make_float4(0.f, 0.f, 0.f, 0.f);
-        sP1[kBatch] = make_float4(0.f, 0.f, __int_as_float(0x7f800000), 0.f);  // skip = +inf
+        sP1[kBatch] = make_float4(0.f, 0.f, __int_as_float(0x7f800000), 0.f);  // hi = +inf
         sP2[kBatch] = make_float4(0.f, 0.f, 0.f, 0.f);
     }
 
@@ -111,7 +111,7 @@ __global__ void __launch_bounds__(kThreads, 4) k_raster_fwd(FwdArgs a) {
             StageC sc;
             stage_entry(a.splat, row, ox, oy, sa, sb, sc);
             sP0[threadIdx.x] = make_float4(sa.mx, sa.my, sa.A, sa.B);
-            sP1[threadIdx.x] = make_float4(sb.C, sb.op, sb.skip, sb.depth);
+            sP1[threadIdx.x] = make_float4(sb.C, sb.op, sb.hi, sb.depth);
             sP2[threadIdx.x] = make_float4(sc.r, sc.g, sc.b, __int_as_float(sc.row));
             const float4 box = stage_extent(sa, sb);
             sMask[threadIdx.x] = (unsigned char)band_mask(box.x, box.y);
@@ -142,13 +142,15 @@ __global__ void __launch_bounds__(kThreads, 4) k_raster_fwd(FwdArgs a) {
                 const float4 p1 = sP1[i];
                 const float dx = fx - p0.x, dy = fy - p0.y;
                 const float power = dx * fmaf(p0.w, dy, p0.z * dx) + p1.x * dy * dy;
-                if (power >= p1.z && T >= kTStopF) {
+                if (power >= p1.z - kSkipDelta && T >= kTStopF) {
                     const float araw = p1.y * ex2_ftz(power);
-                    bool ok = araw >= kFloorHi;
-                    if (!ok && araw >= kFloorLo)  // guard band: float64 decision (rare)
-                        ok = alpha_raw_f64_cold(a.splat, a.exact, __float_as_int(sP2[i].w), px,
-                                                py) >= kFloor;
-                    if (ok) {
+                    bool take = true;
+                    if (power < p1.z)  // near the 1/255 floor (rare): float64 in the guard band
+                        take = araw >= kFloorHi ||
+                               (araw >= kFloorLo &&
+                                alpha_raw_f64_cold(a.splat, a.exact, __float_as_int(sP2[i].w), px,
+                                                   py) >= kFloor);
+                    if (take) {
                         const float4 c = sP2[i];
                         const float alpha = fminf(araw, kClampF);
                         const float w = alpha * T;
