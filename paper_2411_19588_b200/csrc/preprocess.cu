@@ -94,7 +94,7 @@ __device__ __forceinline__ bool project_one(const uws_cloud& cl, const uws_camer
     return true;
 }
 
-__global__ void __launch_bounds__(kThreads) k_preprocess(uws_cloud cl, uws_camera cam,
+__global__ void __launch_bounds__(kThreads, 6) k_preprocess(uws_cloud cl, uws_camera cam,
                                                          uws_projected out, int gx, int gy,
                                                          unsigned long long* status,
                                                          unsigned* ticket) {
