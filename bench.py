@@ -266,7 +266,8 @@ def run_gpu(args):
     # through StepEngine.render (one host read of the overflow flag per frame), at C3
     # and at C5's 1M Gaussians @ 3840x2160
     render_fps = {}
-    for name, (rw, rh) in (("C3 1M 1920x1080", (W, H)), ("C5 1M 3840x2160", (3840, 2160))):
+    for name, (rw, rh) in ((("C3 1M 1920x1080", (W, H)), ("C5 1M 3840x2160", (3840, 2160)))
+                           if not args.no_render_fps else ()):
         eng = trainer.engine if (rw, rh) == (W, H) else uw.StepEngine(state, rw, rh, cfg)
         rcam = uw.Camera.look_at(view_eye(rank), (0, 0, 12), width=rw, height=rh,
                                  fx=1.2 * rw, fy=1.2 * rw)
@@ -570,6 +571,8 @@ def main():
     ap.add_argument("--impl", choices=("b200", "reference"), default="b200")
     ap.add_argument("--cpu-tiles", type=int, default=12)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-render-fps", action="store_true",
+                    help="skip the render-FPS frames (e.g. for a step-only ncu launch list)")
     args = ap.parse_args()
     res = run_reference(args) if args.impl == "reference" else run_gpu(args)
     if res is not None:

@@ -1,0 +1,49 @@
+"""Summarise an `ncu --set full` report: per kernel (first launch of each name)
+duration, DRAM bytes, instructions, issue/occupancy and the top stall reasons.
+
+    python tools/ncu_summary.py report.ncu-rep summary.txt traffic.json
+"""
+import csv, io, json, subprocess, sys
+
+rep, out_txt, out_json = sys.argv[1:4]
+raw = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True,
+                     text=True).stdout
+rows = list(csv.reader(io.StringIO(raw)))
+hdr = rows[0]
+idx = {h: i for i, h in enumerate(hdr)}
+stall = [h for h in hdr if h.startswith("smsp__average_warps_issue_stalled_")
+         and h.endswith("_per_issue_active.ratio")]
+
+
+def num(d, k):
+    try:
+        return float(d[idx[k]])
+    except (KeyError, ValueError):
+        return float("nan")
+
+
+lines, traffic, seen = [], {}, set()
+for d in rows[2:]:
+    name = d[idx["Kernel Name"]].split("(")[0].replace("uws::<unnamed>::", "").replace("void ", "")
+    name = name.replace("radix::", "").replace("uws::", "").replace("(anonymous namespace)::", "")
+    if name in seen:
+        continue
+    seen.add(name)
+    t_us = num(d, "gpu__time_duration.sum")
+    dram = (num(d, "dram__bytes_read.sum") + num(d, "dram__bytes_write.sum")) * 1e6  # MB -> B
+    traffic[name] = {"time_us": t_us, "dram_bytes": dram}
+    st = sorted(((num(d, h), h) for h in stall), reverse=True)[:4]
+    lines.append(
+        f"{name:32s} {t_us:9.1f} us  dram {dram / 1e6:8.1f} MB ({dram / max(t_us, 1e-9) / 1e3:7.1f} GB/s)"
+        f"  inst {num(d, 'smsp__inst_executed.sum') / 1e6:7.1f} M  issue "
+        f"{num(d, 'smsp__issue_active.avg.pct_of_peak_sustained_active'):5.1f}%  warps "
+        f"{num(d, 'sm__warps_active.avg.pct_of_peak_sustained_active'):5.1f}%  regs "
+        f"{d[idx['launch__registers_per_thread']]:>3}\n      stalls: " +
+        ", ".join(f"{h.replace('smsp__average_warps_issue_stalled_', '').replace('_per_issue_active.ratio', '')}"
+                  f"={v:.2f}" for v, h in st))
+with open(out_txt, "w") as f:
+    f.write(f"ncu --set full --clock-control none (single launches, cold cache, serialised); {rep}\n")
+    f.write("\n".join(lines) + "\n")
+with open(out_json, "w") as f:
+    json.dump(traffic, f, indent=1)
+print("\n".join(lines))
