@@ -29,6 +29,7 @@
 // leaves the SM as coalesced stores.
 #include <algorithm>
 
+#include "depth_sort.cuh"
 #include "radix.cuh"
 
 namespace uws {
@@ -557,26 +558,34 @@ __global__ void __launch_bounds__(kThreads) k_cell_scatter(const uint2* __restri
 // workspace plans
 // ---------------------------------------------------------------------------
 struct CountPlan {
-    uint64_t* depth_keys_sorted;
+    uint32_t* keys_hi;            // high words of the depth bits (sort input)
+    uint32_t* keys_hi_sorted;
     uint32_t* sorted_rows;
+    uint32_t* long_cnt;           // runs of equal high words longer than kShortRun
+    uint32_t* long_list;
     uint32_t* m_band;             // [nbands][nblk_r] counts, scanned in place
     unsigned long long* rstat;    // look-back status of the band scan (row-list path)
     unsigned* rticket;
-    uint64_t *k_alt, *k_tmp;
+    uint32_t *k_alt, *k_tmp;
     uint32_t *v_alt, *v_tmp, *hist, *rstatus, *rtickets;
     uint32_t nblk_r;
 };
 
+constexpr int kDepthPasses = 4;  // 8-bit digits of the depth's high word
+
 void plan_count(Workspace& ws, uint32_t k, int nbands, CountPlan& p) {
     const uint32_t kk = k > 0 ? k : 1;
     p.nblk_r = (uint32_t)ceil_div(kk, kBlockItems);
-    p.depth_keys_sorted = ws.take<uint64_t>(kk);
+    p.keys_hi = ws.take<uint32_t>(kk);
+    p.keys_hi_sorted = ws.take<uint32_t>(kk);
     p.sorted_rows = ws.take<uint32_t>(kk);
+    p.long_cnt = ws.take<uint32_t>(1);
+    p.long_list = ws.take<uint32_t>(kk / (depth_sort::kShortRun + 1) + 1);
     p.m_band = ws.take<uint32_t>((size_t)nbands * p.nblk_r);
     p.rstat = ws.take<unsigned long long>(ceil_div((size_t)nbands * p.nblk_r, kThreads * kScanIpt));
     p.rticket = ws.take<unsigned>(1);
-    radix::plan<uint64_t>(ws, kk, 8, &p.k_alt, &p.v_alt, &p.k_tmp, &p.v_tmp, &p.hist, &p.rstatus,
-                          &p.rtickets);
+    radix::plan<uint32_t>(ws, kk, kDepthPasses, &p.k_alt, &p.v_alt, &p.k_tmp, &p.v_tmp, &p.hist,
+                          &p.rstatus, &p.rtickets);
 }
 
 struct EmitPlan {
@@ -649,11 +658,22 @@ extern "C" int uws_bin_count(const uws_projected* proj, int64_t k_cap, const uws
     UWS_REQUIRE(ws.ok(), "uws_bin_count: workspace too small");
     const uint32_t kc = (uint32_t)k_cap;
     const uint32_t* k_dev = (const uint32_t*)proj->num_visible;
-    // 0. stable sort of rows by float64 depth bits (8 digit passes)
-    size_t meta = (char*)(p.rtickets + 8) - (char*)p.hist;
-    UWS_CUDA(radix::sort_pairs<uint64_t>((const uint64_t*)proj->depth, nullptr, p.depth_keys_sorted,
-                                         p.sorted_rows, kc, k_dev, 0, 8, p.k_tmp, p.v_tmp, p.hist,
+    // 0. stable order of the rows by (float64 depth bits, row): radix sort of the
+    //    high words (4 passes), then the runs of equal high words by the low word
+    const uint64_t* dbits = (const uint64_t*)proj->depth;
+    depth_sort::k_depth_hi<<<(unsigned)ceil_div(kc, 256), 256, 0, st>>>(dbits, k_dev, kc, p.keys_hi,
+                                                                       p.long_cnt);
+    UWS_CHECK_LAUNCH("k_depth_hi");
+    size_t meta = (char*)(p.rtickets + kDepthPasses) - (char*)p.hist;
+    UWS_CUDA(radix::sort_pairs<uint32_t>(p.keys_hi, nullptr, p.keys_hi_sorted, p.sorted_rows, kc,
+                                         k_dev, 0, kDepthPasses, p.k_tmp, p.v_tmp, p.hist,
                                          p.rstatus, p.rtickets, meta, st));
+    depth_sort::k_tie_fix<<<(unsigned)ceil_div(kc, 256), 256, 0, st>>>(
+        p.keys_hi_sorted, p.sorted_rows, dbits, k_dev, kc, p.long_cnt, p.long_list);
+    UWS_CHECK_LAUNCH("k_tie_fix");
+    depth_sort::k_tie_fix_long<<<148, depth_sort::kLongThreads, 0, st>>>(
+        p.keys_hi_sorted, p.sorted_rows, dbits, k_dev, kc, p.long_cnt, p.long_list, p.v_tmp);
+    UWS_CHECK_LAUNCH("k_tie_fix_long");
     // 1a. per-block band histograms + totals (E entries, S band items)
     k_band_count<<<p.nblk_r, kThreads, 0, st>>>(p.sorted_rows, (const short4*)proj->rect,
                                                 proj->num_visible, nbands, p.nblk_r, p.m_band,

@@ -1,0 +1,153 @@
+// Depth order of the visible rows: (float64 depth, source row), stable.
+//
+// The reference orders by lexsort((source, depth, tile)) (rasterizer.py:79);
+// the depth-major part is a stable sort of the rows by their float64 depth.
+// Positive doubles order like their bit patterns, so the full key is 64 bits
+// (8 radix passes).  Here the rows are radix-sorted by the HIGH 32 bits only
+// (sign, exponent, 20 mantissa bits: 4 passes) and the rare runs of equal
+// high words -- depths within ~1e-6 relative of each other -- are then put in
+// (low word, row) order:
+//   * runs of <= kShortRun rows: one thread, insertion sort in registers;
+//   * longer runs (pathological: many Gaussians at almost the same depth): one
+//     CTA per run, a stable 4-pass LSD counting sort on the low word.
+// Rows enter the sort in ascending order, so every stage is stable and the
+// result equals the 64-bit sort bit for bit.
+#pragma once
+
+#include "common.cuh"
+#include "scan.cuh"
+
+namespace uws {
+namespace depth_sort {
+
+constexpr int kShortRun = 16;
+constexpr int kLongThreads = 256;
+
+// high 32 bits of the depth's bit pattern; zeroes the long-run counter
+__global__ void k_depth_hi(const uint64_t* __restrict__ depth_bits, const uint32_t* __restrict__ n_dev,
+                           uint32_t n_cap, uint32_t* __restrict__ keys, uint32_t* long_cnt) {
+    const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i == 0) *long_cnt = 0;
+    const uint32_t n = min(*n_dev, n_cap);
+    if (i < n) keys[i] = (uint32_t)(depth_bits[i] >> 32);
+}
+
+// one thread per sorted position; run starts fix their run
+__global__ void k_tie_fix(const uint32_t* __restrict__ keys, uint32_t* __restrict__ rows,
+                          const uint64_t* __restrict__ depth_bits, const uint32_t* __restrict__ n_dev,
+                          uint32_t n_cap, uint32_t* __restrict__ long_cnt,
+                          uint32_t* __restrict__ long_list) {
+    const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+    const uint32_t n = min(*n_dev, n_cap);
+    if (i >= n) return;
+    const uint32_t k = keys[i];
+    if (i > 0 && keys[i - 1] == k) return;      // not the first of its run
+    if (i + 1 >= n || keys[i + 1] != k) return;  // no tie
+    uint32_t len = 2;
+    while (len <= (uint32_t)kShortRun && i + len < n && keys[i + len] == k) ++len;
+    if (len > (uint32_t)kShortRun) {
+        long_list[atomicAdd(long_cnt, 1u)] = i;
+        return;
+    }
+    uint32_t r[kShortRun], lo[kShortRun];
+    for (uint32_t j = 0; j < len; ++j) {
+        r[j] = rows[i + j];
+        lo[j] = (uint32_t)depth_bits[r[j]];
+    }
+    for (uint32_t j = 1; j < len; ++j) {  // stable insertion sort by the low word
+        const uint32_t rv = r[j], lv = lo[j];
+        uint32_t p = j;
+        while (p > 0 && lo[p - 1] > lv) {
+            r[p] = r[p - 1];
+            lo[p] = lo[p - 1];
+            --p;
+        }
+        r[p] = rv;
+        lo[p] = lv;
+    }
+    for (uint32_t j = 0; j < len; ++j) rows[i + j] = r[j];
+}
+
+// One CTA per long run: find its end, then 4 stable counting-sort passes on the
+// low word (8 bits each), chunk by chunk in order, ping-ponging with tmp.
+__global__ void __launch_bounds__(kLongThreads) k_tie_fix_long(
+    const uint32_t* __restrict__ keys, uint32_t* __restrict__ rows,
+    const uint64_t* __restrict__ depth_bits, const uint32_t* __restrict__ n_dev, uint32_t n_cap,
+    const uint32_t* __restrict__ long_cnt, const uint32_t* __restrict__ long_list,
+    uint32_t* __restrict__ tmp) {
+    constexpr int W = kLongThreads / 32;
+    __shared__ uint32_t s_base[256];
+    __shared__ uint32_t s_wc[W][257];
+    __shared__ uint32_t s_tmp[W + 1];
+    __shared__ uint32_t s_end;
+    const uint32_t n = min(*n_dev, n_cap);
+    const uint32_t cnt = *long_cnt;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    for (uint32_t run = blockIdx.x; run < cnt; run += gridDim.x) {
+        const uint32_t start = long_list[run];
+        const uint32_t k = keys[start];
+        // end of the run: first position past start whose key differs
+        if (tid == 0) s_end = n;
+        __syncthreads();
+        for (uint32_t c0 = start; c0 < n; c0 += kLongThreads) {
+            const uint32_t j = c0 + tid;
+            if (j < n && keys[j] != k) atomicMin(&s_end, j);
+            __syncthreads();
+            if (s_end != n) break;
+            __syncthreads();
+        }
+        const uint32_t len = s_end - start;
+        __syncthreads();
+        uint32_t* src = rows + start;
+        uint32_t* dst = tmp + start;
+        for (int pass = 0; pass < 4; ++pass) {
+            const int shift = 8 * pass;
+            s_base[tid] = 0;
+            __syncthreads();
+            for (uint32_t j = tid; j < len; j += kLongThreads)
+                atomicAdd(&s_base[((uint32_t)depth_bits[src[j]] >> shift) & 0xFF], 1u);
+            __syncthreads();
+            {
+                uint32_t tot;
+                const uint32_t v = s_base[tid];
+                const uint32_t ex = block_exclusive_sum<kLongThreads, uint32_t>(v, s_tmp, &tot);
+                __syncthreads();
+                s_base[tid] = ex;
+            }
+            __syncthreads();
+            for (uint32_t c0 = 0; c0 < len; c0 += kLongThreads) {
+                for (int q = tid; q < W * 257; q += kLongThreads) (&s_wc[0][0])[q] = 0;
+                __syncthreads();
+                const uint32_t j = c0 + tid;
+                const bool valid = j < len;
+                const uint32_t row = valid ? src[j] : 0u;
+                const unsigned d = valid ? (((uint32_t)depth_bits[row] >> shift) & 0xFF) : 256u;
+                const unsigned peers = __match_any_sync(0xffffffffu, d);
+                const unsigned below = __popc(peers & lanemask_lt());
+                if (valid && below == 0) s_wc[warp][d] = __popc(peers);
+                __syncthreads();
+                if (valid) {
+                    uint32_t pre = 0;
+                    for (int w = 0; w < warp; ++w) pre += s_wc[w][d];
+                    dst[s_base[d] + pre + below] = row;
+                }
+                __syncthreads();
+                {
+                    uint32_t add = 0;
+#pragma unroll
+                    for (int w = 0; w < W; ++w) add += s_wc[w][tid];
+                    s_base[tid] += add;
+                }
+                __syncthreads();
+            }
+            uint32_t* t = src;
+            src = dst;
+            dst = t;
+        }
+        // 4 passes: the result is back in rows
+        __syncthreads();
+    }
+}
+
+}  // namespace depth_sort
+}  // namespace uws
