@@ -7,7 +7,8 @@
 // (sign, exponent, 20 mantissa bits: 4 passes) and the rare runs of equal
 // high words -- depths within ~1e-6 relative of each other -- are then put in
 // (low word, row) order:
-//   * runs of <= kShortRun rows: one thread, insertion sort in registers;
+//   * runs of <= kShortRun rows: one thread, odd-even transposition network in
+//     registers (stable: adjacent swaps on strictly greater keys, max-key padding);
 //   * longer runs (pathological: many Gaussians at almost the same depth): one
 //     CTA per run, a stable 4-pass LSD counting sort on the low word.
 // Rows enter the sort in ascending order, so every stage is stable and the
@@ -20,7 +21,7 @@
 namespace uws {
 namespace depth_sort {
 
-constexpr int kShortRun = 16;
+constexpr int kShortRun = 8;
 constexpr int kLongThreads = 256;
 
 // high 32 bits of the depth's bit pattern; zeroes the long-run counter
@@ -50,22 +51,26 @@ __global__ void k_tie_fix(const uint32_t* __restrict__ keys, uint32_t* __restric
         return;
     }
     uint32_t r[kShortRun], lo[kShortRun];
-    for (uint32_t j = 0; j < len; ++j) {
-        r[j] = rows[i + j];
-        lo[j] = (uint32_t)depth_bits[r[j]];
+#pragma unroll
+    for (int j = 0; j < kShortRun; ++j) {
+        r[j] = (uint32_t)j < len ? rows[i + j] : 0xffffffffu;
+        lo[j] = (uint32_t)j < len ? (uint32_t)depth_bits[r[j]] : 0xffffffffu;
     }
-    for (uint32_t j = 1; j < len; ++j) {  // stable insertion sort by the low word
-        const uint32_t rv = r[j], lv = lo[j];
-        uint32_t p = j;
-        while (p > 0 && lo[p - 1] > lv) {
-            r[p] = r[p - 1];
-            lo[p] = lo[p - 1];
-            --p;
+#pragma unroll
+    for (int round = 0; round < kShortRun; ++round) {
+#pragma unroll
+        for (int j = round & 1; j + 1 < kShortRun; j += 2) {
+            const bool sw = lo[j] > lo[j + 1];
+            const uint32_t a = lo[j], b = lo[j + 1], ra = r[j], rb = r[j + 1];
+            lo[j] = sw ? b : a;
+            lo[j + 1] = sw ? a : b;
+            r[j] = sw ? rb : ra;
+            r[j + 1] = sw ? ra : rb;
         }
-        r[p] = rv;
-        lo[p] = lv;
     }
-    for (uint32_t j = 0; j < len; ++j) rows[i + j] = r[j];
+#pragma unroll
+    for (int j = 0; j < kShortRun; ++j)
+        if ((uint32_t)j < len) rows[i + j] = r[j];
 }
 
 // One CTA per long run: find its end, then 4 stable counting-sort passes on the

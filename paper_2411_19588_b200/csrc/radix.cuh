@@ -76,16 +76,14 @@ __global__ void __launch_bounds__(kThreads) k_histogram(const K* __restrict__ ke
         if (h[i]) atomicAdd(&hist[i], h[i]);
 }
 
-// exclusive scan of each pass's 256-bin histogram, in place
+// exclusive scan of each pass's 256-bin histogram, in place (one block per pass)
 __global__ void __launch_bounds__(kBins) k_scan_hist(uint32_t* hist, int passes) {
     __shared__ uint32_t tmp[kBins / 32 + 1];
-    for (int p = 0; p < passes; ++p) {
-        uint32_t v = hist[p * kBins + threadIdx.x];
-        uint32_t tot;
-        uint32_t ex = block_exclusive_sum<kBins>(v, tmp, &tot);
-        hist[p * kBins + threadIdx.x] = ex;
-        __syncthreads();
-    }
+    const int p = blockIdx.x;
+    uint32_t v = hist[p * kBins + threadIdx.x];
+    uint32_t tot;
+    uint32_t ex = block_exclusive_sum<kBins>(v, tmp, &tot);
+    hist[p * kBins + threadIdx.x] = ex;
 }
 
 template <typename K>
@@ -237,7 +235,7 @@ inline cudaError_t sort_pairs(const K* keys_in, const uint32_t* vals_in, K* keys
     int hist_blocks = (int)ceil_div(n_cap, kThreads * 8);
     if (hist_blocks > 1184) hist_blocks = 1184;
     k_histogram<K><<<hist_blocks, kThreads, 0, st>>>(keys_in, n_cap, n_dev, begin_bit, passes, hist);
-    k_scan_hist<<<1, kBins, 0, st>>>(hist, passes);
+    k_scan_hist<<<passes, kBins, 0, st>>>(hist, passes);
     const int tiles = (int)ceil_div(n_cap, tile_items<K>());
     // ping-pong so that the last pass writes into keys_out/vals_out
     const K* ksrc = keys_in;
