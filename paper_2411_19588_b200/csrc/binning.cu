@@ -208,6 +208,26 @@ __device__ __forceinline__ void warp_append_1d(int lo, int cnt, uint2 val, int* 
     }
 }
 
+// 32 items (one per lane, lane order == list order) appended to the buckets
+// [lo, hi] they cover: bucket by bucket, the covering lanes write consecutive
+// slots from the bucket's cursor (coalesced runs, no per-item serial chain)
+__device__ __forceinline__ void warp_append_bands(int lo, int hi, uint2 val, int* cur, uint2* out,
+                                                  int lane) {
+    const int umin = __reduce_min_sync(0xffffffffu, lo);
+    const int umax = __reduce_max_sync(0xffffffffu, hi);
+    const unsigned lt = lanemask_lt();
+    for (int b = umin; b <= umax; ++b) {
+        const bool in = lo <= b && b <= hi;
+        const unsigned m = __ballot_sync(0xffffffffu, in);
+        if (m == 0) continue;
+        const int base = cur[b];
+        if (in) out[base + __popc(m & lt)] = val;
+        __syncwarp();
+        if (lane == 0) cur[b] = base + __popc(m);
+        __syncwarp();
+    }
+}
+
 // row-list item: the row and its inclusive tile-column span packed in 16+16 bits
 __device__ __forceinline__ uint2 row_item(uint32_t row, short4 rc) {
     return make_uint2(row, (uint32_t)(uint16_t)rc.x | ((uint32_t)(uint16_t)rc.z << 16));
@@ -247,9 +267,9 @@ __global__ void __launch_bounds__(kThreads) k_band_scatter(const uint32_t* __res
     for (int i = 0; i < kRankChunks; ++i) {
         const short4 rc = rcv[i];
         const bool ok = rect_ok(rc);
-        const int b0 = ok ? rc.y / kBand : 0;
-        const int nb = ok ? rc.w / kBand - b0 + 1 : 0;
-        warp_append_1d(b0, nb, row_item(rowv[i], rc), diff[warp], seg, lane);
+        const int b0 = ok ? rc.y / kBand : (1 << 30);
+        const int b1 = ok ? rc.w / kBand : -1;
+        warp_append_bands(b0, b1, row_item(rowv[i], rc), diff[warp], seg, lane);
     }
 }
 
