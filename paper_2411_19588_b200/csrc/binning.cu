@@ -40,8 +40,8 @@ constexpr int kWarpsB = kThreads / 32;
 constexpr int kBand = 1;                       // tile rows per band
 constexpr int kMaxGX = 256;                    // max tile columns (4096 px)
 constexpr int kMaxBands = 256 / kBand;         // max bands (4096 px tall)
-constexpr int kPerWarp = 64;                   // level 1: ranks per warp sub-block
-constexpr int kBlockItems = kWarpsB * kPerWarp;  // 512
+constexpr int kPerWarp = 128;                  // level 1: ranks per warp sub-block
+constexpr int kBlockItems = kWarpsB * kPerWarp;  // 1024
 constexpr int kRankChunks = kPerWarp / 32;
 constexpr int kSegPerWarp = 64;                // level 2: items per warp sub-block
 constexpr int kSegBlock = kWarpsB * kSegPerWarp;  // 512
