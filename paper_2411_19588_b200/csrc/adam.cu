@@ -46,9 +46,13 @@ __device__ __forceinline__ void adam1(float& p, float& m, float& v, float g, con
     // for den = sqrt(vh) + eps > 0.
     // (The substituted operands keep the unused branch on the inline fast path
     // when the compiler evaluates both sides of the selects.)
+    // (The empty asm makes the substituted operands opaque: otherwise the
+    // compiler proves them dead and feeds the zeros to sqrt/div after all.)
     const double num = __dmul_rn(k.lr, mh);
-    const double den = vh == 0.0 ? hp.eps : __dadd_rn(__dsqrt_rn(vh == 0.0 ? 1.0 : vh), hp.eps);
-    const double q = num == 0.0 ? num : __ddiv_rn(num == 0.0 ? 1.0 : num, den);
+    double vs = vh == 0.0 ? 1.0 : vh, ns = num == 0.0 ? 1.0 : num;
+    asm("" : "+d"(vs), "+d"(ns));
+    const double den = vh == 0.0 ? hp.eps : __dadd_rn(__dsqrt_rn(vs), hp.eps);
+    const double q = num == 0.0 ? num : __ddiv_rn(ns, den);
     const double upd = __dsub_rn((double)p, q);
     p = (float)upd;
     m = (float)mm;

@@ -691,7 +691,7 @@ extern "C" int uws_bin_count(const uws_projected* proj, int64_t k_cap, const uws
     depth_sort::k_tie_fix<<<(unsigned)ceil_div(kc, 256), 256, 0, st>>>(
         p.keys_hi_sorted, p.sorted_rows, dbits, k_dev, kc, p.long_cnt, p.long_list);
     UWS_CHECK_LAUNCH("k_tie_fix");
-    depth_sort::k_tie_fix_long<<<148, depth_sort::kLongThreads, 0, st>>>(
+    depth_sort::k_tie_fix_long<<<32, depth_sort::kLongThreads, 0, st>>>(
         p.keys_hi_sorted, p.sorted_rows, dbits, k_dev, kc, p.long_cnt, p.long_list, p.v_tmp);
     UWS_CHECK_LAUNCH("k_tie_fix_long");
     // 1a. per-block band histograms + totals (E entries, S band items)

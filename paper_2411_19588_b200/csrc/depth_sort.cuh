@@ -50,6 +50,14 @@ __global__ void k_tie_fix(const uint32_t* __restrict__ keys, uint32_t* __restric
         long_list[atomicAdd(long_cnt, 1u)] = i;
         return;
     }
+    if (len == 2) {  // the common tie: one compare-exchange
+        const uint32_t r0 = rows[i], r1 = rows[i + 1];
+        if ((uint32_t)depth_bits[r0] > (uint32_t)depth_bits[r1]) {
+            rows[i] = r1;
+            rows[i + 1] = r0;
+        }
+        return;
+    }
     uint32_t r[kShortRun], lo[kShortRun];
 #pragma unroll
     for (int j = 0; j < kShortRun; ++j) {
