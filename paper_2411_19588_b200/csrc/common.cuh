@@ -91,6 +91,23 @@ __device__ __forceinline__ unsigned lanemask_lt() {
     return m;
 }
 
+// a / b (b > 0, normal) and sqrt(x) as IEEE round-to-nearest, with a zero
+// operand answered directly: a zero in any lane otherwise sends the whole warp
+// down the out-of-line special-operand path of the division / square root.
+// The empty asm keeps the substituted operand opaque to the optimiser.
+__device__ __forceinline__ double div_pos_nz(double a, double b) {
+    double as = a == 0.0 ? 1.0 : a;
+    asm("" : "+d"(as));
+    const double q = __ddiv_rn(as, b);
+    return a == 0.0 ? a : q;  // +-0 / b = +-0
+}
+__device__ __forceinline__ double sqrt_nz(double x) {
+    double xs = x == 0.0 ? 1.0 : x;
+    asm("" : "+d"(xs));
+    const double r = __dsqrt_rn(xs);
+    return x == 0.0 ? x : r;  // sqrt(+-0) = +-0
+}
+
 template <typename T>
 __device__ __forceinline__ T warp_sum(T v) {
 #pragma unroll

@@ -147,7 +147,7 @@ __global__ void __launch_bounds__(kThreads, 6) k_preprocess_bwd(uws_cloud cl, uw
     }
 #pragma unroll
     for (int c = 0; c < 4; ++c) {
-        float v = grot[4 * i + c] + (float)((dq[c] - G.qu[c] * radial) / G.qn);
+        float v = grot[4 * i + c] + (float)div_pos_nz(dq[c] - G.qu[c] * radial, G.qn);
         grot[4 * i + c] = v;
         finite &= isfinite(v);
     }
@@ -157,7 +157,7 @@ __global__ void __launch_bounds__(kThreads, 6) k_preprocess_bwd(uws_cloud cl, uw
         finite &= isfinite(v);
     }
     const double nx = dmx * cam.width * 0.5, ny = dmy * cam.height * 0.5;
-    gnorm[i] += (float)sqrt(nx * nx + ny * ny);
+    gnorm[i] += (float)sqrt_nz(nx * nx + ny * ny);
     gobs[i] += 1.0f;
     if (!finite && nonfinite) atomicAdd(nonfinite, 1.0f);
 }
