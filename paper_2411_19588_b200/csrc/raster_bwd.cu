@@ -224,7 +224,8 @@ __global__ void __launch_bounds__(kThreads, MINB) k_raster_bwd(BwdArgs a) {
         // back to front over the entries this warp's pixels consumed
         for (int k = min(nb, wmax - lo) - 1; k >= 0; --k) {
             const float4 D = sD[k];
-            if (D.y < band_lo || D.x > band_hi) continue;  // misses this warp's band (uniform)
+            // misses this warp's band or the tile's pixel columns (uniform)
+            if (D.y < band_lo || D.x > band_hi || D.w < 0.5f || D.z > (float)kTile - 0.5f) continue;
             const int jrel = lo + k;
             // A thread's kPix pixels share one column, hence dx: the dx-weighted
             // partials are formed once after the pixel loop from sum(dp) and sum(dp dy).

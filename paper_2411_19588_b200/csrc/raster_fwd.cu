@@ -114,7 +114,9 @@ __global__ void __launch_bounds__(kThreads, 4) k_raster_fwd(FwdArgs a) {
             sP1[threadIdx.x] = make_float4(sb.C, sb.op, sb.hi, sb.depth);
             sP2[threadIdx.x] = make_float4(sc.r, sc.g, sc.b, __int_as_float(sc.row));
             const float4 box = stage_extent(sa, sb);
-            sMask[threadIdx.x] = (unsigned char)band_mask(box.x, box.y);
+            // bands the box reaches; none if it misses the tile's pixel columns
+            const bool xin = box.z <= (float)kTile - 0.5f && box.w >= 0.5f;
+            sMask[threadIdx.x] = xin ? (unsigned char)band_mask(box.x, box.y) : 0u;
         }
         __syncthreads();
         // this warp's entries: those whose box reaches its band, in list order
