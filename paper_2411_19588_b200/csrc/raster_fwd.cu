@@ -51,9 +51,9 @@ __device__ __forceinline__ unsigned band_mask(float ylo, float yhi) {
 
 template <bool ROWS>
 __global__ void __launch_bounds__(kThreads, 4) k_raster_fwd(FwdArgs a) {
-    __shared__ float4 sP0[kBatch + 1];  // mx, my, A, B          (+1: sentinel that never passes)
-    __shared__ float4 sP1[kBatch + 1];  // C, op, hi, depth
-    __shared__ float4 sP2[kBatch + 1];  // r, g, b, row
+    // staged records, 3 x float4 each (+1: a sentinel that never passes):
+    //   [mx, my, A, B] [C, op, hi, depth] [r, g, b, row]
+    __shared__ float4 sRec[3 * (kBatch + 1)];
     __shared__ unsigned char sMask[kBatch];
     __shared__ __align__(8) unsigned short sList[kWarps][kBatch + kListPad];
     __shared__ int sRow[ROWS ? kBatch + kChunk : 1];
@@ -72,9 +72,9 @@ __global__ void __launch_bounds__(kThreads, 4) k_raster_fwd(FwdArgs a) {
     float T = inside ? 1.0f : 0.0f, cr = 0.f, cg = 0.f, cb = 0.f, dsum = 0.f, wsum = 0.f;
     int count = 0, last = 0;
     if (threadIdx.x == 0) {
-        sP0[kBatch] = make_float4(0.f, 0.f, 0.f, 0.f);
-        sP1[kBatch] = make_float4(0.f, 0.f, __int_as_float(0x7f800000), 0.f);  // hi = +inf
-        sP2[kBatch] = make_float4(0.f, 0.f, 0.f, 0.f);
+        sRec[3 * kBatch + 0] = make_float4(0.f, 0.f, 0.f, 0.f);
+        sRec[3 * kBatch + 1] = make_float4(0.f, 0.f, __int_as_float(0x7f800000), 0.f);  // hi = +inf
+        sRec[3 * kBatch + 2] = make_float4(0.f, 0.f, 0.f, 0.f);
     }
 
     int start = 0, end = 0, cur = 0, nst = 0;
@@ -110,9 +110,9 @@ __global__ void __launch_bounds__(kThreads, 4) k_raster_fwd(FwdArgs a) {
             StageB sb;
             StageC sc;
             stage_entry(a.splat, row, ox, oy, sa, sb, sc);
-            sP0[threadIdx.x] = make_float4(sa.mx, sa.my, sa.A, sa.B);
-            sP1[threadIdx.x] = make_float4(sb.C, sb.op, sb.hi, sb.depth);
-            sP2[threadIdx.x] = make_float4(sc.r, sc.g, sc.b, __int_as_float(sc.row));
+            sRec[3 * threadIdx.x + 0] = make_float4(sa.mx, sa.my, sa.A, sa.B);
+            sRec[3 * threadIdx.x + 1] = make_float4(sb.C, sb.op, sb.hi, sb.depth);
+            sRec[3 * threadIdx.x + 2] = make_float4(sc.r, sc.g, sc.b, __int_as_float(sc.row));
             const float4 box = stage_extent(sa, sb);
             // bands the box reaches; none if it misses the tile's pixel columns
             const bool xin = box.z <= (float)kTile - 0.5f && box.w >= 0.5f;
@@ -126,22 +126,24 @@ __global__ void __launch_bounds__(kThreads, 4) k_raster_fwd(FwdArgs a) {
                 const int i = c + lane;
                 const bool keep = i < n && ((sMask[i] >> warp) & 1u);
                 const unsigned bal = __ballot_sync(0xffffffffu, keep);
-                if (keep) sList[warp][m + __popc(bal & ((1u << lane) - 1u))] = (unsigned short)i;
+                if (keep)  // byte offset of the record
+                    sList[warp][m + __popc(bal & ((1u << lane) - 1u))] = (unsigned short)(48 * i);
                 m += __popc(bal);
             }
-            if (lane < kListPad) sList[warp][m + lane] = (unsigned short)kBatch;  // sentinel pad
+            if (lane < kListPad) sList[warp][m + lane] = (unsigned short)(48 * kBatch);  // sentinel
             __syncwarp();
         }
         const int rel = base + 1;
 #pragma unroll 1
         for (int j = 0; j < m && T >= kTStopF; j += kListPad) {
             const ushort4 q = *reinterpret_cast<const ushort4*>(&sList[warp][j]);
-            const int idx[kListPad] = {q.x, q.y, q.z, q.w};
+            const int offs[kListPad] = {q.x, q.y, q.z, q.w};
 #pragma unroll
             for (int u = 0; u < kListPad; ++u) {
-                const int i = idx[u];
-                const float4 p0 = sP0[i];
-                const float4 p1 = sP1[i];
+                const float4* rec =
+                    reinterpret_cast<const float4*>(reinterpret_cast<const char*>(sRec) + offs[u]);
+                const float4 p0 = rec[0];
+                const float4 p1 = rec[1];
                 const float dx = fx - p0.x, dy = fy - p0.y;
                 const float power = dx * fmaf(p0.w, dy, p0.z * dx) + p1.x * dy * dy;
                 if (power >= p1.z - kSkipDelta && T >= kTStopF) {
@@ -150,10 +152,10 @@ __global__ void __launch_bounds__(kThreads, 4) k_raster_fwd(FwdArgs a) {
                     if (power < p1.z)  // near the 1/255 floor (rare): float64 in the guard band
                         take = araw >= kFloorHi ||
                                (araw >= kFloorLo &&
-                                alpha_raw_f64_cold(a.splat, a.exact, __float_as_int(sP2[i].w), px,
+                                alpha_raw_f64_cold(a.splat, a.exact, __float_as_int(rec[2].w), px,
                                                    py) >= kFloor);
                     if (take) {
-                        const float4 c = sP2[i];
+                        const float4 c = rec[2];
                         const float alpha = fminf(araw, kClampF);
                         const float w = alpha * T;
                         cr = fmaf(w, c.x, cr);
@@ -163,7 +165,7 @@ __global__ void __launch_bounds__(kThreads, 4) k_raster_fwd(FwdArgs a) {
                         wsum += w;
                         T = T * (1.0f - alpha);
                         ++count;
-                        last = rel + i;
+                        last = rel + offs[u] / 48;
                     }
                 }
             }
