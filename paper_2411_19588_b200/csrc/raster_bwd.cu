@@ -84,10 +84,13 @@ __global__ void __launch_bounds__(kThreads, MINB) k_raster_bwd(BwdArgs a) {
     __shared__ int sRow[ROWS ? kBatch : 1];  // (filter writes only positions < nb <= kBatch)
     __shared__ int sMarkCur[ROWS ? kMaxMarks : 1], sMarkSkip[ROWS ? kMaxMarks : 1];
     __shared__ int sScan[kWarps];
-    __shared__ StageA sA[kBatch];
-    __shared__ StageB sB[kBatch];
-    __shared__ StageC sC[kBatch];
-    __shared__ float4 sD[kBatch];                  // pre-filter box (stage_extent)
+    struct __align__(16) Rec {
+        StageA A;
+        StageB B;
+        StageC C;
+        float4 D;  // pre-filter box (stage_extent)
+    };
+    __shared__ Rec sRec[kBatch];  // one array: one base address for all four loads
     __shared__ float sAcc[kWarps][9][kBatch + 1];  // per-warp partials; +1: the 8 storing lanes hit distinct banks
     __shared__ int sHit[kWarps][kBatch];           // sAcc[w][.][k] valid
     __shared__ float sMed[kWarps][9];
@@ -215,15 +218,16 @@ __global__ void __launch_bounds__(kThreads, MINB) k_raster_bwd(BwdArgs a) {
         for (int s = 0; s < kBatch / kThreads; ++s) {
             const int i = threadIdx.x + s * kThreads;
             if (i < nb) {
-                stage_entry(a.splat, ROWS ? sRow[i] : a.entries[start + lo + i], ox, oy, sA[i],
-                            sB[i], sC[i]);
-                sD[i] = stage_extent(sA[i], sB[i]);
+                Rec& r = sRec[i];
+                stage_entry(a.splat, ROWS ? sRow[i] : a.entries[start + lo + i], ox, oy, r.A, r.B,
+                            r.C);
+                r.D = stage_extent(r.A, r.B);
             }
         }
         __syncthreads();
         // back to front over the entries this warp's pixels consumed
         for (int k = min(nb, wmax - lo) - 1; k >= 0; --k) {
-            const float4 D = sD[k];
+            const float4 D = sRec[k].D;
             // misses this warp's band or the tile's pixel columns (uniform)
             if (D.y < band_lo || D.x > band_hi || D.w < 0.5f || D.z > (float)kTile - 0.5f) continue;
             const int jrel = lo + k;
@@ -232,9 +236,9 @@ __global__ void __launch_bounds__(kThreads, MINB) k_raster_bwd(BwdArgs a) {
             float sdp = 0.f, sdpy = 0.f, sdpyy = 0.f, wg0 = 0.f, wg1 = 0.f, wg2 = 0.f, dx = 0.f;
             bool hit = false;
             if (fx >= D.z && fx <= D.w) {  // column inside the box
-                const StageA A = sA[k];
-                const StageB B = sB[k];
-                const StageC C = sC[k];
+                const StageA A = sRec[k].A;
+                const StageB B = sRec[k].B;
+                const StageC C = sRec[k].C;
                 dx = fx - A.mx;
                 const float tA = A.A * dx;
                 const float skipv = B.hi - kSkipDelta;
@@ -307,10 +311,10 @@ __global__ void __launch_bounds__(kThreads, MINB) k_raster_bwd(BwdArgs a) {
             }
             if (any) {
                 // natural-units conic from the log2-scaled staged values
-                const float ca = sA[k].A * (-2.0f * kLn2);
-                const float cb = sA[k].B * (-kLn2);
-                const float cc = sB[k].C * (-2.0f * kLn2);
-                float* g = a.screen + (size_t)sC[k].row * 9;
+                const float ca = sRec[k].A.A * (-2.0f * kLn2);
+                const float cb = sRec[k].A.B * (-kLn2);
+                const float cc = sRec[k].B.C * (-2.0f * kLn2);
+                float* g = a.screen + (size_t)sRec[k].C.row * 9;
                 atomicAdd(g + 0, s[0]);                      // d_logit (before (1-s))
                 atomicAdd(g + 1, ca * s[1] + cb * s[2]);     // d_mean2d x
                 atomicAdd(g + 2, cb * s[1] + cc * s[2]);     // d_mean2d y
