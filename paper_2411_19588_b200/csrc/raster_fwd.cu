@@ -21,10 +21,8 @@ namespace uws {
 namespace {
 
 constexpr int kBatch = 256;
-constexpr int kThreads = kRasterThreads;       // one pixel per thread
-constexpr int kWarps = kThreads / 32;          // 8
-constexpr int kBandRows = kTile / kWarps;      // each warp owns a 2-row band of the tile
 constexpr int kListPad = 4;                    // per-warp lists are walked 4 entries at a time
+constexpr int kFwdPx = 2;                      // pixels per thread (measured: 1 and 4 are slower)
 
 struct FwdArgs {
     const uws_splat* splat;
@@ -39,18 +37,26 @@ struct FwdArgs {
     uws_raster_out out;
 };
 
-// Bit b set <=> the staged box [ylo, yhi] reaches a pixel centre of band b.
+// Bit b set <=> the staged box [ylo, yhi] reaches a pixel centre of band b
+// (band b = rows R*b .. R*b + R - 1, nb bands).
+template <int R, int NB>
 __device__ __forceinline__ unsigned band_mask(float ylo, float yhi) {
-    // band b covers centres 2b + 0.5 .. 2b + 1.5
-    const float lo = fmaxf(ceilf((ylo - 1.5f) * 0.5f), 0.f);
-    const float hi = fminf(floorf((yhi - 0.5f) * 0.5f), (float)(kWarps - 1));
-    if (!(lo <= hi)) return (ylo != ylo || yhi != yhi) ? 0xffu : 0u;  // NaN box: no pre-filter
+    const float lo = fmaxf(ceilf((ylo - ((float)R - 0.5f)) * (1.0f / R)), 0.f);
+    const float hi = fminf(floorf((yhi - 0.5f) * (1.0f / R)), (float)(NB - 1));
+    if (!(lo <= hi)) return (ylo != ylo || yhi != yhi) ? ((1u << NB) - 1u) : 0u;  // NaN: no filter
     const unsigned l = (unsigned)lo, h = (unsigned)hi;
     return ((2u << h) - 1u) & ~((1u << l) - 1u);
 }
 
-template <bool ROWS>
-__global__ void __launch_bounds__(kThreads, 4) k_raster_fwd(FwdArgs a) {
+// PX horizontally adjacent pixels per thread (1 or 2); a warp owns a band of
+// 32*PX/16 rows.  The PX pixels of a thread share the record loads, dy and the
+// C*dy*dy term; each pixel's power is the same float expression as in K8.
+template <bool ROWS, int PX>
+__global__ void __launch_bounds__(kRasterThreads / PX, 4 * PX) k_raster_fwd(FwdArgs a) {
+    constexpr int kThreads = kRasterThreads / PX;
+    constexpr int kWarps = kThreads / 32;
+    constexpr int kBandRows = kTile / kWarps;
+    constexpr int kLanesPerRow = kTile / PX;
     // staged records, 3 x float4 each (+1: a sentinel that never passes):
     //   [mx, my, A, B] [C, op, hi, depth] [r, g, b, row]
     __shared__ float4 sRec[3 * (kBatch + 1)];
@@ -63,14 +69,28 @@ __global__ void __launch_bounds__(kThreads, 4) k_raster_fwd(FwdArgs a) {
     const int ty = tile / a.gx, tx = tile - ty * a.gx;
     const int ox = tx * kTile, oy = ty * kTile;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    const int lx = lane & (kTile - 1), ly = warp * kBandRows + (lane >> 4);
-    const float fx = (float)lx + 0.5f, fy = (float)ly + 0.5f;
-    const int px = ox + lx, py = oy + ly;
-    const bool inside = px < a.width && py < a.height;
+    const int lx0 = (lane % kLanesPerRow) * PX, ly = warp * kBandRows + lane / kLanesPerRow;
+    const float fy = (float)ly + 0.5f;
+    const int py = oy + ly;
 
     // pixel state; T = 0 marks a pixel outside the image as finished
-    float T = inside ? 1.0f : 0.0f, cr = 0.f, cg = 0.f, cb = 0.f, dsum = 0.f, wsum = 0.f;
-    int count = 0, last = 0;
+    float fx[PX], T[PX], cr[PX], cg[PX], cb[PX], dsum[PX], wsum[PX];
+    int count[PX], last[PX];
+    bool inside[PX];
+#pragma unroll
+    for (int j = 0; j < PX; ++j) {
+        fx[j] = (float)(lx0 + j) + 0.5f;
+        inside[j] = ox + lx0 + j < a.width && py < a.height;
+        T[j] = inside[j] ? 1.0f : 0.0f;
+        cr[j] = cg[j] = cb[j] = dsum[j] = wsum[j] = 0.f;
+        count[j] = last[j] = 0;
+    }
+    auto alive = [&]() {
+        bool any = false;
+#pragma unroll
+        for (int j = 0; j < PX; ++j) any |= T[j] >= kTStopF;
+        return any;
+    };
     if (threadIdx.x == 0) {
         sRec[3 * kBatch + 0] = make_float4(0.f, 0.f, 0.f, 0.f);
         sRec[3 * kBatch + 1] = make_float4(0.f, 0.f, __int_as_float(0x7f800000), 0.f);  // hi = +inf
@@ -87,9 +107,8 @@ __global__ void __launch_bounds__(kThreads, 4) k_raster_fwd(FwdArgs a) {
     }
     int base = 0;  // tile-list entries consumed so far
     while (true) {
-        if (__syncthreads_count(!(T >= kTStopF)) == kThreads) break;
+        if (__syncthreads_count(!alive()) == kThreads) break;
         int n;
-        int row = -1;
         if (ROWS) {
             // fill the staging list with >= 256 rows of this tile (or all that remain)
             while (nst < kBatch && cur < end) {
@@ -99,29 +118,32 @@ __global__ void __launch_bounds__(kThreads, 4) k_raster_fwd(FwdArgs a) {
             }
             n = min(nst, kBatch);
             if (n == 0) break;
-            if (threadIdx.x < n) row = sRow[threadIdx.x];
         } else {
             if (start + base >= end) break;
             n = min(kBatch, end - start - base);
-            if (threadIdx.x < n) row = a.entries[start + base + threadIdx.x];
         }
-        if (row >= 0) {
-            StageA sa;
-            StageB sb;
-            StageC sc;
-            stage_entry(a.splat, row, ox, oy, sa, sb, sc);
-            sRec[3 * threadIdx.x + 0] = make_float4(sa.mx, sa.my, sa.A, sa.B);
-            sRec[3 * threadIdx.x + 1] = make_float4(sb.C, sb.op, sb.hi, sb.depth);
-            sRec[3 * threadIdx.x + 2] = make_float4(sc.r, sc.g, sc.b, __int_as_float(sc.row));
-            const float4 box = stage_extent(sa, sb);
-            // bands the box reaches; none if it misses the tile's pixel columns
-            const bool xin = box.z <= (float)kTile - 0.5f && box.w >= 0.5f;
-            sMask[threadIdx.x] = xin ? (unsigned char)band_mask(box.x, box.y) : 0u;
+#pragma unroll
+        for (int s = 0; s < kBatch / kThreads; ++s) {
+            const int i = threadIdx.x + s * kThreads;
+            if (i < n) {
+                const int row = ROWS ? sRow[i] : a.entries[start + base + i];
+                StageA sa;
+                StageB sb;
+                StageC sc;
+                stage_entry(a.splat, row, ox, oy, sa, sb, sc);
+                sRec[3 * i + 0] = make_float4(sa.mx, sa.my, sa.A, sa.B);
+                sRec[3 * i + 1] = make_float4(sb.C, sb.op, sb.hi, sb.depth);
+                sRec[3 * i + 2] = make_float4(sc.r, sc.g, sc.b, __int_as_float(sc.row));
+                const float4 box = stage_extent(sa, sb);
+                // bands the box reaches; none if it misses the tile's pixel columns
+                const bool xin = box.z <= (float)kTile - 0.5f && box.w >= 0.5f;
+                sMask[i] = xin ? (unsigned char)band_mask<kBandRows, kWarps>(box.x, box.y) : 0u;
+            }
         }
         __syncthreads();
         // this warp's entries: those whose box reaches its band, in list order
         int m = 0;
-        if (__any_sync(0xffffffffu, T >= kTStopF)) {
+        if (__any_sync(0xffffffffu, alive())) {
             for (int c = 0; c < n; c += 32) {
                 const int i = c + lane;
                 const bool keep = i < n && ((sMask[i] >> warp) & 1u);
@@ -135,8 +157,8 @@ __global__ void __launch_bounds__(kThreads, 4) k_raster_fwd(FwdArgs a) {
         }
         const int rel = base + 1;
 #pragma unroll 1
-        for (int j = 0; j < m && T >= kTStopF; j += kListPad) {
-            const ushort4 q = *reinterpret_cast<const ushort4*>(&sList[warp][j]);
+        for (int jl = 0; jl < m && alive(); jl += kListPad) {
+            const ushort4 q = *reinterpret_cast<const ushort4*>(&sList[warp][jl]);
             const int offs[kListPad] = {q.x, q.y, q.z, q.w};
 #pragma unroll
             for (int u = 0; u < kListPad; ++u) {
@@ -144,28 +166,33 @@ __global__ void __launch_bounds__(kThreads, 4) k_raster_fwd(FwdArgs a) {
                     reinterpret_cast<const float4*>(reinterpret_cast<const char*>(sRec) + offs[u]);
                 const float4 p0 = rec[0];
                 const float4 p1 = rec[1];
-                const float dx = fx - p0.x, dy = fy - p0.y;
-                const float power = dx * fmaf(p0.w, dy, p0.z * dx) + p1.x * dy * dy;
-                if (power >= p1.z - kSkipDelta && T >= kTStopF) {
-                    const float araw = p1.y * ex2_ftz(power);
-                    bool take = true;
-                    if (power < p1.z)  // near the 1/255 floor (rare): float64 in the guard band
-                        take = araw >= kFloorHi ||
-                               (araw >= kFloorLo &&
-                                alpha_raw_f64_cold(a.splat, a.exact, __float_as_int(rec[2].w), px,
-                                                   py) >= kFloor);
-                    if (take) {
-                        const float4 c = rec[2];
-                        const float alpha = fminf(araw, kClampF);
-                        const float w = alpha * T;
-                        cr = fmaf(w, c.x, cr);
-                        cg = fmaf(w, c.y, cg);
-                        cb = fmaf(w, c.z, cb);
-                        dsum = fmaf(w, p1.w, dsum);
-                        wsum += w;
-                        T = T * (1.0f - alpha);
-                        ++count;
-                        last = rel + offs[u] / 48;
+                const float dy = fy - p0.y;
+                const float qy = p1.x * dy * dy;
+#pragma unroll
+                for (int j = 0; j < PX; ++j) {
+                    const float dx = fx[j] - p0.x;
+                    const float power = dx * fmaf(p0.w, dy, p0.z * dx) + qy;
+                    if (power >= p1.z - kSkipDelta && T[j] >= kTStopF) {
+                        const float araw = p1.y * ex2_ftz(power);
+                        bool take = true;
+                        if (power < p1.z)  // near the 1/255 floor (rare): float64 in the guard band
+                            take = araw >= kFloorHi ||
+                                   (araw >= kFloorLo &&
+                                    alpha_raw_f64_cold(a.splat, a.exact, __float_as_int(rec[2].w),
+                                                       ox + lx0 + j, py) >= kFloor);
+                        if (take) {
+                            const float4 c = rec[2];
+                            const float alpha = fminf(araw, kClampF);
+                            const float w = alpha * T[j];
+                            cr[j] = fmaf(w, c.x, cr[j]);
+                            cg[j] = fmaf(w, c.y, cg[j]);
+                            cb[j] = fmaf(w, c.z, cb[j]);
+                            dsum[j] = fmaf(w, p1.w, dsum[j]);
+                            wsum[j] += w;
+                            T[j] = T[j] * (1.0f - alpha);
+                            ++count[j];
+                            last[j] = rel + offs[u] / 48;
+                        }
                     }
                 }
             }
@@ -191,33 +218,36 @@ __global__ void __launch_bounds__(kThreads, 4) k_raster_fwd(FwdArgs a) {
             nst = rem;
         }
     }
-    if (!inside) return;
-    const int pix = py * a.width + px;
-    const float depth = count > 0 ? dsum / wsum : a.far_plane;
-    a.out.depth[pix] = depth;
-    a.out.weight[pix] = wsum;
-    a.out.final_T[pix] = T;
-    a.out.count[pix] = count;
-    if (a.out.last) a.out.last[pix] = last;
-    const float c3[3] = {cr, cg, cb};
-    if (a.medium == nullptr) {
+#pragma unroll
+    for (int j = 0; j < PX; ++j) {
+        if (!inside[j]) continue;
+        const int pix = py * a.width + ox + lx0 + j;
+        const float depth = count[j] > 0 ? dsum[j] / wsum[j] : a.far_plane;
+        a.out.depth[pix] = depth;
+        a.out.weight[pix] = wsum[j];
+        a.out.final_T[pix] = T[j];
+        a.out.count[pix] = count[j];
+        if (a.out.last) a.out.last[pix] = last[j];
+        const float c3[3] = {cr[j], cg[j], cb[j]};
+        if (a.medium == nullptr) {
+#pragma unroll
+            for (int ch = 0; ch < 3; ++ch) {
+                a.out.color[3 * pix + ch] = c3[ch];
+                if (a.out.color_clean) a.out.color_clean[3 * pix + ch] = c3[ch];
+            }
+            continue;
+        }
+        // underwater epilogue: z = logistic(depth); C*exp(-Bd z) + Binf (1 - exp(-Bb z))
+        const float z = 2.0f / (1.0f + expf(-(float)kLogisticRate * depth)) - 1.0f;
 #pragma unroll
         for (int ch = 0; ch < 3; ++ch) {
-            a.out.color[3 * pix + ch] = c3[ch];
-            if (a.out.color_clean) a.out.color_clean[3 * pix + ch] = c3[ch];
+            const float att = expf(-a.medium[ch] * z);
+            const float bs = a.medium[3 + ch] * (1.0f - expf(-a.medium[6 + ch] * z));
+            a.out.color[3 * pix + ch] = c3[ch] * att + bs;
+            a.out.color_clean[3 * pix + ch] = c3[ch];
+            if (a.out.attenuation) a.out.attenuation[3 * pix + ch] = att;
+            if (a.out.backscatter) a.out.backscatter[3 * pix + ch] = bs;
         }
-        return;
-    }
-    // underwater epilogue: z = logistic(depth); C*exp(-Bd z) + Binf (1 - exp(-Bb z))
-    const float z = 2.0f / (1.0f + expf(-(float)kLogisticRate * depth)) - 1.0f;
-#pragma unroll
-    for (int ch = 0; ch < 3; ++ch) {
-        const float att = expf(-a.medium[ch] * z);
-        const float bs = a.medium[3 + ch] * (1.0f - expf(-a.medium[6 + ch] * z));
-        a.out.color[3 * pix + ch] = c3[ch] * att + bs;
-        a.out.color_clean[3 * pix + ch] = c3[ch];
-        if (a.out.attenuation) a.out.attenuation[3 * pix + ch] = att;
-        if (a.out.backscatter) a.out.backscatter[3 * pix + ch] = bs;
     }
 }
 
@@ -248,7 +278,7 @@ extern "C" int uws_raster_fwd(const uws_projected* proj, const int32_t* offsets,
     a.far_plane = (float)cam->far_plane;
     a.medium = medium;
     a.out = *out;
-    k_raster_fwd<false><<<a.gx * gy, kThreads, 0, as_stream(stream)>>>(a);
+    k_raster_fwd<false, kFwdPx><<<a.gx * gy, kRasterThreads / kFwdPx, 0, as_stream(stream)>>>(a);
     UWS_CHECK_LAUNCH("k_raster_fwd");
     return UWS_OK;
 }
@@ -275,7 +305,7 @@ extern "C" int uws_raster_fwd_rows(const uws_projected* proj, const int32_t* row
     a.far_plane = (float)cam->far_plane;
     a.medium = medium;
     a.out = *out;
-    k_raster_fwd<true><<<a.gx * gy, kThreads, 0, as_stream(stream)>>>(a);
+    k_raster_fwd<true, kFwdPx><<<a.gx * gy, kRasterThreads / kFwdPx, 0, as_stream(stream)>>>(a);
     UWS_CHECK_LAUNCH("k_raster_fwd_rows");
     return UWS_OK;
 }
