@@ -21,7 +21,9 @@
 namespace uws {
 namespace {
 
-constexpr int kThreads = 256;
+constexpr int kThreads = 128;
+constexpr int kIpt = 2;
+constexpr int kMinBlocks = 8;
 
 struct Proj {
     double mx, my, depth, a, b, c, radius, k0, k1, k2, s;
@@ -94,45 +96,58 @@ __device__ __forceinline__ bool project_one(const uws_cloud& cl, const uws_camer
     return true;
 }
 
-__global__ void __launch_bounds__(kThreads, 6) k_preprocess(uws_cloud cl, uws_camera cam,
-                                                         uws_projected out, int gx, int gy,
-                                                         unsigned long long* status,
-                                                         unsigned* ticket) {
+// writes one visible row
+__device__ __forceinline__ void emit_row(uws_projected& out, unsigned long long row, int64_t i,
+                                         const Proj& p) {
+    out.source_index[row] = (int32_t)i;
+    uws_splat sp;
+    sp.mx = p.mx; sp.my = p.my;
+    sp.ca = (float)p.k0; sp.cb = (float)p.k1; sp.cc = (float)p.k2; sp.opacity = (float)p.s;
+    sp.r = p.r; sp.g = p.g; sp.b = p.bl; sp.depth = (float)p.depth;
+    out.splat[row] = sp;
+    double4 ex4 = make_double4(p.k0, p.k1, p.k2, p.s);
+    reinterpret_cast<double4*>(out.exact)[row] = ex4;
+    out.depth[row] = p.depth;
+    short4 rc = make_short4(p.x0, p.y0, p.x1, p.y1);
+    reinterpret_cast<short4*>(out.rect)[row] = rc;
+    if (out.cov2d) {
+        out.cov2d[3 * row + 0] = p.a;
+        out.cov2d[3 * row + 1] = p.b;
+        out.cov2d[3 * row + 2] = p.c;
+    }
+    if (out.radius) out.radius[row] = p.radius;
+}
+
+// kIpt consecutive Gaussians per thread (independent float64 chains the
+// scheduler can interleave); a block covers kThreads * kIpt Gaussians.
+__global__ void __launch_bounds__(kThreads, kMinBlocks) k_preprocess(uws_cloud cl, uws_camera cam,
+                                                                     uws_projected out, int gx,
+                                                                     int gy,
+                                                                     unsigned long long* status,
+                                                                     unsigned* ticket) {
     __shared__ int s_tile;
     __shared__ unsigned long long s_scan[kThreads / 32 + 1];
     __shared__ unsigned long long s_base;
     if (threadIdx.x == 0) s_tile = (int)atomicAdd(ticket, 1u);
     __syncthreads();
     const int tile = s_tile;
-    const int64_t i = (int64_t)tile * kThreads + threadIdx.x;
-    Proj p;
-    bool vis = false;
-    if (i < cl.n) vis = project_one(cl, cam, i, gx, gy, p);
+    const int64_t i0 = ((int64_t)tile * kThreads + threadIdx.x) * kIpt;
+    Proj p[kIpt];
+    bool vis[kIpt];
+    unsigned cnt = 0;
+#pragma unroll
+    for (int q = 0; q < kIpt; ++q) {
+        vis[q] = i0 + q < cl.n && project_one(cl, cam, i0 + q, gx, gy, p[q]);
+        cnt += vis[q];
+    }
     unsigned long long total;
-    unsigned long long ex = block_exclusive_sum<kThreads, unsigned long long>(vis ? 1ull : 0ull,
-                                                                             s_scan, &total);
+    unsigned long long ex = block_exclusive_sum<kThreads, unsigned long long>(cnt, s_scan, &total);
     if (threadIdx.x == 0) s_base = lookback_exclusive(status, tile, total);
     __syncthreads();
-    const unsigned long long row = s_base + ex;
-    if (vis) {
-        out.source_index[row] = (int32_t)i;
-        uws_splat sp;
-        sp.mx = p.mx; sp.my = p.my;
-        sp.ca = (float)p.k0; sp.cb = (float)p.k1; sp.cc = (float)p.k2; sp.opacity = (float)p.s;
-        sp.r = p.r; sp.g = p.g; sp.b = p.bl; sp.depth = (float)p.depth;
-        out.splat[row] = sp;
-        double4 ex4 = make_double4(p.k0, p.k1, p.k2, p.s);
-        reinterpret_cast<double4*>(out.exact)[row] = ex4;
-        out.depth[row] = p.depth;
-        short4 rc = make_short4(p.x0, p.y0, p.x1, p.y1);
-        reinterpret_cast<short4*>(out.rect)[row] = rc;
-        if (out.cov2d) {
-            out.cov2d[3 * row + 0] = p.a;
-            out.cov2d[3 * row + 1] = p.b;
-            out.cov2d[3 * row + 2] = p.c;
-        }
-        if (out.radius) out.radius[row] = p.radius;
-    }
+    unsigned long long row = s_base + ex;
+#pragma unroll
+    for (int q = 0; q < kIpt; ++q)
+        if (vis[q]) emit_row(out, row++, i0 + q, p[q]);
     if (tile == (int)gridDim.x - 1 && threadIdx.x == kThreads - 1)
         *out.num_visible = (int32_t)(s_base + total);
 }
@@ -144,7 +159,7 @@ using namespace uws;
 
 extern "C" int uws_preprocess_workspace_size(int64_t n, size_t* bytes) {
     UWS_REQUIRE(bytes != nullptr && n >= 0, "uws_preprocess_workspace_size: bad argument");
-    int64_t blocks = ceil_div(n > 0 ? n : 1, kThreads);
+    int64_t blocks = ceil_div(n > 0 ? n : 1, kThreads * kIpt);
     Workspace ws(nullptr, 0, true);
     ws.take<unsigned long long>(blocks);
     ws.take<unsigned>(1);
@@ -165,7 +180,7 @@ extern "C" int uws_preprocess_fwd(const uws_cloud* cloud, const uws_camera* cam,
     }
     int gx = (int)ceil_div(cam->width, kTile), gy = (int)ceil_div(cam->height, kTile);
     UWS_REQUIRE(gx < 32768 && gy < 32768, "uws_preprocess_fwd: image too large for int16 tile ids");
-    int64_t blocks = ceil_div(cloud->n, kThreads);
+    int64_t blocks = ceil_div(cloud->n, kThreads * kIpt);
     Workspace ws(workspace, workspace_bytes);
     auto* status = ws.take<unsigned long long>(blocks);
     auto* ticket = ws.take<unsigned>(1);
