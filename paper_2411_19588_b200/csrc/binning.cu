@@ -581,8 +581,9 @@ struct CountPlan {
     uint32_t* keys_hi;            // high words of the depth bits (sort input)
     uint32_t* keys_hi_sorted;
     uint32_t* sorted_rows;
-    uint32_t* long_cnt;           // runs of equal high words longer than kShortRun
+    uint32_t* long_cnt;           // [0] runs of equal high words longer than kShortRun, [1] > 32
     uint32_t* long_list;
+    uint32_t* huge_list;
     uint32_t* m_band;             // [nbands][nblk_r] counts, scanned in place
     unsigned long long* rstat;    // look-back status of the band scan (row-list path)
     unsigned* rticket;
@@ -599,8 +600,9 @@ void plan_count(Workspace& ws, uint32_t k, int nbands, CountPlan& p) {
     p.keys_hi = ws.take<uint32_t>(kk);
     p.keys_hi_sorted = ws.take<uint32_t>(kk);
     p.sorted_rows = ws.take<uint32_t>(kk);
-    p.long_cnt = ws.take<uint32_t>(1);
+    p.long_cnt = ws.take<uint32_t>(2);
     p.long_list = ws.take<uint32_t>(kk / (depth_sort::kShortRun + 1) + 1);
+    p.huge_list = ws.take<uint32_t>(kk / (depth_sort::kWarpRun + 1) + 1);
     p.m_band = ws.take<uint32_t>((size_t)nbands * p.nblk_r);
     p.rstat = ws.take<unsigned long long>(ceil_div((size_t)nbands * p.nblk_r, kThreads * kScanIpt));
     p.rticket = ws.take<unsigned>(1);
@@ -691,8 +693,11 @@ extern "C" int uws_bin_count(const uws_projected* proj, int64_t k_cap, const uws
     depth_sort::k_tie_fix<<<(unsigned)ceil_div(kc, 256), 256, 0, st>>>(
         p.keys_hi_sorted, p.sorted_rows, dbits, k_dev, kc, p.long_cnt, p.long_list);
     UWS_CHECK_LAUNCH("k_tie_fix");
+    depth_sort::k_tie_fix_warp<<<148, 256, 0, st>>>(p.keys_hi_sorted, p.sorted_rows, dbits, k_dev,
+                                                    kc, p.long_cnt, p.long_list, p.huge_list);
+    UWS_CHECK_LAUNCH("k_tie_fix_warp");
     depth_sort::k_tie_fix_long<<<32, depth_sort::kLongThreads, 0, st>>>(
-        p.keys_hi_sorted, p.sorted_rows, dbits, k_dev, kc, p.long_cnt, p.long_list, p.v_tmp);
+        p.keys_hi_sorted, p.sorted_rows, dbits, k_dev, kc, p.long_cnt, p.huge_list, p.v_tmp);
     UWS_CHECK_LAUNCH("k_tie_fix_long");
     // 1a. per-block band histograms + totals (E entries, S band items)
     k_band_count<<<p.nblk_r, kThreads, 0, st>>>(p.sorted_rows, (const short4*)proj->rect,

@@ -9,6 +9,8 @@
 // (low word, row) order:
 //   * runs of <= kShortRun rows: one thread, odd-even transposition network in
 //     registers (stable: adjacent swaps on strictly greater keys, max-key padding);
+//   * runs of up to 32 rows: one warp, bitonic sort on (low word << 32 | row)
+//     (unique keys, so the order equals the stable one);
 //   * longer runs (pathological: many Gaussians at almost the same depth): one
 //     CTA per run, a stable 4-pass LSD counting sort on the low word.
 // Rows enter the sort in ascending order, so every stage is stable and the
@@ -22,13 +24,14 @@ namespace uws {
 namespace depth_sort {
 
 constexpr int kShortRun = 8;
+constexpr int kWarpRun = 32;
 constexpr int kLongThreads = 256;
 
-// high 32 bits of the depth's bit pattern; zeroes the long-run counter
+// high 32 bits of the depth's bit pattern; zeroes the run counters
 __global__ void k_depth_hi(const uint64_t* __restrict__ depth_bits, const uint32_t* __restrict__ n_dev,
                            uint32_t n_cap, uint32_t* __restrict__ keys, uint32_t* long_cnt) {
     const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
-    if (i == 0) *long_cnt = 0;
+    if (i < 2) long_cnt[i] = 0;  // [0] runs > kShortRun, [1] runs > kWarpRun
     const uint32_t n = min(*n_dev, n_cap);
     if (i < n) keys[i] = (uint32_t)(depth_bits[i] >> 32);
 }
@@ -81,12 +84,53 @@ __global__ void k_tie_fix(const uint32_t* __restrict__ keys, uint32_t* __restric
         if ((uint32_t)j < len) rows[i + j] = r[j];
 }
 
+// One warp per run of kShortRun < len: runs of up to 32 rows are sorted in
+// registers by a warp bitonic network on (low word << 32 | row); longer runs
+// are passed on to k_tie_fix_long.
+__global__ void __launch_bounds__(256) k_tie_fix_warp(
+    const uint32_t* __restrict__ keys, uint32_t* __restrict__ rows,
+    const uint64_t* __restrict__ depth_bits, const uint32_t* __restrict__ n_dev, uint32_t n_cap,
+    uint32_t* __restrict__ cnt, const uint32_t* __restrict__ list, uint32_t* __restrict__ huge) {
+    const uint32_t n = min(*n_dev, n_cap);
+    const uint32_t runs = cnt[0];
+    const int lane = threadIdx.x & 31;
+    const uint32_t nwarps = gridDim.x * (blockDim.x / 32);
+    for (uint32_t r = blockIdx.x * (blockDim.x / 32) + (threadIdx.x >> 5); r < runs; r += nwarps) {
+        const uint32_t start = list[r];
+        const uint32_t k = keys[start];
+        const uint32_t j = start + lane;
+        const bool in = j < n && keys[j] == k;
+        const unsigned ball = __ballot_sync(0xffffffffu, in);
+        // run length within this window: contiguous from lane 0
+        const int len = __popc(~ball) == 0 ? 32 : __ffs(~ball) - 1;
+        if (len == 32 && start + 32 < n && keys[start + 32] == k) {  // longer than a warp
+            if (lane == 0) huge[atomicAdd(&cnt[1], 1u)] = start;
+            continue;
+        }
+        const uint32_t row = lane < len ? rows[j] : 0u;
+        unsigned long long key =
+            lane < len ? ((unsigned long long)(uint32_t)depth_bits[row] << 32) | row : ~0ull;
+#pragma unroll
+        for (int kk = 2; kk <= 32; kk <<= 1) {
+#pragma unroll
+            for (int jj = kk >> 1; jj > 0; jj >>= 1) {
+                const unsigned long long other = __shfl_xor_sync(0xffffffffu, key, jj);
+                const bool up = (lane & kk) == 0;       // ascending sub-sequence
+                const bool lower = (lane & jj) == 0;    // this lane holds the smaller slot
+                const bool take_min = up == lower;
+                key = take_min ? (other < key ? other : key) : (other > key ? other : key);
+            }
+        }
+        if (lane < len) rows[j] = (uint32_t)key;
+    }
+}
+
 // One CTA per long run: find its end, then 4 stable counting-sort passes on the
 // low word (8 bits each), chunk by chunk in order, ping-ponging with tmp.
 __global__ void __launch_bounds__(kLongThreads) k_tie_fix_long(
     const uint32_t* __restrict__ keys, uint32_t* __restrict__ rows,
     const uint64_t* __restrict__ depth_bits, const uint32_t* __restrict__ n_dev, uint32_t n_cap,
-    const uint32_t* __restrict__ long_cnt, const uint32_t* __restrict__ long_list,
+    const uint32_t* __restrict__ long_cnt, const uint32_t* __restrict__ long_list,  // runs > 32
     uint32_t* __restrict__ tmp) {
     constexpr int W = kLongThreads / 32;
     __shared__ uint32_t s_base[256];
@@ -94,7 +138,7 @@ __global__ void __launch_bounds__(kLongThreads) k_tie_fix_long(
     __shared__ uint32_t s_tmp[W + 1];
     __shared__ uint32_t s_end;
     const uint32_t n = min(*n_dev, n_cap);
-    const uint32_t cnt = *long_cnt;
+    const uint32_t cnt = long_cnt[1];
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     for (uint32_t run = blockIdx.x; run < cnt; run += gridDim.x) {
         const uint32_t start = long_list[run];
