@@ -137,3 +137,26 @@ def test_pipelined_steps_match_synchronous(cap):
         assert _close(getattr(sa.cloud, f), getattr(sb.cloud, f)), f
     assert torch.equal(sa.obs_count, sb.obs_count)
     assert float(ea.grads.flat.abs().max()) == 0.0
+
+
+def test_engine_with_nothing_visible():
+    """Every Gaussian behind the camera: K = 0 through sort, lists, both raster
+    kernels and Adam; the image is the medium alone and only the medium learns."""
+    g = load("survey2k")
+    s, cam = _state(g)
+    pos = s.cloud.positions.clone()
+    pos[:, 2] = -50.0                       # behind the look_at camera
+    s.cloud.positions.copy_(pos)
+    before = {f: getattr(s.cloud, f).clone() for f in FIELDS}
+    eng = uw.StepEngine(s, cam.width, cam.height, uw.OptimConfig())
+    gt = torch.as_tensor(g.gt, dtype=torch.float32).cuda()
+    st = eng.step([(cam, gt)])
+    assert not st.skipped and np.isfinite(st.total)
+    out = eng.last_render()
+    assert int(out.count.sum()) == 0
+    for f in FIELDS:   # zero gradients: only the renormalisation touches rotations
+        if f != "rotations":
+            assert torch.equal(getattr(s.cloud, f), before[f]), f
+    assert float(s.medium_exp_avg.abs().sum()) > 0.0
+    r = eng.render(cam)
+    assert int(r.count.sum()) == 0
