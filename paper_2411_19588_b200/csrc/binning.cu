@@ -186,28 +186,6 @@ __global__ void __launch_bounds__(kThreads) k_band_count(const uint32_t* __restr
     }
 }
 
-// one item per iteration, in lane order; its buckets [lo, lo+cnt) are distinct
-__device__ __forceinline__ void warp_append_1d(int lo, int cnt, uint2 val, int* cur, uint2* out,
-                                               int lane) {
-    unsigned any = __ballot_sync(0xffffffffu, cnt > 0);
-    while (any) {
-        const int j = __ffs(any) - 1;
-        any &= any - 1;
-        const int l0 = __shfl_sync(0xffffffffu, lo, j);
-        const int n = __shfl_sync(0xffffffffu, cnt, j);
-        uint2 v;
-        v.x = __shfl_sync(0xffffffffu, val.x, j);
-        v.y = __shfl_sync(0xffffffffu, val.y, j);
-        for (int l = lane; l < n; l += 32) {
-            const int b = l0 + l;
-            const int pos = cur[b];
-            cur[b] = pos + 1;
-            out[pos] = v;
-        }
-        __syncwarp();
-    }
-}
-
 // 32 items (one per lane, lane order == list order) appended to the buckets
 // [lo, hi] they cover: bucket by bucket, the covering lanes write consecutive
 // slots from the bucket's cursor (coalesced runs, no per-item serial chain)
