@@ -8,25 +8,25 @@
 // produced by two levels of STABLE bucketing of the depth-sorted rows, so
 // every tile entry is written exactly once and no E-sized key is ever read
 // back:
-//   0. stable radix sort of the K visible rows by the bit pattern of their
-//      float64 depth (positive doubles order like their bits; rows are in
-//      source order, so stability yields the source-index tie-break);
-//   1. rank order -> BAND lists (a band = 4 tile rows): each Gaussian is
-//      appended, in rank order, to the list of every band its rectangle
-//      touches;
-//   2. band lists -> tile lists: each (Gaussian, band) item is appended, in
-//      list order, to the tiles of its rectangle inside the band.
+//   0. stable order of the K visible rows by the bit pattern of their float64
+//      depth (positive doubles order like their bits; rows are in source
+//      order, so stability yields the source-index tie-break): radix sort of
+//      the high words + run fix-up (depth_sort.cuh);
+//   1. rank order -> tile-ROW lists (kBand = 1 tile row per band): each
+//      Gaussian is appended, in rank order, to the list of every tile row its
+//      rectangle touches, as an 8-byte item (row, column span).  The training
+//      and render kernels filter these row lists per tile on the fly;
+//   2. (API path only) row lists -> tile lists: each (Gaussian, row) item is
+//      appended, in list order, to the tiles of its span.
 // A stable append needs, per (block of items, bucket), the number of earlier
 // items in the same bucket.  Each block is cut into 8 warp sub-blocks; a warp
 // builds its bucket histogram with shared-memory difference arrays and a warp
-// scan, block totals are scanned across blocks, and each warp then walks its
-// items IN ORDER, one item per iteration, its lanes covering the item's
-// buckets (all distinct) with private shared-memory cursors -- deterministic,
-// no global atomics, bit-identical to the reference order given the same
-// depths and rectangles.  The 4-row bands make the level-2 items ~3x fewer
-// and ~3x fatter than tile-row items (~21 cells: one warp iteration each).
-// Level-2 blocks stage their entries in shared memory so each tile run
-// leaves the SM as coalesced stores.
+// scan, block totals are scanned across blocks (decoupled look-back), and each
+// warp then appends its items 32 at a time, bucket by bucket: the lanes whose
+// span covers the bucket write consecutive slots from its cursor in list
+// order -- deterministic, no global atomics, bit-identical to the reference
+// order given the same depths and rectangles.  Level-2 blocks stage their
+// entries in shared memory so each tile run leaves the SM as coalesced stores.
 #include <algorithm>
 
 #include "depth_sort.cuh"
