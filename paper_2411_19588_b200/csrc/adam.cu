@@ -160,6 +160,68 @@ __global__ void __launch_bounds__(kThreads, MINB) k_adam_cloud(float* __restrict
     P[o + 3] = (float)__ddiv_rn(d, nr);
 }
 
+// Vector form for even n (the rotation block [6n, 10n) is then 16-byte aligned
+// and every float4 group holds either one quaternion or four scalars of the
+// other fields): one thread per group, 16-byte loads of p, m, v and g; the
+// first n threads also fold the densify statistics of Gaussian t.
+__global__ void __launch_bounds__(kThreads, 4) k_adam_cloud4(float* __restrict__ P,
+                                                             float* __restrict__ M,
+                                                             float* __restrict__ V,
+                                                             float* __restrict__ Gr, int64_t n,
+                                                             uws_adam_params hp, AdamCtl ctl) {
+    const int64_t t = (int64_t)blockIdx.x * kThreads + threadIdx.x;
+    const int64_t groups = 14 * n / 4;
+    if (t >= groups) return;
+    const bool skip = ctl.skip && *ctl.skip > 0.0f;
+    if (t < n) {
+        if (!skip && ctl.grad_accum) {
+            ctl.grad_accum[t] += Gr[14 * n + t];
+            ctl.obs_count[t] += (int32_t)Gr[15 * n + t];
+        }
+        if (ctl.zero_grads) {
+            Gr[14 * n + t] = 0.f;
+            Gr[15 * n + t] = 0.f;
+        }
+    }
+    float4* const G4 = reinterpret_cast<float4*>(Gr) + t;
+    if (skip) {
+        if (ctl.zero_grads) *G4 = make_float4(0.f, 0.f, 0.f, 0.f);
+        return;
+    }
+    const float4 p4 = reinterpret_cast<const float4*>(P)[t];
+    const float4 m4 = reinterpret_cast<const float4*>(M)[t];
+    const float4 v4 = reinterpret_cast<const float4*>(V)[t];
+    const float4 g4 = *G4;
+    float p[4] = {p4.x, p4.y, p4.z, p4.w}, m[4] = {m4.x, m4.y, m4.z, m4.w};
+    float v[4] = {v4.x, v4.y, v4.z, v4.w};
+    const float g[4] = {g4.x, g4.y, g4.z, g4.w};
+    const int64_t j0 = 4 * t;
+    const bool rot = j0 >= 6 * n && j0 < 10 * n;
+#pragma unroll
+    for (int c = 0; c < 4; ++c) {
+        const int64_t j = j0 + c;
+        const int f = rot ? 2 : (j < 3 * n ? 0 : (j < 6 * n ? 1 : (j < 13 * n ? 3 : 4)));
+        const AdamK k{hp.lr[f], hp.bias1[f], hp.bias2[f], hp.inv_bias1[f], hp.inv_bias2[f]};
+        adam1(p[c], m[c], v[c], g[c], k, hp);
+    }
+    if (rot) {
+        // normalize_rotations: q / max(|q|, 1e-12) in float64, stored float32
+        const double a = p[0], b = p[1], c = p[2], d = p[3];
+        double nr = __dsqrt_rn(__dadd_rn(__dadd_rn(__dadd_rn(__dmul_rn(a, a), __dmul_rn(b, b)),
+                                                  __dmul_rn(c, c)),
+                                         __dmul_rn(d, d)));
+        nr = fmax(nr, 1e-12);
+        p[0] = (float)__ddiv_rn(a, nr);
+        p[1] = (float)__ddiv_rn(b, nr);
+        p[2] = (float)__ddiv_rn(c, nr);
+        p[3] = (float)__ddiv_rn(d, nr);
+    }
+    reinterpret_cast<float4*>(P)[t] = make_float4(p[0], p[1], p[2], p[3]);
+    reinterpret_cast<float4*>(M)[t] = make_float4(m[0], m[1], m[2], m[3]);
+    reinterpret_cast<float4*>(V)[t] = make_float4(v[0], v[1], v[2], v[3]);
+    if (ctl.zero_grads) *G4 = make_float4(0.f, 0.f, 0.f, 0.f);
+}
+
 __global__ void k_adam_medium(float* __restrict__ P, float* __restrict__ M, float* __restrict__ V,
                               float* __restrict__ Gr, uws_adam_params hp, AdamCtl ctl) {
     const int v = threadIdx.x;
@@ -212,12 +274,21 @@ extern "C" int uws_adam_step(float* params, float* exp_avg, float* exp_avg_sq, f
     }
     if (n > 0) {
         UWS_REQUIRE(params && exp_avg && exp_avg_sq && grads, "uws_adam_step: null cloud buffer");
-        constexpr int kEpt = 2;
-        const int nb_flat = (int)ceil_div(10 * n, kThreads * kEpt);
-        const int nb_rot = (int)ceil_div(n, kThreads);
-        k_adam_cloud<kEpt, 4><<<(unsigned)(nb_flat + nb_rot), kThreads, 0, st>>>(
-            params, exp_avg, exp_avg_sq, grads, n, nb_flat, *hp, ctl);
-        UWS_CHECK_LAUNCH("k_adam_cloud");
+        const bool aligned = n % 2 == 0 &&
+                             ((uintptr_t)params | (uintptr_t)exp_avg | (uintptr_t)exp_avg_sq |
+                              (uintptr_t)grads) % 16 == 0;
+        if (aligned) {
+            k_adam_cloud4<<<(unsigned)ceil_div(14 * n / 4, kThreads), kThreads, 0, st>>>(
+                params, exp_avg, exp_avg_sq, grads, n, *hp, ctl);
+            UWS_CHECK_LAUNCH("k_adam_cloud4");
+        } else {
+            constexpr int kEpt = 2;
+            const int nb_flat = (int)ceil_div(10 * n, kThreads * kEpt);
+            const int nb_rot = (int)ceil_div(n, kThreads);
+            k_adam_cloud<kEpt, 4><<<(unsigned)(nb_flat + nb_rot), kThreads, 0, st>>>(
+                params, exp_avg, exp_avg_sq, grads, n, nb_flat, *hp, ctl);
+            UWS_CHECK_LAUNCH("k_adam_cloud");
+        }
     }
     if (medium_params && zero_grads) {
         // medium slots and pad zeroed after every reader is done; the skip

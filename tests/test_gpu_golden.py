@@ -141,3 +141,33 @@ def test_adam_bit_exact(scene):
         np.testing.assert_array_equal(np_(state.adam[f].v), vh[f], err_msg=f)
     for f in med_names:
         np.testing.assert_array_equal(np_(getattr(medium, f)), med_host[f], err_msg=f)
+
+
+@pytest.mark.parametrize("n", [1999, 2000])
+def test_adam_bit_exact_odd_and_even_n(n):
+    """Both Adam kernels (vector for even n, scalar for odd n) == the reference adam_step."""
+    g = load("survey2k")
+    arrays = {f: getattr(g.cloud, f)[:n] for f in ("positions", "log_scales", "rotations",
+                                                   "sh_coeffs", "opacity_logits")}
+    cloud = uw.GaussianCloud(**arrays)
+    state = uw.TrainState(cloud, uw.MediumParams.zero(), iteration=3)
+    buf = uw.GradientBuffer(n)
+    buf.flat.copy_(torch.as_tensor(np.random.default_rng(5).normal(
+        scale=1e-3, size=buf.flat.numel()).astype(np.float32)))
+    cfg = uw.OptimConfig()
+    host = {f: np.asarray(v, np.float32).copy() for f, v in arrays.items()}
+    mh = {f: np.zeros_like(v) for f, v in host.items()}
+    vh = {f: np.zeros_like(v) for f, v in host.items()}
+    lrs = {"positions": uw.position_lr(3, cfg), "log_scales": cfg.scaling_lr,
+           "rotations": cfg.rotation_lr, "sh_coeffs": cfg.feature_lr,
+           "opacity_logits": cfg.opacity_lr}
+    for step in (1, 2):
+        uw.apply_gradients(state, buf, cfg)
+        for f in host:
+            gr = np_(getattr(buf, "d_" + f))
+            host[f], mh[f], vh[f] = O.adam(host[f], gr, mh[f], vh[f], step, lrs[f])
+        host["rotations"] = O.renormalize(host["rotations"])
+    for f in host:
+        np.testing.assert_array_equal(np_(getattr(cloud, f)), host[f], err_msg=f)
+        np.testing.assert_array_equal(np_(state.adam[f].m), mh[f], err_msg=f)
+        np.testing.assert_array_equal(np_(state.adam[f].v), vh[f], err_msg=f)
