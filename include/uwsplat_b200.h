@@ -196,11 +196,13 @@ int uws_raster_bwd_rows(const uws_projected* proj, const int32_t* row_start,
  *      guidance subgradient lambda_guide*sign(.) is added into the medium
  *      slots (backward.py:270-274).  nonfinite (optional device float) is
  *      incremented when an accumulated gradient is not finite
- *      (GradientBuffer.all_finite, backward.py:66-69). ----------------- */
+ *      (GradientBuffer.all_finite, backward.py:66-69).  accumulate = 0
+ *      stores the visible rows' parameter gradients instead of adding them
+ *      (first view into a buffer known to be zero: saves the read). ------ */
 int uws_preprocess_bwd(const uws_cloud* cloud, const uws_camera* cam, const uws_projected* proj,
                        int64_t k_cap, float* screen_grads, double* medium_acc,
                        const float* medium, int32_t has_guidance, double lambda_guide,
-                       float* grads, float* nonfinite, void* stream);
+                       float* grads, float* nonfinite, int32_t accumulate, void* stream);
 
 /* ---- optimizer (replaces optim.apply_gradients :98-120 / adam_step :69-83,
  *      GaussianCloud.normalize_rotations scene.py:165-167 and

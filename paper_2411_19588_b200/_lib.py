@@ -84,7 +84,7 @@ _SIGS = {
                                     c_void_p]),
     "uws_preprocess_bwd": (c_int, [POINTER(CloudC), POINTER(CameraC), POINTER(ProjectedC),
                                    c_int64, c_void_p, c_void_p, c_void_p, c_int32, c_double,
-                                   c_void_p, c_void_p, c_void_p]),
+                                   c_void_p, c_void_p, c_int32, c_void_p]),
     "uws_adam_step": (c_int, [c_void_p, c_void_p, c_void_p, c_void_p, c_int64, c_void_p,
                               c_void_p, c_void_p, c_void_p, POINTER(AdamParamsC), c_void_p,
                               c_void_p, c_void_p, c_int32, c_void_p]),

@@ -124,5 +124,5 @@ def backward_render(out: RenderOutput, dL_dC, cloud: GaussianCloud,
     guided = 1 if (medium is not None and medium.has_guidance) else 0
     _lib.call("uws_preprocess_bwd", ctypes.byref(cl), ctypes.byref(cc), ctypes.byref(pc), k_cap,
               _lib.ptr(screen), _lib.ptr(med_acc), med, guided, float(lambda_guide),
-              _lib.ptr(buf.flat), 0, st)
+              _lib.ptr(buf.flat), 0, 1, st)
     return buf

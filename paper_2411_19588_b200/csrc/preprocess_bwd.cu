@@ -18,6 +18,7 @@ namespace {
 
 constexpr int kThreads = 128;
 
+template <bool ACC>  // add into the gradient buffer (else store: it is known to be zero)
 __global__ void __launch_bounds__(kThreads, 6) k_preprocess_bwd(uws_cloud cl, uws_camera cam,
                                                              const int32_t* __restrict__ src_index,
                                                              const double* __restrict__ exact,
@@ -134,31 +135,31 @@ __global__ void __launch_bounds__(kThreads, 6) k_preprocess_bwd(uws_cloud cl, uw
     bool finite = true;
 #pragma unroll
     for (int c = 0; c < 3; ++c) {
-        float v = gpos[3 * i + c] + (float)(dtx * R[c] + dty * R[3 + c] + dtz * R[6 + c]);
+        float v = (ACC ? gpos[3 * i + c] : 0.f) + (float)(dtx * R[c] + dty * R[3 + c] + dtz * R[6 + c]);
         gpos[3 * i + c] = v;
         finite &= isfinite(v);
-        v = gls[3 * i + c] + (float)dls[c];
+        v = (ACC ? gls[3 * i + c] : 0.f) + (float)dls[c];
         gls[3 * i + c] = v;
         finite &= isfinite(v);
         const double col = (double)cl.sh_coeffs[3 * i + c] * kSH_C0 + 0.5;
-        v = gsh[3 * i + c] + (col > 0.0 ? (float)(kSH_C0 * dcol[c]) : 0.0f);
+        v = (ACC ? gsh[3 * i + c] : 0.f) + (col > 0.0 ? (float)(kSH_C0 * dcol[c]) : 0.0f);
         gsh[3 * i + c] = v;
         finite &= isfinite(v);
     }
 #pragma unroll
     for (int c = 0; c < 4; ++c) {
-        float v = grot[4 * i + c] + (float)div_pos_nz(dq[c] - G.qu[c] * radial, G.qn);
+        float v = (ACC ? grot[4 * i + c] : 0.f) + (float)div_pos_nz(dq[c] - G.qu[c] * radial, G.qn);
         grot[4 * i + c] = v;
         finite &= isfinite(v);
     }
     {
-        float v = gop[i] + (float)((1.0 - sop) * gl);
+        float v = (ACC ? gop[i] : 0.f) + (float)((1.0 - sop) * gl);
         gop[i] = v;
         finite &= isfinite(v);
     }
     const double nx = dmx * cam.width * 0.5, ny = dmy * cam.height * 0.5;
-    gnorm[i] += (float)sqrt_nz(nx * nx + ny * ny);
-    gobs[i] += 1.0f;
+    gnorm[i] = (ACC ? gnorm[i] : 0.f) + (float)sqrt_nz(nx * nx + ny * ny);
+    gobs[i] = (ACC ? gobs[i] : 0.f) + 1.0f;
     if (!finite && nonfinite) atomicAdd(nonfinite, 1.0f);
 }
 
@@ -189,16 +190,22 @@ extern "C" int uws_preprocess_bwd(const uws_cloud* cloud, const uws_camera* cam,
                                   const uws_projected* proj, int64_t k_cap, float* screen_grads,
                                   double* medium_acc, const float* medium, int32_t has_guidance,
                                   double lambda_guide, float* grads, float* nonfinite,
-                                  void* stream) {
+                                  int32_t accumulate, void* stream) {
     UWS_REQUIRE(cloud && cam && proj && grads && proj->num_visible, "uws_preprocess_bwd: null argument");
     UWS_REQUIRE(k_cap >= 0 && k_cap <= cloud->n, "uws_preprocess_bwd: k out of range");
     UWS_REQUIRE(medium_acc == nullptr || medium != nullptr, "uws_preprocess_bwd: medium missing");
     cudaStream_t st = as_stream(stream);
     if (k_cap > 0) {
         UWS_REQUIRE(screen_grads != nullptr, "uws_preprocess_bwd: screen_grads missing");
-        k_preprocess_bwd<<<(unsigned)ceil_div(k_cap, kThreads), kThreads, 0, st>>>(
-            *cloud, *cam, proj->source_index, proj->exact, proj->num_visible, screen_grads, grads,
-            nonfinite);
+        const unsigned nb = (unsigned)ceil_div(k_cap, kThreads);
+        if (accumulate)
+            k_preprocess_bwd<true><<<nb, kThreads, 0, st>>>(*cloud, *cam, proj->source_index,
+                                                           proj->exact, proj->num_visible,
+                                                           screen_grads, grads, nonfinite);
+        else
+            k_preprocess_bwd<false><<<nb, kThreads, 0, st>>>(*cloud, *cam, proj->source_index,
+                                                            proj->exact, proj->num_visible,
+                                                            screen_grads, grads, nonfinite);
         UWS_CHECK_LAUNCH("k_preprocess_bwd");
     }
     if (medium_acc) {

@@ -193,7 +193,8 @@ class StepEngine:
         _lib.call("uws_preprocess_bwd", ctypes.byref(cl), ctypes.byref(cc), ctypes.byref(pc),
                   self.n, _lib.ptr(self.screen), _lib.ptr(self.med_acc), _lib.ptr(medium.flat),
                   guided, float(self.cfg.lambda_guide), _lib.ptr(self.grads.flat),
-                  _lib.ptr(self.grads.nonfinite), st)
+                  _lib.ptr(self.grads.nonfinite), 1 if view > 0 else 0, st)
+        # (the first view stores: Adam leaves the parameter gradients zeroed)
 
     def last_render(self) -> RenderOutput:
         """Forward buffers of the most recent view (valid until the next step).
