@@ -160,3 +160,26 @@ def test_engine_with_nothing_visible():
     assert float(s.medium_exp_avg.abs().sum()) > 0.0
     r = eng.render(cam)
     assert int(r.count.sum()) == 0
+
+
+def test_engine_two_views_per_step_equals_summed_api_gradients():
+    """max_views=2: the engine's step (first view stores, second accumulates) ==
+    apply_gradients on the sum of the two API backward buffers."""
+    g = load("survey2k")
+    sa, cam0 = _state(g)
+    sb, _ = _state(g)
+    cam1 = uw.Camera.look_at((2.5, -2.2, -1.2), (0, 0, 12), width=cam0.width,
+                             height=cam0.height, fx=cam0.fx, fy=cam0.fy)
+    gt = torch.as_tensor(g.gt, dtype=torch.float32).cuda()
+    cfg = uw.OptimConfig()
+    eng = uw.StepEngine(sa, cam0.width, cam0.height, cfg, max_views=2)
+    st = eng.step([(cam0, gt), (cam1, gt)])
+    assert not st.skipped and st.views == 2
+    buf = uw.GradientBuffer(len(sb.cloud))
+    for cam in (cam0, cam1):
+        out = uw.render(sb.cloud, cam, sb.medium, "underwater")
+        _, dL = uw.total_loss(out.color, gt, sb.medium, cfg.lambda_ssim, cfg.lambda_guide)
+        uw.backward_render(out, dL, sb.cloud, sb.medium, cfg.lambda_guide, buf=buf)
+    uw.apply_gradients(sb, buf, cfg)
+    for f in FIELDS:
+        assert _close(getattr(sa.cloud, f), getattr(sb.cloud, f)), f
