@@ -158,6 +158,7 @@ class StageTimer:
     def __init__(self, torch):
         self.torch = torch
         self.events = {}
+        self.order = []      # (name, start, end) in launch order
         self.enabled = False
 
     def wrap(self, lib_mod):
@@ -173,12 +174,21 @@ class StageTimer:
             r = orig(name, *args)
             e.record()
             timer.events.setdefault(name, []).append((s, e))
+            timer.order.append((name, s, e))
             return r
 
         lib_mod.call = call
 
     def totals(self):
         return {k: sum(s.elapsed_time(e) for s, e in v) for k, v in self.events.items()}
+
+    def gaps(self):
+        """Device time between consecutive timed calls (other launches, memsets,
+        host-side stalls), summed per preceding stage."""
+        out = {}
+        for (n0, _, e0), (_, s1, _) in zip(self.order, self.order[1:]):
+            out[n0] = out.get(n0, 0.0) + max(e0.elapsed_time(s1), 0.0)
+        return out
 
 
 def run_gpu(args):
@@ -254,8 +264,12 @@ def run_gpu(args):
         step_resident()
     clocks = ClockSampler(local)
     with clocks:
-        ms, launches = timed(step_resident, args.steps, stage_timer=True)
+        ms, launches = timed(step_resident, args.steps)
+    # per-stage breakdown from a separate run with CUDA events around every C-ABI
+    # call (kept out of the timed region above)
+    timed(step_resident, args.steps, stage_timer=True)
     stages = timer.totals()
+    gaps = timer.gaps()
     for _ in range(max(1, args.warmup // 2)):
         step_e2e()
     ms_e2e, _ = timed(step_e2e, args.steps)
@@ -382,6 +396,7 @@ def run_gpu(args):
         "render_fps": render_fps,
         "roofline": roofline,
         "stages_ms": {k: round(v, 4) for k, v in per_step.items()},
+        "gaps_after_stage_ms": {k: round(v / args.steps, 4) for k, v in gaps.items()},
         "stage_share": stage_share,
         "stage_roofline": stage_roofline,
         "workload_stats": {"K": k_vis, "E": e_ent, "P_pix": p_pix},
