@@ -148,22 +148,22 @@ __global__ void __launch_bounds__(kRasterThreads / PX, 4 * PX) k_raster_fwd(FwdA
                 const int i = c + lane;
                 const bool keep = i < n && ((sMask[i] >> warp) & 1u);
                 const unsigned bal = __ballot_sync(0xffffffffu, keep);
-                if (keep)  // byte offset of the record
-                    sList[warp][m + __popc(bal & ((1u << lane) - 1u))] = (unsigned short)(48 * i);
+                if (keep)  // index of the staged record
+                    sList[warp][m + __popc(bal & ((1u << lane) - 1u))] = (unsigned short)i;
                 m += __popc(bal);
             }
-            if (lane < kListPad) sList[warp][m + lane] = (unsigned short)(48 * kBatch);  // sentinel
+            if (lane < kListPad) sList[warp][m + lane] = (unsigned short)kBatch;  // sentinel
             __syncwarp();
         }
         const int rel = base + 1;
 #pragma unroll 1
         for (int jl = 0; jl < m && alive(); jl += kListPad) {
             const ushort4 q = *reinterpret_cast<const ushort4*>(&sList[warp][jl]);
-            const int offs[kListPad] = {q.x, q.y, q.z, q.w};
+            const int idx[kListPad] = {q.x, q.y, q.z, q.w};
 #pragma unroll
             for (int u = 0; u < kListPad; ++u) {
                 const float4* rec =
-                    reinterpret_cast<const float4*>(reinterpret_cast<const char*>(sRec) + offs[u]);
+                    sRec + 3 * idx[u];
                 const float4 p0 = rec[0];
                 const float4 p1 = rec[1];
                 const float dy = fy - p0.y;
@@ -191,7 +191,7 @@ __global__ void __launch_bounds__(kRasterThreads / PX, 4 * PX) k_raster_fwd(FwdA
                             wsum[j] += w;
                             T[j] = T[j] * (1.0f - alpha);
                             ++count[j];
-                            last[j] = rel + offs[u] / 48;
+                            last[j] = rel + idx[u];
                         }
                     }
                 }
