@@ -51,6 +51,15 @@ __device__ __forceinline__ unsigned band_mask(float ylo, float yhi) {
 // PX horizontally adjacent pixels per thread (1 or 2); a warp owns a band of
 // 32*PX/16 rows.  The PX pixels of a thread share the record loads, dy and the
 // C*dy*dy term; each pixel's power is the same float expression as in K8.
+__device__ __forceinline__ float4 lds128(uint32_t addr) {
+    float4 v;
+    asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];"
+                 : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w)
+                 : "r"(addr)
+                 : "memory");
+    return v;
+}
+
 template <bool ROWS, int PX>
 __global__ void __launch_bounds__(kRasterThreads / PX, 4 * PX) k_raster_fwd(FwdArgs a) {
     constexpr int kThreads = kRasterThreads / PX;
@@ -97,6 +106,8 @@ __global__ void __launch_bounds__(kRasterThreads / PX, 4 * PX) k_raster_fwd(FwdA
         sRec[3 * kBatch + 2] = make_float4(0.f, 0.f, 0.f, 0.f);
     }
 
+    // 32-bit shared-window address of the record array, kept in one register
+    const uint32_t sbase = (uint32_t)__cvta_generic_to_shared(sRec);
     int start = 0, end = 0, cur = 0, nst = 0;
     if (ROWS) {
         cur = a.row_start[ty];
@@ -162,10 +173,9 @@ __global__ void __launch_bounds__(kRasterThreads / PX, 4 * PX) k_raster_fwd(FwdA
             const int idx[kListPad] = {q.x, q.y, q.z, q.w};
 #pragma unroll
             for (int u = 0; u < kListPad; ++u) {
-                const float4* rec =
-                    sRec + 3 * idx[u];
-                const float4 p0 = rec[0];
-                const float4 p1 = rec[1];
+                const uint32_t ra = sbase + 48u * (uint32_t)idx[u];
+                const float4 p0 = lds128(ra);
+                const float4 p1 = lds128(ra + 16u);
                 const float dy = fy - p0.y;
                 const float qy = p1.x * dy * dy;
 #pragma unroll
@@ -178,10 +188,10 @@ __global__ void __launch_bounds__(kRasterThreads / PX, 4 * PX) k_raster_fwd(FwdA
                         if (power < p1.z)  // near the 1/255 floor (rare): float64 in the guard band
                             take = araw >= kFloorHi ||
                                    (araw >= kFloorLo &&
-                                    alpha_raw_f64_cold(a.splat, a.exact, __float_as_int(rec[2].w),
+                                    alpha_raw_f64_cold(a.splat, a.exact, __float_as_int(lds128(ra + 32u).w),
                                                        ox + lx0 + j, py) >= kFloor);
                         if (take) {
-                            const float4 c = rec[2];
+                            const float4 c = lds128(ra + 32u);
                             const float alpha = fminf(araw, kClampF);
                             const float w = alpha * T[j];
                             cr[j] = fmaf(w, c.x, cr[j]);
