@@ -168,6 +168,8 @@ __global__ void __launch_bounds__(kThreads, MINB) k_raster_bwd(BwdArgs a) {
     __syncthreads();
     const int maxlast = sMaxLast;
 
+    const uint32_t sbase = (uint32_t)__cvta_generic_to_shared(sRec);  // 64-byte records
+    static_assert(sizeof(Rec) == 64, "record layout");
     const int nbatch = (maxlast + kBatch - 1) / kBatch;
     int rend = 0, stride = 1;
     if (ROWS && nbatch > 0) {
@@ -227,7 +229,8 @@ __global__ void __launch_bounds__(kThreads, MINB) k_raster_bwd(BwdArgs a) {
         __syncthreads();
         // back to front over the entries this warp's pixels consumed
         for (int k = min(nb, wmax - lo) - 1; k >= 0; --k) {
-            const float4 D = sRec[k].D;
+            const uint32_t ra = sbase + 64u * (uint32_t)k;
+            const float4 D = lds128(ra + 48u);
             // misses this warp's band or the tile's pixel columns (uniform)
             if (D.y < band_lo || D.x > band_hi || D.w < 0.5f || D.z > (float)kTile - 0.5f) continue;
             const int jrel = lo + k;
@@ -236,9 +239,10 @@ __global__ void __launch_bounds__(kThreads, MINB) k_raster_bwd(BwdArgs a) {
             float sdp = 0.f, sdpy = 0.f, sdpyy = 0.f, wg0 = 0.f, wg1 = 0.f, wg2 = 0.f, dx = 0.f;
             bool hit = false;
             if (fx >= D.z && fx <= D.w) {  // column inside the box
-                const StageA A = sRec[k].A;
-                const StageB B = sRec[k].B;
-                const StageC C = sRec[k].C;
+                const float4 a4 = lds128(ra), b4 = lds128(ra + 16u), c4 = lds128(ra + 32u);
+                const StageA A{a4.x, a4.y, a4.z, a4.w};
+                const StageB B{b4.x, b4.y, b4.z, b4.w};
+                const StageC C{c4.x, c4.y, c4.z, __float_as_int(c4.w)};
                 dx = fx - A.mx;
                 const float tA = A.A * dx;
                 const float skipv = B.hi - kSkipDelta;

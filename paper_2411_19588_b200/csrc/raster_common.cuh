@@ -51,6 +51,17 @@ __device__ __forceinline__ float lg2_ftz(float x) {
     return y;
 }
 
+// 16-byte shared-memory load from a 32-bit shared-window address (keeps the
+// base of a record array in one register instead of rematerialising it)
+__device__ __forceinline__ float4 lds128(uint32_t addr) {
+    float4 v;
+    asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];"
+                 : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w)
+                 : "r"(addr)
+                 : "memory");
+    return v;
+}
+
 // float64 alpha_raw exactly as the reference evaluates it (rasterizer.py:159-163)
 __device__ __forceinline__ double alpha_raw_f64(const uws_splat* __restrict__ splat,
                                              const double* __restrict__ exact, int row, int px,

@@ -51,15 +51,6 @@ __device__ __forceinline__ unsigned band_mask(float ylo, float yhi) {
 // PX horizontally adjacent pixels per thread (1 or 2); a warp owns a band of
 // 32*PX/16 rows.  The PX pixels of a thread share the record loads, dy and the
 // C*dy*dy term; each pixel's power is the same float expression as in K8.
-__device__ __forceinline__ float4 lds128(uint32_t addr) {
-    float4 v;
-    asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];"
-                 : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w)
-                 : "r"(addr)
-                 : "memory");
-    return v;
-}
-
 template <bool ROWS, int PX>
 __global__ void __launch_bounds__(kRasterThreads / PX, 4 * PX) k_raster_fwd(FwdArgs a) {
     constexpr int kThreads = kRasterThreads / PX;
