@@ -120,6 +120,7 @@ __global__ void __launch_bounds__(kThreads, MINB) k_raster_bwd(BwdArgs a) {
     for (int p = 0; p < kPix; ++p) {
         const int ly = ly0 + 2 * p;
         fy[p] = (float)ly + 0.5f;
+        asm("" : "+f"(fy[p]));  // keep it in a register (not rematerialised from tid)
         S[p] = 0.f;
         T[p] = 1.f;
         mylast[p] = 0;
