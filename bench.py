@@ -270,7 +270,7 @@ def run_gpu(args):
     timed(step_resident, args.steps, stage_timer=True)
     stages = timer.totals()
     gaps = timer.gaps()
-    for _ in range(max(1, args.warmup // 2)):
+    for _ in range(max(2, args.warmup // 2)):   # both pipeline slots warm
         step_e2e()
     ms_e2e, _ = timed(step_e2e, args.steps)
     trainer.flush()

@@ -222,6 +222,8 @@ class StepEngine:
             src = gt if isinstance(gt, torch.Tensor) else torch.from_numpy(
                 np.ascontiguousarray(gt, dtype=np.float32))
             buf = slot.gt_buffer(i, (self.height, self.width, 3))
+            other = self._slots[(self._slots.index(slot) + 1) % 2]
+            other.gt_buffer(i, (self.height, self.width, 3))  # allocate both now, not mid-pipeline
             with torch.cuda.stream(cs):
                 buf.copy_(src, non_blocking=True)
             out.append((cam, buf))
