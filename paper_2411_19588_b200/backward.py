@@ -99,7 +99,8 @@ def backward_render(out: RenderOutput, dL_dC, cloud: GaussianCloud,
     ``buf`` (optional) is accumulated into instead of a fresh buffer, which is
     how several views are summed before one optimizer step.
     """
-    if out.proj is None or out.bins is None:
+    rows = getattr(out, "rows", None)
+    if out.proj is None or (out.bins is None and rows is None):
         raise ValueError("render output was produced without retained buffers")
     proj, bins, cam = out.proj, out.bins, out.camera
     if buf is None:
@@ -117,9 +118,14 @@ def backward_render(out: RenderOutput, dL_dC, cloud: GaussianCloud,
     st = _lib.stream_handle()
     pc, cc, oc = proj.c_struct(), cam.c_struct(), out.c_struct()
     med = _lib.ptr(medium.flat) if underwater else 0
-    _lib.call("uws_raster_bwd", ctypes.byref(pc), _lib.ptr(bins.offsets), _lib.ptr(bins.entries),
-              ctypes.byref(cc), med, ctypes.byref(oc), _lib.ptr(dL), _lib.ptr(screen),
-              _lib.ptr(med_acc), st)
+    if rows is not None:   # the forward composited from row lists: filter them again
+        _lib.call("uws_raster_bwd_rows", ctypes.byref(pc), _lib.ptr(rows.row_start),
+                  _lib.ptr(rows.items), ctypes.byref(cc), med, ctypes.byref(oc), _lib.ptr(dL),
+                  _lib.ptr(screen), _lib.ptr(med_acc), st)
+    else:
+        _lib.call("uws_raster_bwd", ctypes.byref(pc), _lib.ptr(bins.offsets),
+                  _lib.ptr(bins.entries), ctypes.byref(cc), med, ctypes.byref(oc), _lib.ptr(dL),
+                  _lib.ptr(screen), _lib.ptr(med_acc), st)
     cl = cloud.c_struct()
     guided = 1 if (medium is not None and medium.has_guidance) else 0
     _lib.call("uws_preprocess_bwd", ctypes.byref(cl), ctypes.byref(cc), ctypes.byref(pc), k_cap,

@@ -40,7 +40,7 @@ from .backward import GradientBuffer
 from .losses import total_loss_device
 from .optim import OptimConfig, apply_gradients_device, rollback_steps
 from .projection import ProjectedCloud, preprocess_into
-from .rasterizer import RenderOutput, _alloc_output
+from .rasterizer import RenderOutput, RowLists, _alloc_output
 from .scene import Camera, TrainState
 
 log = logging.getLogger(__name__)
@@ -202,6 +202,7 @@ class StepEngine:
         out = self.out
         out.proj = self.proj
         out.bins = None
+        out.rows = RowLists(self.gx, self.gy, self.row_start, self.row_items)
         return out
 
     # -- ground truth staging -------------------------------------------------------

@@ -77,6 +77,66 @@ def bin_and_sort(proj: ProjectedCloud, width: int, height: int,
     return TileBins(gx, gy, offsets, entries[:e])
 
 
+class RowLists:
+    """Tile-ROW lists: for every tile row, the depth-ordered 8-byte items
+    ``(row, x0 | x1 << 16)`` of the Gaussians whose rectangle spans it.  The
+    list of tile (tx, ty) is the subsequence of row ty's list whose column span
+    contains tx, so the compositing kernels filter it on the fly."""
+
+    def __init__(self, grid_x: int, grid_y: int, row_start: torch.Tensor, items: torch.Tensor):
+        self.grid_x = grid_x
+        self.grid_y = grid_y
+        self.row_start = row_start
+        self.items = items
+
+
+def bin_rows(proj: ProjectedCloud, width: int, height: int) -> RowLists:
+    """First level of bin_and_sort (rasterizer.py:50-85): the stable depth order
+    bucketed into tile-row lists (one host read of the item count)."""
+    cam = Camera(width=width, height=height, fx=1.0, fy=1.0, cx=0.0, cy=0.0, R=[[1, 0, 0],
+                 [0, 1, 0], [0, 0, 1]], t=[0, 0, 0])
+    gx, gy = cam.grid
+    dev = proj.device
+    row_start = torch.zeros(gy + 1, dtype=torch.int32, device=dev)
+    k_cap = proj.n_source
+    if k_cap == 0:
+        return RowLists(gx, gy, row_start, torch.zeros(1, 2, dtype=torch.int32, device=dev))
+    cb, eb = _lib.size_out(), _lib.size_out()
+    _lib.call("uws_bin_workspace_size", k_cap, 0, gx, gy, ctypes.byref(cb), ctypes.byref(eb))
+    count_ws = torch.empty(cb.value, dtype=torch.uint8, device=dev)
+    totals = torch.zeros(2, dtype=torch.int64, device=dev)
+    overflow = torch.zeros(1, dtype=torch.int32, device=dev)
+    pc, cc = proj.c_struct(), cam.c_struct()
+    st = _lib.stream_handle()
+    _lib.call("uws_bin_count", ctypes.byref(pc), k_cap, ctypes.byref(cc), _lib.ptr(totals),
+              _lib.ptr(count_ws), cb.value, st)
+    s = int(totals[1].item())
+    items = torch.empty(max(s, 1), 2, dtype=torch.int32, device=dev)
+    _lib.call("uws_bin_rows", ctypes.byref(pc), k_cap, max(s, 1), ctypes.byref(cc),
+              _lib.ptr(totals), _lib.ptr(row_start), _lib.ptr(items), _lib.ptr(overflow), 0,
+              _lib.ptr(count_ws), cb.value, st)
+    return RowLists(gx, gy, row_start, items)
+
+
+class _LazyTileBins(TileBins):
+    """TileBins materialised on first access (render() composites from row
+    lists; the full CSR tile lists exist only if someone asks for them)."""
+
+    def __init__(self, proj: ProjectedCloud, width: int, height: int):
+        self._args = (proj, width, height)
+        self._bins = None
+        gx, gy = (width + TILE_SIZE - 1) // TILE_SIZE, (height + TILE_SIZE - 1) // TILE_SIZE
+        self.grid_x, self.grid_y = gx, gy
+
+    def _get(self) -> TileBins:
+        if self._bins is None:
+            self._bins = bin_and_sort(*self._args)
+        return self._bins
+
+    offsets = property(lambda self: self._get().offsets)
+    entries = property(lambda self: self._get().entries)
+
+
 @dataclass
 class RenderOutput:
     """Forward buffers (rasterizer.py:132-145); proj/bins retained for backward."""
@@ -94,6 +154,7 @@ class RenderOutput:
     last: Optional[torch.Tensor] = None          # per-pixel consumed list prefix
     attenuation_map: Optional[torch.Tensor] = None
     backscatter_map: Optional[torch.Tensor] = None
+    rows: Optional[RowLists] = None               # row lists the forward composited from
 
     def c_struct(self) -> _lib.RasterOutC:
         return _lib.RasterOutC(_lib.ptr(self.color), _lib.ptr(self.color_clean),
@@ -143,11 +204,21 @@ def render(cloud: GaussianCloud, cam, medium: Optional[MediumParams] = None,
         raise ValueError("underwater mode requires medium parameters")
     cam = Camera.from_any(cam)
     proj = project_cloud(cloud, cam, with_geometry=False)
-    bins = bin_and_sort(proj, cam.width, cam.height)
-    out = composite(proj, bins, cam, medium, mode, medium_maps)
+    rows = bin_rows(proj, cam.width, cam.height)
+    out = _alloc_output(cam.height, cam.width, proj.device, mode, medium_maps)
+    pc, cc, oc = proj.c_struct(), cam.c_struct(), out.c_struct()
+    med = _lib.ptr(medium.flat) if mode == "underwater" else 0
+    _lib.call("uws_raster_fwd_rows", ctypes.byref(pc), _lib.ptr(rows.row_start),
+              _lib.ptr(rows.items), ctypes.byref(cc), med, ctypes.byref(oc),
+              _lib.stream_handle())
+    out.proj, out.rows, out.camera = proj, rows, cam
+    # the reference's CSR tile lists, built only when accessed (same order and
+    # indices as the filtered row lists)
+    out.bins = _LazyTileBins(proj, cam.width, cam.height)
     if not retain:
         out.proj = None
         out.bins = None
+        out.rows = None
     return out
 
 

@@ -89,7 +89,12 @@ def test_row_list_render_matches_tile_list_render(name):
     s, cam = _state(g)
     mode = g.mode
     med = s.medium if mode == "underwater" else None
-    ref = uw.render(s.cloud, cam, med, mode)
+    # the tile-list kernel on the materialised CSR lists (rasterizer.bin_and_sort)
+    proj = uw.project_cloud(s.cloud, cam)
+    ref = uw.composite(proj, uw.bin_and_sort(proj, cam.width, cam.height), cam, med, mode)
+    api = uw.render(s.cloud, cam, med, mode)     # row lists, materialised on demand only
+    for f in ("color", "depth", "weight", "final_transmittance", "count", "last"):
+        assert torch.equal(getattr(api, f), getattr(ref, f)), f
     eng = uw.StepEngine(s, cam.width, cam.height, uw.OptimConfig(), entry_capacity=16)
     out = eng.render(cam, mode)      # tiny capacity: exercises the overflow re-run
     for f in ("color", "depth", "weight", "final_transmittance", "count", "last"):
@@ -183,3 +188,24 @@ def test_engine_two_views_per_step_equals_summed_api_gradients():
     uw.apply_gradients(sb, buf, cfg)
     for f in FIELDS:
         assert _close(getattr(sa.cloud, f), getattr(sb.cloud, f)), f
+
+
+@pytest.mark.parametrize("name", ["survey2k", "opaque3k"])
+def test_tile_list_backward_matches_row_list_backward(name):
+    """backward_render through the materialised tile lists (composite) == through the
+    row lists (render): same pairs, same order, same partials."""
+    g = load(name)
+    s, cam = _state(g)
+    med = s.medium if g.mode == "underwater" else None
+    mode = g.mode
+    gt = torch.as_tensor(g.gt, dtype=torch.float32).cuda()
+    out_rows = uw.render(s.cloud, cam, med, mode)
+    proj = uw.project_cloud(s.cloud, cam)
+    out_tiles = uw.composite(proj, uw.bin_and_sort(proj, cam.width, cam.height), cam, med, mode)
+    assert out_tiles.rows is None and out_rows.rows is not None
+    bufs = []
+    for out in (out_rows, out_tiles):
+        _, dL = uw.total_loss(out.color, gt, med, 0.3, 0.1)
+        bufs.append(np_(uw.backward_render(out, dL, s.cloud, med, 0.1).flat).astype(np.float64))
+    a, b = bufs
+    assert np.abs(a - b).max() <= 1e-5 * max(np.abs(b).max(), 1e-30)
