@@ -59,15 +59,34 @@ __global__ void __launch_bounds__(kThreads, 3) k_ssim_moments(const float* __res
     const int x0 = blockIdx.x * kT, y0 = blockIdx.y * kT;  // valid-window origin == image pixel
     const int VW = W - 2 * kR, VH = H - 2 * kR;
     const size_t plane = (size_t)VH * VW;
-    // stage rows of kP*C contiguous floats (coalesced)
-    const int rowlen = kP * C;
-    for (int i = threadIdx.x; i < kP * rowlen; i += kThreads) {
-        const int r = i / rowlen, q = i - r * rowlen;
-        const int gy = y0 + r, gx = x0 + q / C;
-        const bool ok = gy < H && gx < W;
-        const size_t o = ((size_t)gy * W + x0) * C + q;
-        sa[r * pitch + q] = ok ? __ldg(img_a + o) : 0.f;
-        sb[r * pitch + q] = ok ? __ldg(img_b + o) : 0.f;
+    // stage rows of kP*C contiguous floats (coalesced): one warp per row
+    {
+        const int rowlen = kP * C;
+        const int lane = threadIdx.x & 31;
+        const int qmax = min(rowlen, (W - x0) * C);  // columns inside the image
+        for (int r = threadIdx.x >> 5; r < kP; r += kThreads / 32) {
+            const int gy = y0 + r;
+            const float* ra = img_a + ((size_t)min(gy, H - 1) * W + x0) * C;
+            const float* rb = img_b + ((size_t)min(gy, H - 1) * W + x0) * C;
+            const bool rok = gy < H;
+            constexpr int kU = (kP * kMaxC + 31) / 32;  // covers the longest row
+            float va[kU], vb[kU];
+#pragma unroll
+            for (int u = 0; u < kU; ++u) {  // all loads in flight before the stores
+                const int q = lane + 32 * u;
+                const bool ok = rok && q < qmax;
+                va[u] = ok ? __ldg(ra + q) : 0.f;
+                vb[u] = ok ? __ldg(rb + q) : 0.f;
+            }
+#pragma unroll
+            for (int u = 0; u < kU; ++u) {
+                const int q = lane + 32 * u;
+                if (q < rowlen) {
+                    sa[r * pitch + q] = va[u];
+                    sb[r * pitch + q] = vb[u];
+                }
+            }
+        }
     }
     __syncthreads();
     float ssum = 0.f;
