@@ -29,6 +29,23 @@ constexpr double kC1 = 0.01 * 0.01, kC2 = 0.03 * 0.03;
 
 __constant__ float c_taps[kN];
 
+// 4-byte asynchronous global -> shared copy; ok = false writes a zero
+__device__ __forceinline__ void cp_async4(float* sdst, const float* gsrc, bool ok) {
+    const unsigned s = (unsigned)__cvta_generic_to_shared(sdst);
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 4, %2;" ::"r"(s), "l"(gsrc),
+                 "r"(ok ? 4 : 0)
+                 : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() {
+    asm volatile("cp.async.commit_group;" ::: "memory");
+}
+template <int N>
+__device__ __forceinline__ void cp_async_wait() {
+    asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
+}
+
+constexpr size_t kGradSmem = (size_t)(2 * 3 * kP * (kP + 1) + 3 * kP * (kT + 1)) * sizeof(float);
+
 __device__ __forceinline__ float block_sum_f(float v, float* sred) {
     v = warp_sum(v);
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -182,41 +199,42 @@ __global__ void __launch_bounds__(kThreads, 3) k_ssim_grad(const float* __restri
                                                            float k_ssim, float k_l1,
                                                            float* __restrict__ grad,
                                                            double* __restrict__ part_l1) {
-    __shared__ float sm[3][kP][kP + 1];
-    __shared__ float hs[3][kP][kT + 1];
+    // double-buffered derivative-map windows [2][3][kP][kP+1] (cp.async: the next
+    // channel's window streams in while this channel is filtered), then hs
+    extern __shared__ float smem[];
+    typedef float Win[3][kP][kP + 1];
+    Win* sbuf = reinterpret_cast<Win*>(smem);
+    float (*hs)[kP][kT + 1] = reinterpret_cast<float (*)[kP][kT + 1]>(smem + 2 * 3 * kP * (kP + 1));
     __shared__ float sred[kThreads / 32];
     const int C = CT > 0 ? CT : C_;
     const int x0 = blockIdx.x * kT, y0 = blockIdx.y * kT;
     const int VW = W - 2 * kR, VH = H - 2 * kR;
     const size_t plane = (size_t)VH * VW;
+    // adj[y][x] = sum_{u,v} w_u w_v M[y+u-2R][x+v-2R], M zero outside the valid grid
+    auto issue = [&](int ch) {
+        Win& dst = sbuf[ch & 1];
+        for (int i = threadIdx.x; i < kP * kP; i += kThreads) {
+            const int r = i / kP, c = i - r * kP;
+            const int my = y0 + r - 2 * kR, mx = x0 + c - 2 * kR;
+            const bool ok = my >= 0 && my < VH && mx >= 0 && mx < VW;
+            const size_t o = ok ? (size_t)my * VW + mx : 0;
+#pragma unroll
+            for (int m = 0; m < 3; ++m)
+                cp_async4(&dst[m][r][c], maps + (m * C + ch) * plane + o, ok);
+        }
+        cp_async_commit();
+    };
+    issue(0);
     float l1sum = 0.f;
     for (int ch = 0; ch < C; ++ch) {
-        // adj[y][x] = sum_{u,v} w_u w_v M[y+u-2R][x+v-2R], M zero outside the valid grid
-        {
-            constexpr int kIt = (kP * kP + kThreads - 1) / kThreads;
-            float x[kIt][3];
-#pragma unroll
-            for (int k = 0; k < kIt; ++k) {  // all loads in flight before the stores
-                const int i = threadIdx.x + k * kThreads;
-                const int r = i / kP, c = i - r * kP;
-                const int my = y0 + r - 2 * kR, mx = x0 + c - 2 * kR;
-                const bool ok = i < kP * kP && my >= 0 && my < VH && mx >= 0 && mx < VW;
-                const size_t o = (size_t)my * VW + mx;
-#pragma unroll
-                for (int m = 0; m < 3; ++m)
-                    x[k][m] = ok ? __ldg(maps + (m * C + ch) * plane + o) : 0.f;
-            }
-#pragma unroll
-            for (int k = 0; k < kIt; ++k) {
-                const int i = threadIdx.x + k * kThreads;
-                const int r = i / kP, c = i - r * kP;
-                if (i < kP * kP) {
-#pragma unroll
-                    for (int m = 0; m < 3; ++m) sm[m][r][c] = x[k][m];
-                }
-            }
+        if (ch + 1 < C) {
+            issue(ch + 1);
+            cp_async_wait<1>();
+        } else {
+            cp_async_wait<0>();
         }
         __syncthreads();
+        float (*sm)[kP][kP + 1] = sbuf[ch & 1];
         for (int it = threadIdx.x; it < kP * (kT / kHR); it += kThreads) {
             const int r = it >> 2, c0 = (it & 3) * kHR;
             float g[3][kHR];
@@ -405,6 +423,10 @@ extern "C" int uws_loss_fwd_bwd(const float* rendered, const float* gt, int32_t 
                                       cudaFuncAttributeMaxDynamicSharedMemorySize, mx));
         UWS_CUDA(cudaFuncSetAttribute(k_ssim_moments<0>,
                                       cudaFuncAttributeMaxDynamicSharedMemorySize, mx));
+        UWS_CUDA(cudaFuncSetAttribute(k_ssim_grad<3>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      (int)kGradSmem));
+        UWS_CUDA(cudaFuncSetAttribute(k_ssim_grad<0>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      (int)kGradSmem));
         attr_set = true;
     }
     dim3 g1((unsigned)ceil_div(vw, kT), (unsigned)ceil_div(vh, kT));
@@ -417,11 +439,11 @@ extern "C" int uws_loss_fwd_bwd(const float* rendered, const float* gt, int32_t 
     const float k_ssim = (float)(lambda_ssim * (-1.0 / n_win));
     const float k_l1 = (float)((1.0 - lambda_ssim) / n_px);
     if (c == 3)
-        k_ssim_grad<3><<<g2, kThreads, 0, st>>>(rendered, gt, h, w, c, p.maps, k_ssim, k_l1, dL_dC,
-                                                p.part_l1);
+        k_ssim_grad<3><<<g2, kThreads, kGradSmem, st>>>(rendered, gt, h, w, c, p.maps, k_ssim,
+                                                        k_l1, dL_dC, p.part_l1);
     else
-        k_ssim_grad<0><<<g2, kThreads, 0, st>>>(rendered, gt, h, w, c, p.maps, k_ssim, k_l1, dL_dC,
-                                                p.part_l1);
+        k_ssim_grad<0><<<g2, kThreads, kGradSmem, st>>>(rendered, gt, h, w, c, p.maps, k_ssim,
+                                                        k_l1, dL_dC, p.part_l1);
     UWS_CHECK_LAUNCH("k_ssim_grad");
     k_loss_finalize<<<1, kThreads, 0, st>>>(p.part_s, p.n_s, p.part_l1, p.n_l1, n_px, n_win, medium,
                                             has_guidance, lambda_ssim, lambda_guide, result,
