@@ -721,3 +721,183 @@ def densify_and_prune(arrays, m, v, grad_accum, obs_count, extent, rng,
     new_v = {f: np.concatenate([v[f][keep], np.zeros((n_added,) + v[f].shape[1:], np.float32)])
              for f in fields}
     return new, new_m, new_v, (int(clone.sum()), n_split, int(prune.sum()))
+
+
+# ---------------------------------------------------------------------------
+# guidance refresh: dark-pixel backscatter estimate (backscatter.py:52-270)
+# ---------------------------------------------------------------------------
+BS_WATER_BOX = (0.0, 1.0)          # backscatter.py:21
+BS_BACKSCATTER_BOX = (0.0, 5.0)    # backscatter.py:22
+BS_BB_STARTS = (0.1, 0.5, 1.0, 2.0, 4.0)   # backscatter.py:29
+BS_LM_ITERS = 200                  # backscatter.py:30
+BS_LM_TOL = 1e-10                  # backscatter.py:31
+
+
+def bs_resize(image, depth, resized_height):
+    """Downscale (backscatter.py:52-79, 244-249): bilinear colour, nearest depth,
+    half-pixel centres, edge clamp.  Returns float64 (image, depth)."""
+    image = np.asarray(image, dtype=np.float64)
+    depth = np.asarray(depth, dtype=np.float64)
+    h, w = image.shape[:2]
+    th = min(resized_height, h)
+    if th == h:
+        return image, depth
+    tw = max(1, round(w * th / h))
+    # nearest: truncated centre coordinate, clamped to the last row/column
+    rn = np.minimum((np.arange(th) + 0.5) * h / th, h - 1).astype(np.int64)
+    cn = np.minimum((np.arange(tw) + 0.5) * w / tw, w - 1).astype(np.int64)
+    depth = depth[rn][:, cn]
+    # bilinear: source coordinate of each output centre, clipped into the image
+    sy = np.clip((np.arange(th) + 0.5) * h / th - 0.5, 0, h - 1)
+    sx = np.clip((np.arange(tw) + 0.5) * w / tw - 0.5, 0, w - 1)
+    iy0 = np.floor(sy).astype(np.int64)
+    ix0 = np.floor(sx).astype(np.int64)
+    iy1 = np.minimum(iy0 + 1, h - 1)
+    ix1 = np.minimum(ix0 + 1, w - 1)
+    wy = (sy - iy0)[:, None, None]
+    wx = (sx - ix0)[None, :, None]
+    upper = image[iy0][:, ix0] * (1 - wx) + image[iy0][:, ix1] * wx
+    lower = image[iy1][:, ix0] * (1 - wx) + image[iy1][:, ix1] * wx
+    return upper * (1 - wy) + lower * wy, depth
+
+
+def bs_linspace_labels(values, lo, hi, num):
+    """cluster_range over linspace(lo, hi, num) (backscatter.py:82-97, numpy
+    linspace: i*step + lo, last edge = hi).  Returns (labels, degenerate);
+    raises ValueError where the reference raises DataError (non-increasing edges)."""
+    edges = np.linspace(lo, hi, num)
+    if edges.size < 2 or edges[-1] <= edges[0]:
+        return np.zeros(np.shape(values), dtype=np.int64), True
+    if np.any(np.diff(edges) <= 0):
+        raise ValueError("cluster edges must be strictly increasing")
+    lab = np.searchsorted(edges, values, side="right") - 1
+    return np.clip(lab, 0, edges.size - 2), False
+
+
+def bs_dark_pixels(image, depth, p_dark=0.01, edges_num=10):
+    """select_dark_pixels (backscatter.py:100-132): in every depth cluster the
+    ceil(p*size) smallest RGB sums, ties by raster order; returned in raster
+    order.  Restated as one stable sort on (cluster, sum)."""
+    image = np.maximum(np.asarray(image, dtype=np.float64), 0.0)
+    depth = np.maximum(np.asarray(depth, dtype=np.float64), 0.0)
+    z = depth.ravel()
+    rgb = image.reshape(-1, 3)
+    lab, degenerate = bs_linspace_labels(z, z.min(), z.max(), edges_num)
+    lab = lab.ravel()
+    sums = rgb.sum(axis=1)
+    order = np.lexsort((np.arange(z.size), sums, lab))   # cluster, then sum, then index
+    size = np.bincount(lab, minlength=1)
+    start = np.concatenate([[0], np.cumsum(size)[:-1]])
+    quota = np.maximum(1, np.ceil(p_dark * size).astype(np.int64))
+    rank = np.arange(z.size) - start[lab[order]]
+    pick = np.sort(order[rank < quota[lab[order]]])
+    return z[pick], rgb[pick], degenerate
+
+
+def _bs_sse(b_inf, b_b, z, y):
+    r = b_inf * (1.0 - np.exp(-b_b * z)) - y
+    return float(r @ r)
+
+
+def bs_lm(z, y, start, lo, hi):
+    """Box-projected Levenberg-Marquardt from one start (backscatter.py:142-175)."""
+    p = np.clip(start, lo, hi).astype(np.float64)
+    sse = _bs_sse(p[0], p[1], z, y)
+    lam = 1e-3
+    for _ in range(BS_LM_ITERS):
+        ez = np.exp(-p[1] * z)
+        jac = np.stack([1.0 - ez, p[0] * z * ez], axis=1)
+        res = p[0] * (1.0 - ez) - y
+        h = jac.T @ jac
+        g = jac.T @ res
+        moved = None
+        for _ in range(12):
+            damp = lam * np.diag(np.maximum(np.diag(h), 1e-12))
+            try:
+                d = np.linalg.solve(h + damp, -g)
+            except np.linalg.LinAlgError:
+                lam *= 10.0
+                continue
+            q = np.clip(p + d, lo, hi)
+            q_sse = _bs_sse(q[0], q[1], z, y)
+            if q_sse <= sse:
+                moved = np.linalg.norm(q - p)
+                p, sse = q, q_sse
+                lam = max(lam / 3.0, 1e-12)
+                break
+            lam *= 3.0
+        if moved is None:
+            return p, sse
+        if moved < BS_LM_TOL:
+            return p, sse
+    return p, sse
+
+
+def bs_fit(z, y, box_binf=BS_WATER_BOX, box_bb=BS_BACKSCATTER_BOX):
+    """fit_saturating_exponential (backscatter.py:178-208):
+    (b_inf, b_b, rms, degenerate)."""
+    z = np.asarray(z, dtype=np.float64).ravel()
+    y = np.asarray(y, dtype=np.float64).ravel()
+    lo = np.array([box_binf[0], box_bb[0]])
+    hi = np.array([box_binf[1], box_bb[1]])
+    if z.size < 3 or np.unique(z).size < 2:
+        b_inf = float(np.clip(np.mean(y) if y.size else 0.0, *box_binf))
+        rms = float(np.sqrt(np.mean((b_inf * (1 - np.exp(-hi[1] * z)) - y) ** 2))) if y.size else 0.0
+        return b_inf, float(hi[1]), rms, True
+    if np.max(np.abs(y)) == 0.0:
+        return float(lo[0]), float(lo[1]), 0.0, False
+    best, best_sse = None, np.inf
+    for b0 in (float(np.mean(y)), float(np.max(y))):
+        for bb0 in BS_BB_STARTS:
+            p, sse = bs_lm(z, y, np.array([b0, bb0]), lo, hi)
+            if sse < best_sse - 1e-15:
+                best, best_sse = p, sse
+    return float(best[0]), float(best[1]), float(np.sqrt(best_sse / z.size)), False
+
+
+def bs_fit_points(dark_z, colors, intervals_num=25):
+    """Per-interval per-channel lower envelope (backscatter.py:251-268): for each
+    channel a list of (z, value) in interval order."""
+    lab, degenerate = bs_linspace_labels(dark_z, dark_z.min(), dark_z.max(), intervals_num)
+    pts = []
+    for k in range(3):
+        if degenerate:
+            j = int(np.argmin(colors[:, k]))
+            pts.append((np.array([dark_z[j]]), np.array([colors[j, k]])))
+            continue
+        zs, ys = [], []
+        for i in range(intervals_num - 1):
+            idx = np.nonzero(lab == i)[0]
+            if idx.size:
+                j = idx[int(np.argmin(colors[idx, k]))]
+                zs.append(dark_z[j])
+                ys.append(colors[j, k])
+        pts.append((np.array(zs), np.array(ys)))
+    return pts, degenerate
+
+
+def estimate_backscatter(image, depth, p_dark=0.01, intervals_num=25, resized_height=300,
+                         edges_num=10):
+    """estimate_backscatter (backscatter.py:211-270).  Returns a namespace with
+    water_color_est, backscatter_est, residual (float64 (3,)), degenerate,
+    plus the intermediate dark set and fit points for stage checks."""
+    image, depth = bs_resize(image, depth, resized_height)
+    image = np.maximum(image, 0.0)
+    depth = np.maximum(depth, 0.0)
+    dz, rgb, degenerate = bs_dark_pixels(image, depth, p_dark, edges_num)
+    out = SimpleNamespace(dark_z=dz, dark_rgb=rgb, points=None)
+    if dz.size == 0 or degenerate:
+        mean = image.reshape(-1, 3).mean(axis=0)
+        out.water_color_est = np.clip(mean, *BS_WATER_BOX)
+        out.backscatter_est = np.full(3, BS_BACKSCATTER_BOX[1])
+        out.residual = np.zeros(3)
+        out.degenerate = True
+        return out
+    pts, any_deg = bs_fit_points(dz, rgb, intervals_num)
+    out.points = pts
+    fits = [bs_fit(z, y) for z, y in pts]
+    out.water_color_est = np.array([f[0] for f in fits])
+    out.backscatter_est = np.array([f[1] for f in fits])
+    out.residual = np.array([f[2] for f in fits])
+    out.degenerate = bool(any_deg or any(f[3] for f in fits))
+    return out
