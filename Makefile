@@ -6,7 +6,7 @@ SRC := paper_2411_19588_b200/csrc
 OBJ := build/obj
 LIB := paper_2411_19588_b200/libuwsplat_b200.so
 # float64 translation units that must evaluate expressions exactly like numpy
-EXACT := preprocess preprocess_bwd densify
+EXACT := preprocess preprocess_bwd densify backscatter
 FAST := binning raster_fwd raster_bwd loss adam capi
 OBJS := $(addprefix $(OBJ)/,$(addsuffix .o,$(EXACT) $(FAST)))
 HDRS := $(wildcard $(SRC)/*.cuh) include/uwsplat_b200.h
@@ -16,7 +16,7 @@ all: $(LIB)
 $(OBJ):
 	mkdir -p $(OBJ)
 
-$(OBJ)/preprocess.o $(OBJ)/preprocess_bwd.o $(OBJ)/densify.o: $(OBJ)/%.o: $(SRC)/%.cu $(HDRS) | $(OBJ)
+$(OBJ)/preprocess.o $(OBJ)/preprocess_bwd.o $(OBJ)/densify.o $(OBJ)/backscatter.o: $(OBJ)/%.o: $(SRC)/%.cu $(HDRS) | $(OBJ)
 	$(NVCC) $(NVFLAGS) -fmad=false -c $< -o $@ 2> $(OBJ)/$*.ptxas.log || (cat $(OBJ)/$*.ptxas.log; false)
 
 $(OBJ)/%.o: $(SRC)/%.cu $(HDRS) | $(OBJ)

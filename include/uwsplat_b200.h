@@ -241,6 +241,38 @@ int uws_densify_apply(const float* params, const float* exp_avg, const float* ex
 int uws_reset_opacities(float* params, float* exp_avg, float* exp_avg_sq, int64_t n, float value,
                         void* stream);
 
+/* ---- guidance refresh (replaces backscatter.estimate_backscatter :211-270,
+ *      called every refit_period iterations by pipeline.py:204-208).
+ *      image: (h, w, 3) float32; depth: (h, w), either the remapped float64
+ *      depth (depth_is_raw = 0, the reference's argument) or the raw float32
+ *      render depth (depth_is_raw = 1: logistic_remap, medium.py:26-29, is
+ *      applied inside, as pipeline.py:205 does before the call).
+ *      Resize to min(resized_height, h) rows (bilinear colour, nearest depth),
+ *      per depth cluster the ceil(p_dark*size) darkest pixels (stable), the
+ *      per-interval per-channel minima, and a box-constrained multi-start
+ *      Levenberg-Marquardt fit of v(z) = b_inf (1 - exp(-b_b z)) per channel.
+ *      result[12] (device float64): water_color_est[3], backscatter_est[3],
+ *      residual[3], degenerate (0/1), number of dark pixels, error (1: cluster
+ *      edges not strictly increasing, the reference's DataError).
+ *      medium_guide (optional, device float32[6] = medium slots 9..14): set to
+ *      the float32 estimate when it is not degenerate (pipeline.py:206-208).
+ *      dark (optional, device float64 [4 * pixels]): the dark set as
+ *      (z, r, g, b) rows in raster order.  edges_num and intervals_num <= 257. */
+typedef struct uws_backscatter_cfg {
+    double p_dark;          /* 0.01 */
+    int32_t intervals_num;  /* 25 */
+    int32_t resized_height; /* 300 */
+    int32_t edges_num;      /* 10 */
+    int32_t pad;
+} uws_backscatter_cfg;
+
+int uws_backscatter_workspace_size(int32_t h, int32_t w, const uws_backscatter_cfg* cfg,
+                                   size_t* bytes);
+int uws_estimate_backscatter(const float* image, const void* depth, int32_t depth_is_raw,
+                             int32_t h, int32_t w, const uws_backscatter_cfg* cfg,
+                             double* result, float* medium_guide, double* dark,
+                             void* workspace, size_t workspace_bytes, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

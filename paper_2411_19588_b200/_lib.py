@@ -51,6 +51,11 @@ class AdamParamsC(ctypes.Structure):
                 ("one_minus_beta2", c_double), ("eps", c_double)]
 
 
+class BackscatterCfgC(ctypes.Structure):
+    _fields_ = [("p_dark", c_double), ("intervals_num", c_int32), ("resized_height", c_int32),
+                ("edges_num", c_int32), ("pad", c_int32)]
+
+
 _SIGS = {
     "uws_version": (c_char_p, []),
     "uws_last_error": (c_char_p, []),
@@ -95,6 +100,12 @@ _SIGS = {
                                   c_void_p, c_double, c_int64, c_int64, c_int64, c_void_p,
                                   c_void_p, c_void_p, c_void_p]),
     "uws_reset_opacities": (c_int, [c_void_p, c_void_p, c_void_p, c_int64, c_float, c_void_p]),
+    "uws_backscatter_workspace_size": (c_int, [c_int32, c_int32, POINTER(BackscatterCfgC),
+                                               POINTER(c_size_t)]),
+    "uws_estimate_backscatter": (c_int, [c_void_p, c_void_p, c_int32, c_int32, c_int32,
+                                         POINTER(BackscatterCfgC),
+                                         c_void_p, c_void_p, c_void_p, c_void_p, c_size_t,
+                                         c_void_p]),
 }
 
 EXPORTED = tuple(_SIGS)

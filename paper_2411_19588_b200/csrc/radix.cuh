@@ -77,7 +77,7 @@ __global__ void __launch_bounds__(kThreads) k_histogram(const K* __restrict__ ke
 }
 
 // exclusive scan of each pass's 256-bin histogram, in place (one block per pass)
-__global__ void __launch_bounds__(kBins) k_scan_hist(uint32_t* hist, int passes) {
+static __global__ void __launch_bounds__(kBins) k_scan_hist(uint32_t* hist, int passes) {
     __shared__ uint32_t tmp[kBins / 32 + 1];
     const int p = blockIdx.x;
     uint32_t v = hist[p * kBins + threadIdx.x];

@@ -322,6 +322,18 @@ class StepEngine:
         slot, self._pending = self._pending, None
         return self._finalize(slot) if slot is not None else None
 
+    def refresh_guidance(self, gt, **kw):
+        """Guidance refresh of the training loop (pipeline.py:204-208): the
+        dark-pixel estimate from the last step's last view -- its ground truth
+        ``gt`` and the engine's render depth of that view -- becomes the
+        medium's guidance unless degenerate.  Call after step() / flush()."""
+        from .backscatter import refresh_guidance
+        if self._pending is not None:
+            raise RuntimeError("refresh_guidance reads the last step's render: call flush() first")
+        if not isinstance(gt, torch.Tensor):
+            gt = torch.from_numpy(np.ascontiguousarray(gt, dtype=np.float32))
+        return refresh_guidance(self.state.medium, gt, self.out.depth, **kw)
+
     def step(self, views: Sequence) -> EngineStats:
         """One optimizer step over this rank's views, synchronously.
 

@@ -237,6 +237,11 @@ class MediumParams:
     def has_guidance(self) -> bool:
         return self._has_wg and self._has_bg
 
+    def mark_guidance(self):
+        """Slots 9..14 were written on the device (guidance refresh): make them
+        the active guidance anchors."""
+        self._has_wg = self._has_bg = True
+
     def clamp_(self):
         """Project into the boxes (scene.py:207-211); fused into Adam on the hot path."""
         self._flat[0:3].clamp_(min=0.0)

@@ -146,3 +146,23 @@ class ViewShardedTrainer:
 
     def flush(self):
         return self.engine.flush()
+
+    def refresh_guidance(self, gt, **kw):
+        """pipeline.py:204-208 for the replicated medium: rank 0 estimates from
+        its last view (``gt`` = that view's ground truth) and every rank adopts
+        the same float32 anchors (one 7-float broadcast), so the replicas stay
+        identical.  Returns rank 0's estimate (None on the other ranks)."""
+        eng = self.engine
+        med = self.state.medium
+        est = eng.refresh_guidance(gt, **kw) if self.rank == 0 else None
+        if eng.dist is not None and self.world > 1:
+            msg = torch.zeros(7, dtype=torch.float32, device=med.flat.device)
+            if self.rank == 0:
+                msg[:6] = med.flat[9:15]
+                msg[6] = 0.0 if est.degenerate else 1.0
+            src = eng.dist.get_global_rank(eng.group, 0) if eng.group is not None else 0
+            eng.dist.broadcast(msg, src=src, group=eng.group)
+            if self.rank != 0 and float(msg[6]) > 0.5:
+                med.flat[9:15].copy_(msg[:6])
+                med.mark_guidance()
+        return est

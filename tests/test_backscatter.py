@@ -62,3 +62,106 @@ def test_oracle_known_answers():
     assert O.bs_fit(np.array([0.1, 0.2]), np.array([0.2, 0.4]))[3]
     # all-zero values: the lower box corner, not degenerate
     assert O.bs_fit(z, np.zeros_like(z)) == (0.0, 0.0, 0.0, False)
+
+
+# ---------------------------------------------------------------------------
+# GPU: uws_estimate_backscatter against the reference fixtures / the oracle
+# ---------------------------------------------------------------------------
+def _fit_close(est, water, bsc, residual):
+    np.testing.assert_allclose(est.water_color_est, water, rtol=0, atol=PARAM_TOL)
+    np.testing.assert_allclose(est.backscatter_est, bsc, rtol=0, atol=PARAM_TOL)
+    np.testing.assert_allclose(est.residual, residual, rtol=1e-6, atol=1e-12)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("name", CASES)
+def test_device_estimate_matches_reference(golden, name):
+    import paper_2411_19588_b200 as uw
+
+    img, depth, kw = backscatter_inputs(name)
+    raw = BACKSCATTER_CASES[name][3] == "raw"
+    est, dz, drgb = uw.estimate_backscatter(img, depth, depth_is_raw=raw, return_dark=True, **kw)
+    dz, drgb = dz.cpu().numpy(), drgb.cpu().numpy()
+    gz, grgb = golden[f"{name}_dark_z"], golden[f"{name}_dark_rgb"]
+    assert est.n_dark == gz.size
+    # the dark-pixel set: bit-exact (the raw case remaps with CUDA's exp, numpy's
+    # SIMD exp may differ by 1 ulp: the same pixels, depths within 2 ulp of 1.0 --
+    # absolute, the remap ends in "- 1.0")
+    np.testing.assert_array_equal(drgb, grgb)
+    if raw:
+        np.testing.assert_allclose(dz, gz, rtol=0, atol=4.5e-16)
+    else:
+        np.testing.assert_array_equal(dz, gz)
+    assert est.degenerate == bool(golden[f"{name}_degenerate"])
+    _fit_close(est, golden[f"{name}_water"], golden[f"{name}_bsc"], golden[f"{name}_residual"])
+
+
+@pytest.mark.gpu
+def test_device_estimate_accepts_device_tensors_and_rejects_bad_shapes():
+    import torch
+
+    import paper_2411_19588_b200 as uw
+
+    img, depth, kw = backscatter_inputs("uw_small")
+    a = uw.estimate_backscatter(img, depth)
+    b = uw.estimate_backscatter(torch.as_tensor(img).cuda(), torch.as_tensor(depth).cuda())
+    np.testing.assert_array_equal(a.water_color_est, b.water_color_est)
+    np.testing.assert_array_equal(a.backscatter_est, b.backscatter_est)
+    with pytest.raises(uw.DataError):
+        uw.estimate_backscatter(img, depth[:-1])
+    with pytest.raises(uw.DataError):
+        uw.estimate_backscatter(img[..., :2], depth)
+
+
+@pytest.mark.gpu
+def test_refresh_guidance_writes_medium_anchors(golden):
+    import torch
+
+    import paper_2411_19588_b200 as uw
+
+    img, raw, _ = backscatter_inputs("uw_raw_depth")
+    med = uw.MediumParams((0.6, 0.45, 0.3), (0.2, 0.35, 0.5), (0.8, 1.0, 1.2))
+    assert not med.has_guidance
+    est = uw.refresh_guidance(med, torch.as_tensor(img).cuda(), torch.as_tensor(raw).cuda())
+    assert not est.degenerate and med.has_guidance
+    np.testing.assert_array_equal(med.water_color_guide.cpu().numpy(),
+                                  est.water_color_est.astype(np.float32))
+    np.testing.assert_array_equal(med.backscatter_guide.cpu().numpy(),
+                                  est.backscatter_est.astype(np.float32))
+    _fit_close(est, golden["uw_raw_depth_water"], golden["uw_raw_depth_bsc"],
+               golden["uw_raw_depth_residual"])
+    # a degenerate estimate leaves the medium untouched (pipeline.py:206)
+    flat = np.zeros((64, 80))
+    img2, _, _ = backscatter_inputs("flat_depth")
+    med2 = uw.MediumParams((0.6, 0.45, 0.3), (0.2, 0.35, 0.5), (0.8, 1.0, 1.2))
+    est2 = uw.refresh_guidance(med2, torch.as_tensor(img2).cuda(),
+                               torch.as_tensor(flat, dtype=torch.float32).cuda())
+    assert est2.degenerate and not med2.has_guidance
+
+
+@pytest.mark.gpu
+def test_engine_refresh_guidance_matches_oracle_on_render_depth():
+    """The training loop's refit (pipeline.py:204-208) through StepEngine: the
+    estimate from the last view's ground truth and render depth equals the
+    oracle's estimate on the same (gt, logistic_remap(depth)) pair."""
+    import torch
+
+    import paper_2411_19588_b200 as uw
+    from golden_util import load
+    from gpu_util import device_scene
+
+    g = load("survey2k")
+    cloud, cam, medium = device_scene(g)
+    state = uw.TrainState(cloud, medium, iteration=1)
+    eng = uw.StepEngine(state, cam.width, cam.height, uw.OptimConfig())
+    gt = torch.as_tensor(g.gt, dtype=torch.float32).cuda()
+    eng.step([(cam, gt)])
+    depth = eng.out.depth.cpu().numpy()
+    est = eng.refresh_guidance(gt)
+    ref = O.estimate_backscatter(g.gt.astype(np.float32), O.logistic(depth.astype(np.float64)))
+    assert est.degenerate == ref.degenerate
+    _fit_close(est, ref.water_color_est, ref.backscatter_est, ref.residual)
+    if not est.degenerate:
+        assert state.medium.has_guidance
+        np.testing.assert_array_equal(state.medium.backscatter_guide.cpu().numpy(),
+                                      est.backscatter_est.astype(np.float32))
