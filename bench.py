@@ -300,6 +300,22 @@ def run_gpu(args):
                             "mpix_per_s": round(rw * rh / fms / 1e3, 1)}
         if eng is not trainer.engine:
             del eng
+    # guidance refresh (pipeline.py:204-208; every refit_period = 500 steps): the
+    # dark-pixel estimate from the C3 ground truth and the engine's render depth,
+    # including the host read of the 96-byte result record (untimed for the step)
+    refresh_ms = None
+    if not args.no_render_fps:
+        depth_raw = trainer.engine.out.depth
+        for _ in range(2):
+            uw.estimate_backscatter(gt_dev, depth_raw, depth_is_raw=True)
+        barrier()
+        t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        t0.record()
+        for _ in range(5):
+            uw.estimate_backscatter(gt_dev, depth_raw, depth_is_raw=True)
+        t1.record()
+        barrier()
+        refresh_ms = round(t0.elapsed_time(t1) / 5, 4)
     torch.cuda.empty_cache()
 
     px_step = W * H * world
@@ -394,6 +410,7 @@ def run_gpu(args):
                 "d2h_bytes_per_step": 4 + 8 + 7 * 8},
         "gpu_launches": int(launches),
         "render_fps": render_fps,
+        "guidance_refresh_ms": refresh_ms,
         "roofline": roofline,
         "stages_ms": {k: round(v, 4) for k, v in per_step.items()},
         "gaps_after_stage_ms": {k: round(v / args.steps, 4) for k, v in gaps.items()},
