@@ -30,6 +30,7 @@ constexpr int kPix = 4;                          // pixels per thread
 constexpr int kThreads = kRasterThreads / kPix;  // 64
 constexpr int kWarps = kThreads / 32;            // 2
 constexpr int kBandRows = kTile / kWarps;        // each warp owns an 8-row band of the tile
+static_assert(kWarps == 2, "one x-range per warp band in Rec::D");
 // the clamp guard band as |araw - mid| < half (a slightly wider superset of [kClampLo, kClampHi))
 constexpr float kClampMid = 0.5f * (kClampLo + kClampHi);
 constexpr float kClampHalf = 0.51f * (kClampHi - kClampLo);
@@ -88,7 +89,7 @@ __global__ void __launch_bounds__(kThreads, MINB) k_raster_bwd(BwdArgs a) {
         StageA A;
         StageB B;
         StageC C;
-        float4 D;  // pre-filter box (stage_extent)
+        float4 D;  // pre-filter: x-range of the pass region in band 0 and band 1
     };
     __shared__ Rec sRec[kBatch];  // one array: one base address for all four loads
     __shared__ float sAcc[kWarps][9][kBatch + 1];  // per-warp partials; +1: the 8 storing lanes hit distinct banks
@@ -103,8 +104,6 @@ __global__ void __launch_bounds__(kThreads, MINB) k_raster_bwd(BwdArgs a) {
     const int lx = lane & (kTile - 1);
     const int ly0 = warp * kBandRows + (lane >> 4);  // pixel p sits on row ly0 + 2p
     const float fx = (float)lx + 0.5f;
-    const float band_lo = (float)(warp * kBandRows) + 0.5f;
-    const float band_hi = band_lo + (float)(kBandRows - 1);
     const int start = ROWS ? 0 : a.offsets[tile];
 
     if (threadIdx.x == 0) sMaxLast = 0;
@@ -224,7 +223,12 @@ __global__ void __launch_bounds__(kThreads, MINB) k_raster_bwd(BwdArgs a) {
                 Rec& r = sRec[i];
                 stage_entry(a.splat, ROWS ? sRow[i] : a.entries[start + lo + i], ox, oy, r.A, r.B,
                             r.C);
-                r.D = stage_extent(r.A, r.B);
+                // exact x-ranges of the pass region within each warp's band rows
+                PassRegion pr;
+                pr.init(r.A, r.B);
+                const float2 x0 = pr.xrange(0.5f, (float)kBandRows - 0.5f);
+                const float2 x1 = pr.xrange((float)kBandRows + 0.5f, (float)kTile - 0.5f);
+                r.D = make_float4(x0.x, x0.y, x1.x, x1.y);
             }
         }
         __syncthreads();
@@ -232,14 +236,15 @@ __global__ void __launch_bounds__(kThreads, MINB) k_raster_bwd(BwdArgs a) {
         for (int k = min(nb, wmax - lo) - 1; k >= 0; --k) {
             const uint32_t ra = sbase + 64u * (uint32_t)k;
             const float4 D = lds128(ra + 48u);
-            // misses this warp's band or the tile's pixel columns (uniform)
-            if (D.y < band_lo || D.x > band_hi || D.w < 0.5f || D.z > (float)kTile - 0.5f) continue;
+            const float xlo = warp ? D.z : D.x, xhi = warp ? D.w : D.y;
+            // the pass region misses this warp's band within the tile's columns (uniform)
+            if (xhi < 0.5f || xlo > (float)kTile - 0.5f) continue;
             const int jrel = lo + k;
             // A thread's kPix pixels share one column, hence dx: the dx-weighted
             // partials are formed once after the pixel loop from sum(dp) and sum(dp dy).
             float sdp = 0.f, sdpy = 0.f, sdpyy = 0.f, wg0 = 0.f, wg1 = 0.f, wg2 = 0.f, dx = 0.f;
             bool hit = false;
-            if (fx >= D.z && fx <= D.w) {  // column inside the box
+            if (fx >= xlo && fx <= xhi) {  // column inside the band's range
                 const float4 a4 = lds128(ra), b4 = lds128(ra + 16u), c4 = lds128(ra + 32u);
                 const StageA A{a4.x, a4.y, a4.z, a4.w};
                 const StageB B{b4.x, b4.y, b4.z, b4.w};

@@ -121,6 +121,61 @@ __device__ __forceinline__ float4 stage_extent(const StageA& s, const StageB& t)
     return make_float4(s.my - ey, s.my + ey, s.mx - ex, s.mx + ex);
 }
 
+// Exact x-range {xlo, xhi} (tile-local pixel-centre coordinates) of the region
+// where `power >= hi - kSkipDelta` can hold, restricted to the pixel-centre rows
+// y in [y0, y1]; empty (xlo > xhi) when the region misses those rows.  The
+// region is the ellipse q = a dx^2 + b dx dy + c dy^2 <= Q of stage_extent,
+// enlarged by 0.2% (+1e-3) so that it stays a superset of what the float32
+// per-pixel test accepts.  Its rightmost point (ex, -b ex / 2c) and leftmost
+// point (-ex, b ex / 2c) bound the range when their row lies in the strip;
+// otherwise the range ends on the strip's boundary rows (the boundary x(dy)
+// curves are concave / convex).
+struct PassRegion {
+    float mx, my, b, fourAQ, det4, ey, ex, yr, inv2a;
+    int mode;  // 0: ellipse, 1: nothing passes, 2: no pre-filter (degenerate / NaN)
+
+    __device__ __forceinline__ void init(const StageA& s, const StageB& t) {
+        const float a = -s.A, c = -t.C;
+        b = -s.B;
+        mx = s.mx;
+        my = s.my;
+        const float Q = fmaf(-(t.hi - kSkipDelta), 1.002f, 1e-3f);
+        det4 = 4.f * a * c - b * b;
+        mode = 0;
+        if (!(t.hi - kSkipDelta <= 0.f)) mode = 1;
+        else if (!(det4 > 0.f) || !(a > 0.f) || !(c > 0.f) || !(Q >= 0.f)) mode = 2;
+        fourAQ = 4.f * a * Q;
+        ey = sqrtf(fourAQ / det4);
+        ex = sqrtf(4.f * c * Q / det4);
+        yr = -b * ex / (2.f * c);  // row of the rightmost point; the leftmost is at -yr
+        inv2a = 0.5f / a;
+    }
+
+    __device__ __forceinline__ float2 xrange(float y0, float y1) const {
+        if (mode == 1) return make_float2(1e30f, -1e30f);
+        if (mode == 2) return make_float2(-1e30f, 1e30f);
+        const float lo = fmaxf(y0 - my, -ey), hi = fminf(y1 - my, ey);
+        if (lo > hi) return make_float2(1e30f, -1e30f);
+        // boundary abscissae at the two (clipped) strip rows
+        const float dl = sqrtf(fmaxf(fourAQ - det4 * lo * lo, 0.f));
+        const float dh = sqrtf(fmaxf(fourAQ - det4 * hi * hi, 0.f));
+        const float xmax = (yr >= lo && yr <= hi)
+                               ? ex
+                               : fmaxf((-b * lo + dl) * inv2a, (-b * hi + dh) * inv2a);
+        const float xmin = (-yr >= lo && -yr <= hi)
+                               ? -ex
+                               : fminf((-b * lo - dl) * inv2a, (-b * hi - dh) * inv2a);
+        return make_float2(mx + xmin - fmaf(1e-3f, fabsf(xmin), 0.01f),
+                           mx + xmax + fmaf(1e-3f, fabsf(xmax), 0.01f));
+    }
+};
+
+__device__ __forceinline__ float2 band_xrange(const StageA& s, const StageB& t, float y0, float y1) {
+    PassRegion r;
+    r.init(s, t);
+    return r.xrange(y0, y1);
+}
+
 // Stage entry `row` of a tile whose origin is (ox, oy).
 __device__ __forceinline__ void stage_entry(const uws_splat* __restrict__ splat, int row, int ox,
                                             int oy, StageA& a, StageB& b, StageC& c) {

@@ -136,10 +136,17 @@ __global__ void __launch_bounds__(kRasterThreads / PX, 4 * PX) k_raster_fwd(FwdA
                 sRec[3 * i + 0] = make_float4(sa.mx, sa.my, sa.A, sa.B);
                 sRec[3 * i + 1] = make_float4(sb.C, sb.op, sb.hi, sb.depth);
                 sRec[3 * i + 2] = make_float4(sc.r, sc.g, sc.b, __int_as_float(sc.row));
-                const float4 box = stage_extent(sa, sb);
-                // bands the box reaches; none if it misses the tile's pixel columns
-                const bool xin = box.z <= (float)kTile - 0.5f && box.w >= 0.5f;
-                sMask[i] = xin ? (unsigned char)band_mask<kBandRows, kWarps>(box.x, box.y) : 0u;
+                // bands whose rows the pass region reaches within the tile's columns
+                PassRegion pr;
+                pr.init(sa, sb);
+                unsigned msk = 0u;
+#pragma unroll
+                for (int bnd = 0; bnd < kWarps; ++bnd) {
+                    const float2 xr = pr.xrange((float)(bnd * kBandRows) + 0.5f,
+                                                (float)(bnd * kBandRows + kBandRows) - 0.5f);
+                    if (xr.y >= 0.5f && xr.x <= (float)kTile - 0.5f) msk |= 1u << bnd;
+                }
+                sMask[i] = (unsigned char)msk;
             }
         }
         __syncthreads();
