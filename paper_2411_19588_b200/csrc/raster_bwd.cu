@@ -78,11 +78,10 @@ __device__ __forceinline__ float butterfly8(const float v[8], int lane) {
     return r;
 }
 
-constexpr int kMaxMarks = 128;  // recorded batch starts per tile (row-list source)
+constexpr int kMaxMarks = 64;   // recorded batch starts per tile (row-list source)
 
 template <bool ROWS, int MINB>
 __global__ void __launch_bounds__(kThreads, MINB) k_raster_bwd(BwdArgs a) {
-    __shared__ int sRow[ROWS ? kBatch : 1];  // (filter writes only positions < nb <= kBatch)
     __shared__ int sMarkCur[ROWS ? kMaxMarks : 1], sMarkSkip[ROWS ? kMaxMarks : 1];
     __shared__ int sScan[kWarps];
     struct __align__(16) Rec {
@@ -93,7 +92,11 @@ __global__ void __launch_bounds__(kThreads, MINB) k_raster_bwd(BwdArgs a) {
     };
     __shared__ Rec sRec[kBatch];  // one array: one base address for all four loads
     __shared__ float sAcc[kWarps][9][kBatch + 1];  // per-warp partials; +1: the 8 storing lanes hit distinct banks
-    __shared__ int sHit[kWarps][kBatch];           // sAcc[w][.][k] valid
+    // the batch's rows (filled and consumed by the staging phase) share sAcc's storage: sAcc is
+    // written only by the walk that follows and read back before the next batch is staged
+    int* const sRow = reinterpret_cast<int*>(&sAcc[0][0][0]);  // (filter writes positions < nb <= kBatch)
+    static_assert(kWarps * 9 * (kBatch + 1) >= kBatch, "sRow alias");
+    __shared__ unsigned char sHit[kWarps][kBatch];  // sAcc[w][.][k] valid
     __shared__ float sMed[kWarps][9];
     __shared__ int sMaxLast;
 
