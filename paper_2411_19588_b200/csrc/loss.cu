@@ -28,6 +28,27 @@ constexpr int kMaxC = 4;             // channels staged at once by the moments p
 constexpr double kC1 = 0.01 * 0.01, kC2 = 0.03 * 0.03;
 
 __constant__ float c_taps[kN];
+__constant__ float2 c_taps2[kN];  // (w, w): the tap for both lanes of an FFMA2
+
+// c + a * b on two float lanes with one FFMA2 (sm_100): per lane the same
+// IEEE fma as fmaf, so results are bitwise those of two FFMAs
+__device__ __forceinline__ float2 fma2(float2 a, float2 b, float2 c) {
+    unsigned long long d;
+    asm("fma.rn.f32x2 %0, %1, %2, %3;"
+        : "=l"(d)
+        : "l"(*reinterpret_cast<unsigned long long*>(&a)),
+          "l"(*reinterpret_cast<unsigned long long*>(&b)),
+          "l"(*reinterpret_cast<unsigned long long*>(&c)));
+    return *reinterpret_cast<float2*>(&d);
+}
+__device__ __forceinline__ float2 mul2(float2 a, float2 b) {
+    unsigned long long d;
+    asm("mul.rn.f32x2 %0, %1, %2;"
+        : "=l"(d)
+        : "l"(*reinterpret_cast<unsigned long long*>(&a)),
+          "l"(*reinterpret_cast<unsigned long long*>(&b)));
+    return *reinterpret_cast<float2*>(&d);
+}
 
 // 4-byte asynchronous global -> shared copy; ok = false writes a zero
 __device__ __forceinline__ void cp_async4(float* sdst, const float* gsrc, bool ok) {
@@ -111,55 +132,65 @@ __global__ void __launch_bounds__(kThreads, 3) k_ssim_moments(const float* __res
         // horizontal: item = (row, group of 8 columns)
         for (int it = threadIdx.x; it < kP * (kT / kHR); it += kThreads) {
             const int r = it >> 2, c0 = (it & 3) * kHR;
-            float m[5][kHR];
+            // (mu_a, mu_b) and (E[a^2], E[b^2]) accumulate in FFMA2 pairs
+            float2 m01[kHR], m23[kHR];
+            float m4[kHR];
 #pragma unroll
-            for (int v = 0; v < 5; ++v)
-#pragma unroll
-                for (int j = 0; j < kHR; ++j) m[v][j] = 0.f;
+            for (int j = 0; j < kHR; ++j) {
+                m01[j] = m23[j] = make_float2(0.f, 0.f);
+                m4[j] = 0.f;
+            }
             const float* pa = sa + r * pitch + c0 * C + ch;
             const float* pb = sb + r * pitch + c0 * C + ch;
 #pragma unroll
             for (int q = 0; q < kHR + kN - 1; ++q) {
-                const float xa = pa[q * C], xb = pb[q * C];
-                const float aa = xa * xa, bb = xb * xb, ab = xa * xb;
+                const float2 x01 = make_float2(pa[q * C], pb[q * C]);
+                const float2 x23 = mul2(x01, x01);
+                const float ab = x01.x * x01.y;
 #pragma unroll
                 for (int j = 0; j < kHR; ++j) {
                     const int t = q - j;
                     if (t < 0 || t >= kN) continue;
-                    const float w = c_taps[t];
-                    m[0][j] = fmaf(w, xa, m[0][j]);
-                    m[1][j] = fmaf(w, xb, m[1][j]);
-                    m[2][j] = fmaf(w, aa, m[2][j]);
-                    m[3][j] = fmaf(w, bb, m[3][j]);
-                    m[4][j] = fmaf(w, ab, m[4][j]);
+                    const float2 w2 = c_taps2[t];
+                    m01[j] = fma2(w2, x01, m01[j]);
+                    m23[j] = fma2(w2, x23, m23[j]);
+                    m4[j] = fmaf(c_taps[t], ab, m4[j]);
                 }
             }
 #pragma unroll
-            for (int v = 0; v < 5; ++v)
-#pragma unroll
-                for (int j = 0; j < kHR; ++j) hs[(v * kP + r) * (kT + 1) + c0 + j] = m[v][j];
+            for (int j = 0; j < kHR; ++j) {
+                hs[(0 * kP + r) * (kT + 1) + c0 + j] = m01[j].x;
+                hs[(1 * kP + r) * (kT + 1) + c0 + j] = m01[j].y;
+                hs[(2 * kP + r) * (kT + 1) + c0 + j] = m23[j].x;
+                hs[(3 * kP + r) * (kT + 1) + c0 + j] = m23[j].y;
+                hs[(4 * kP + r) * (kT + 1) + c0 + j] = m4[j];
+            }
         }
         __syncthreads();
         // vertical: item = (column, group of 4 rows)
         {
             const int c = threadIdx.x & (kT - 1), r0 = (threadIdx.x >> 5) * kVR;
-            float u[5][kVR];
+            float2 u01[kVR], u23[kVR];
+            float u4[kVR];
 #pragma unroll
-            for (int v = 0; v < 5; ++v)
-#pragma unroll
-                for (int j = 0; j < kVR; ++j) u[v][j] = 0.f;
+            for (int j = 0; j < kVR; ++j) {
+                u01[j] = u23[j] = make_float2(0.f, 0.f);
+                u4[j] = 0.f;
+            }
 #pragma unroll
             for (int q = 0; q < kVR + kN - 1; ++q) {
-                float h[5];
-#pragma unroll
-                for (int v = 0; v < 5; ++v) h[v] = hs[(v * kP + r0 + q) * (kT + 1) + c];
+                const float* hq = hs + (r0 + q) * (kT + 1) + c;
+                const float2 h01 = make_float2(hq[0 * kP * (kT + 1)], hq[1 * kP * (kT + 1)]);
+                const float2 h23 = make_float2(hq[2 * kP * (kT + 1)], hq[3 * kP * (kT + 1)]);
+                const float h4 = hq[4 * kP * (kT + 1)];
 #pragma unroll
                 for (int j = 0; j < kVR; ++j) {
                     const int t = q - j;
                     if (t < 0 || t >= kN) continue;
-                    const float w = c_taps[t];
-#pragma unroll
-                    for (int v = 0; v < 5; ++v) u[v][j] = fmaf(w, h[v], u[v][j]);
+                    const float2 w2 = c_taps2[t];
+                    u01[j] = fma2(w2, h01, u01[j]);
+                    u23[j] = fma2(w2, h23, u23[j]);
+                    u4[j] = fmaf(c_taps[t], h4, u4[j]);
                 }
             }
             const int ox = x0 + c;
@@ -167,7 +198,7 @@ __global__ void __launch_bounds__(kThreads, 3) k_ssim_moments(const float* __res
             for (int j = 0; j < kVR; ++j) {
                 const int oy = y0 + r0 + j;
                 if (oy >= VH || ox >= VW) continue;
-                const float u1 = u[0][j], u2 = u[1][j], v1 = u[2][j], v2 = u[3][j], v12 = u[4][j];
+                const float u1 = u01[j].x, u2 = u01[j].y, v1 = u23[j].x, v2 = u23[j].y, v12 = u4[j];
                 const float A1 = 2.0f * u1 * u2 + (float)kC1;
                 const float A2 = 2.0f * (v12 - u1 * u2) + (float)kC2;
                 const float B1 = u1 * u1 + u2 * u2 + (float)kC1;
@@ -237,29 +268,31 @@ __global__ void __launch_bounds__(kThreads, 3) k_ssim_grad(const float* __restri
         float (*sm)[kP][kP + 1] = sbuf[ch & 1];
         for (int it = threadIdx.x; it < kP * (kT / kHR); it += kThreads) {
             const int r = it >> 2, c0 = (it & 3) * kHR;
-            float g[3][kHR];
+            float2 g01[kHR];
+            float g2[kHR];
 #pragma unroll
-            for (int m = 0; m < 3; ++m)
-#pragma unroll
-                for (int j = 0; j < kHR; ++j) g[m][j] = 0.f;
+            for (int j = 0; j < kHR; ++j) {
+                g01[j] = make_float2(0.f, 0.f);
+                g2[j] = 0.f;
+            }
 #pragma unroll
             for (int q = 0; q < kHR + kN - 1; ++q) {
-                float x[3];
-#pragma unroll
-                for (int m = 0; m < 3; ++m) x[m] = sm[m][r][c0 + q];
+                const float2 x01 = make_float2(sm[0][r][c0 + q], sm[1][r][c0 + q]);
+                const float x2 = sm[2][r][c0 + q];
 #pragma unroll
                 for (int j = 0; j < kHR; ++j) {
                     const int t = q - j;
                     if (t < 0 || t >= kN) continue;
-                    const float w = c_taps[t];
-#pragma unroll
-                    for (int m = 0; m < 3; ++m) g[m][j] = fmaf(w, x[m], g[m][j]);
+                    g01[j] = fma2(c_taps2[t], x01, g01[j]);
+                    g2[j] = fmaf(c_taps[t], x2, g2[j]);
                 }
             }
 #pragma unroll
-            for (int m = 0; m < 3; ++m)
-#pragma unroll
-                for (int j = 0; j < kHR; ++j) hs[m][r][c0 + j] = g[m][j];
+            for (int j = 0; j < kHR; ++j) {
+                hs[0][r][c0 + j] = g01[j].x;
+                hs[1][r][c0 + j] = g01[j].y;
+                hs[2][r][c0 + j] = g2[j];
+            }
         }
         __syncthreads();
         {
@@ -274,23 +307,23 @@ __global__ void __launch_bounds__(kThreads, 3) k_ssim_grad(const float* __restri
                 pa[j] = ok ? __ldg(img_a + o) : 0.f;
                 pb[j] = ok ? __ldg(img_b + o) : 0.f;
             }
-            float g[3][kVR];
+            float2 g01[kVR];
+            float g2[kVR];
 #pragma unroll
-            for (int m = 0; m < 3; ++m)
-#pragma unroll
-                for (int j = 0; j < kVR; ++j) g[m][j] = 0.f;
+            for (int j = 0; j < kVR; ++j) {
+                g01[j] = make_float2(0.f, 0.f);
+                g2[j] = 0.f;
+            }
 #pragma unroll
             for (int q = 0; q < kVR + kN - 1; ++q) {
-                float h[3];
-#pragma unroll
-                for (int m = 0; m < 3; ++m) h[m] = hs[m][r0 + q][c];
+                const float2 h01 = make_float2(hs[0][r0 + q][c], hs[1][r0 + q][c]);
+                const float h2 = hs[2][r0 + q][c];
 #pragma unroll
                 for (int j = 0; j < kVR; ++j) {
                     const int t = q - j;
                     if (t < 0 || t >= kN) continue;
-                    const float w = c_taps[t];
-#pragma unroll
-                    for (int m = 0; m < 3; ++m) g[m][j] = fmaf(w, h[m], g[m][j]);
+                    g01[j] = fma2(c_taps2[t], h01, g01[j]);
+                    g2[j] = fmaf(c_taps[t], h2, g2[j]);
                 }
             }
 #pragma unroll
@@ -302,7 +335,7 @@ __global__ void __launch_bounds__(kThreads, 3) k_ssim_grad(const float* __restri
                 const float d = a - b;
                 const float sg = (d > 0.f) ? 1.f : ((d < 0.f) ? -1.f : 0.f);
                 l1sum += fabsf(d);
-                grad[o] = k_ssim * (g[0][j] + 2.0f * a * g[1][j] + b * g[2][j]) + k_l1 * sg;
+                grad[o] = k_ssim * (g01[j].x + 2.0f * a * g01[j].y + b * g2[j]) + k_l1 * sg;
             }
         }
         __syncthreads();  // sm / hs reuse by the next channel
@@ -365,6 +398,9 @@ int ensure_taps() {
     float f[kN];
     for (int i = 0; i < kN; ++i) f[i] = (float)(k[i] / s);
     UWS_CUDA(cudaMemcpyToSymbol(c_taps, f, sizeof(f)));
+    float2 f2[kN];
+    for (int i = 0; i < kN; ++i) f2[i] = make_float2(f[i], f[i]);
+    UWS_CUDA(cudaMemcpyToSymbol(c_taps2, f2, sizeof(f2)));
     g_taps_ready = true;
     return UWS_OK;
 }
