@@ -579,9 +579,8 @@ struct Plan {
     uint64_t *key, *key_sorted;
     uint32_t *idx_sorted, *lab, *lab_g, *lab_sorted, *idx_final, *pick;
     // radix temporaries (64-bit sums: 8 passes; cluster labels: 1 pass)
-    uint64_t *k64_alt, *k64_tmp;
-    uint32_t *v64_alt, *v64_tmp, *h64, *s64, *t64;
-    uint32_t *k32_alt, *k32_tmp, *v32_alt, *v32_tmp, *h32, *s32, *t32;
+    radix::Plan<uint64_t> r64;
+    radix::Plan<uint32_t> r32;
 };
 
 inline void dims(int h, int w, int rh, int* th, int* tw) {
@@ -611,10 +610,8 @@ inline void plan(Workspace& ws, int h, int w, int rh, Plan& p) {
     p.lab_sorted = ws.take<uint32_t>(n);
     p.idx_final = ws.take<uint32_t>(n);
     p.pick = ws.take<uint32_t>(n);
-    radix::plan<uint64_t>(ws, n, 8, &p.k64_alt, &p.v64_alt, &p.k64_tmp, &p.v64_tmp, &p.h64,
-                                    &p.s64, &p.t64);
-    radix::plan<uint32_t>(ws, n, 1, &p.k32_alt, &p.v32_alt, &p.k32_tmp, &p.v32_tmp, &p.h32, &p.s32,
-                          &p.t32);
+    radix::plan<uint64_t>(ws, n, 8, p.r64);
+    radix::plan<uint32_t>(ws, n, 1, p.r32);
 }
 
 }  // namespace bsc
@@ -673,16 +670,12 @@ extern "C" int uws_estimate_backscatter(const float* image, const void* depth, i
     k_bs_label<<<blocks, kThreads, 0, st>>>(p.z, P, cfg->edges_num, p.hdr, p.lab);
     UWS_CHECK_LAUNCH("k_bs_label");
     // stable by RGB sum (pixel order on ties), then stable by cluster
-    const size_t meta64 = (char*)(p.t64 + 8) - (char*)p.h64;
-    UWS_CUDA(radix::sort_pairs<uint64_t>(p.key, nullptr, p.key_sorted, p.idx_sorted, P,
-                                                   nullptr, 0, 8, p.k64_tmp, p.v64_tmp, p.h64,
-                                                   p.s64, p.t64, meta64, st));
+    UWS_CUDA(radix::sort_pairs<uint64_t>(p.r64, p.key, nullptr, p.key_sorted, p.idx_sorted, P,
+                                         nullptr, 0, st));
     k_bs_gather<<<blocks, kThreads, 0, st>>>(p.lab, p.idx_sorted, P, p.lab_g);
     UWS_CHECK_LAUNCH("k_bs_gather");
-    const size_t meta32 = (char*)(p.t32 + 1) - (char*)p.h32;
-    UWS_CUDA(radix::sort_pairs<uint32_t>(p.lab_g, p.idx_sorted, p.lab_sorted, p.idx_final, P,
-                                         nullptr, 0, 1, p.k32_tmp, p.v32_tmp, p.h32, p.s32, p.t32,
-                                         meta32, st));
+    UWS_CUDA(radix::sort_pairs<uint32_t>(p.r32, p.lab_g, p.idx_sorted, p.lab_sorted, p.idx_final, P,
+                                         nullptr, 0, st));
     k_bs_pick<<<blocks, kThreads, 0, st>>>(p.lab_sorted, p.idx_final, P, p.hdr, cfg->p_dark, p.pick);
     UWS_CHECK_LAUNCH("k_bs_pick");
     k_bs_compact<<<1, 1024, 0, st>>>(p.pick, p.z, p.rgb, P, p.dz, p.drgb, dark, p.hdr);

@@ -565,8 +565,7 @@ struct CountPlan {
     uint32_t* m_band;             // [nbands][nblk_r] counts, scanned in place
     unsigned long long* rstat;    // look-back status of the band scan (row-list path)
     unsigned* rticket;
-    uint32_t *k_alt, *k_tmp;
-    uint32_t *v_alt, *v_tmp, *hist, *rstatus, *rtickets;
+    radix::Plan<uint32_t> rs;
     uint32_t nblk_r;
 };
 
@@ -584,8 +583,7 @@ void plan_count(Workspace& ws, uint32_t k, int nbands, CountPlan& p) {
     p.m_band = ws.take<uint32_t>((size_t)nbands * p.nblk_r);
     p.rstat = ws.take<unsigned long long>(ceil_div((size_t)nbands * p.nblk_r, kThreads * kScanIpt));
     p.rticket = ws.take<unsigned>(1);
-    radix::plan<uint32_t>(ws, kk, kDepthPasses, &p.k_alt, &p.v_alt, &p.k_tmp, &p.v_tmp, &p.hist,
-                          &p.rstatus, &p.rtickets);
+    radix::plan<uint32_t>(ws, kk, kDepthPasses, p.rs);
 }
 
 struct EmitPlan {
@@ -661,13 +659,12 @@ extern "C" int uws_bin_count(const uws_projected* proj, int64_t k_cap, const uws
     // 0. stable order of the rows by (float64 depth bits, row): radix sort of the
     //    high words (4 passes), then the runs of equal high words by the low word
     const uint64_t* dbits = (const uint64_t*)proj->depth;
+    UWS_CUDA(cudaMemsetAsync(p.rs.hist, 0, p.rs.meta_bytes, st));
     depth_sort::k_depth_hi<<<(unsigned)ceil_div(kc, 256), 256, 0, st>>>(dbits, k_dev, kc, p.keys_hi,
-                                                                       p.long_cnt);
+                                                                       p.long_cnt, p.rs.neg_min);
     UWS_CHECK_LAUNCH("k_depth_hi");
-    size_t meta = (char*)(p.rtickets + kDepthPasses) - (char*)p.hist;
-    UWS_CUDA(radix::sort_pairs<uint32_t>(p.keys_hi, nullptr, p.keys_hi_sorted, p.sorted_rows, kc,
-                                         k_dev, 0, kDepthPasses, p.k_tmp, p.v_tmp, p.hist,
-                                         p.rstatus, p.rtickets, meta, st));
+    UWS_CUDA(radix::sort_pairs<uint32_t>(p.rs, p.keys_hi, nullptr, p.keys_hi_sorted, p.sorted_rows,
+                                         kc, k_dev, 0, st, /*meta_zeroed=*/true, /*relative=*/true));
     depth_sort::k_tie_fix<<<(unsigned)ceil_div(kc, 256), 256, 0, st>>>(
         p.keys_hi_sorted, p.sorted_rows, dbits, k_dev, kc, p.long_cnt, p.long_list);
     UWS_CHECK_LAUNCH("k_tie_fix");
@@ -675,7 +672,7 @@ extern "C" int uws_bin_count(const uws_projected* proj, int64_t k_cap, const uws
                                                     kc, p.long_cnt, p.long_list, p.huge_list);
     UWS_CHECK_LAUNCH("k_tie_fix_warp");
     depth_sort::k_tie_fix_long<<<32, depth_sort::kLongThreads, 0, st>>>(
-        p.keys_hi_sorted, p.sorted_rows, dbits, k_dev, kc, p.long_cnt, p.huge_list, p.v_tmp);
+        p.keys_hi_sorted, p.sorted_rows, dbits, k_dev, kc, p.long_cnt, p.huge_list, p.rs.v_tmp);
     UWS_CHECK_LAUNCH("k_tie_fix_long");
     // 1a. per-block band histograms + totals (E entries, S band items)
     k_band_count<<<p.nblk_r, kThreads, 0, st>>>(p.sorted_rows, (const short4*)proj->rect,

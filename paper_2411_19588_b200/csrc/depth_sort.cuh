@@ -4,7 +4,8 @@
 // the depth-major part is a stable sort of the rows by their float64 depth.
 // Positive doubles order like their bit patterns, so the full key is 64 bits
 // (8 radix passes).  Here the rows are radix-sorted by the HIGH 32 bits only
-// (sign, exponent, 20 mantissa bits: 4 passes) and the rare runs of equal
+// (sign, exponent, 20 mantissa bits: 4 passes, fewer after the
+// trivial top digits of the keys made relative to their minimum are skipped) and the rare runs of equal
 // high words -- depths within ~1e-6 relative of each other -- are then put in
 // (low word, row) order:
 //   * runs of <= kShortRun rows: one thread, odd-even transposition network in
@@ -27,13 +28,30 @@ constexpr int kShortRun = 8;
 constexpr int kWarpRun = 32;
 constexpr int kLongThreads = 256;
 
-// high 32 bits of the depth's bit pattern; zeroes the run counters
-__global__ void k_depth_hi(const uint64_t* __restrict__ depth_bits, const uint32_t* __restrict__ n_dev,
-                           uint32_t n_cap, uint32_t* __restrict__ keys, uint32_t* long_cnt) {
+// High 32 bits of the depth's bit pattern, and their minimum as ~min into the
+// (zeroed) neg_min word: the radix sort makes the keys relative to it, so the
+// top digit of one scene's depths (a few exponent steps) is trivial and skipped.
+// Zeroes the run counters.
+__global__ void __launch_bounds__(256) k_depth_hi(const uint64_t* __restrict__ depth_bits,
+                                                  const uint32_t* __restrict__ n_dev, uint32_t n_cap,
+                                                  uint32_t* __restrict__ keys, uint32_t* long_cnt,
+                                                  uint32_t* neg_min) {
+    __shared__ uint32_t s_min[8];
     const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
     if (i < 2) long_cnt[i] = 0;  // [0] runs > kShortRun, [1] runs > kWarpRun
     const uint32_t n = min(*n_dev, n_cap);
-    if (i < n) keys[i] = (uint32_t)(depth_bits[i] >> 32);
+    uint32_t k = 0xffffffffu;
+    if (i < n) {
+        k = (uint32_t)(depth_bits[i] >> 32);
+        keys[i] = k;
+    }
+    k = __reduce_min_sync(0xffffffffu, k);
+    if ((threadIdx.x & 31) == 0) s_min[threadIdx.x >> 5] = k;
+    __syncthreads();
+    if (threadIdx.x < 32) {  // one atomic per block
+        k = __reduce_min_sync(0xffffffffu, threadIdx.x < 8 ? s_min[threadIdx.x] : 0xffffffffu);
+        if (threadIdx.x == 0 && k != 0xffffffffu) atomicMax(neg_min, ~k);
+    }
 }
 
 // one thread per sorted position; run starts fix their run

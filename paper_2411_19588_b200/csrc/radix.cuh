@@ -5,6 +5,13 @@
 // order), resolves its global per-digit base by decoupled look-back over the
 // preceding tiles, reorders in shared memory and writes digit runs coalesced.
 // Every key is read once and written once per pass.
+//
+// Passes whose digit is the same for every key are identity permutations; the
+// histogram shows them before any pass runs, so their kernels exit at once and
+// the remaining passes pick their ping-pong buffers from the per-pass flags so
+// that the last executed pass still lands in the output.  Optionally the keys
+// are first made relative to their minimum (a producer-maintained ~min word),
+// which turns the high digits of clustered keys (depths of one scene) trivial.
 #pragma once
 
 #include "scan.cuh"
@@ -43,20 +50,27 @@ __device__ __forceinline__ uint32_t dev_count(const uint32_t* n_dev, uint32_t n_
     return n < n_cap ? n : n_cap;
 }
 
+// keys are rewritten in place as key - min when neg_min (holding ~min) is given
 template <typename K>
-__global__ void __launch_bounds__(kThreads) k_histogram(const K* __restrict__ keys, uint32_t n_cap,
+__global__ void __launch_bounds__(kThreads) k_histogram(K* __restrict__ keys, uint32_t n_cap,
                                                        const uint32_t* n_dev, int begin_bit,
-                                                       int passes, uint32_t* __restrict__ hist) {
+                                                       int passes, uint32_t* __restrict__ hist,
+                                                       const K* __restrict__ neg_min) {
     __shared__ uint32_t h[8 * kBins];
     for (int i = threadIdx.x; i < passes * kBins; i += kThreads) h[i] = 0;
     __syncthreads();
     const uint32_t n = dev_count(n_dev, n_cap);
     const unsigned lt = lanemask_lt();
     const uint32_t stride = gridDim.x * kThreads;
+    const K kmin = neg_min ? K(~*neg_min) : K(0);
     for (uint32_t base = blockIdx.x * kThreads; base < n; base += stride) {
         uint32_t i = base + threadIdx.x;
         bool valid = i < n;
         K key = valid ? keys[i] : K(0);
+        if (neg_min && valid) {
+            key -= kmin;
+            keys[i] = key;
+        }
         const unsigned vmask = __ballot_sync(0xffffffffu, valid);
         if (vmask == 0) continue;  // whole warp past the end (lane 0 would index bin 256)
         for (int p = 0; p < passes; ++p) {
@@ -76,26 +90,64 @@ __global__ void __launch_bounds__(kThreads) k_histogram(const K* __restrict__ ke
         if (h[i]) atomicAdd(&hist[i], h[i]);
 }
 
-// exclusive scan of each pass's 256-bin histogram, in place (one block per pass)
-static __global__ void __launch_bounds__(kBins) k_scan_hist(uint32_t* hist, int passes) {
+// exclusive scan of each pass's 256-bin histogram, in place (one block per pass);
+// trivial[p] = 1 when one digit holds every key (the pass is the identity)
+static __global__ void __launch_bounds__(kBins) k_scan_hist(uint32_t* hist, int passes,
+                                                            const uint32_t* n_dev, uint32_t n_cap,
+                                                            uint32_t* trivial) {
     __shared__ uint32_t tmp[kBins / 32 + 1];
     const int p = blockIdx.x;
+    const uint32_t n = dev_count(n_dev, n_cap);
     uint32_t v = hist[p * kBins + threadIdx.x];
+    const int all = __syncthreads_or(v == n);
     uint32_t tot;
     uint32_t ex = block_exclusive_sum<kBins>(v, tmp, &tot);
     hist[p * kBins + threadIdx.x] = ex;
+    if (threadIdx.x == 0) trivial[p] = all ? 1u : 0u;
 }
 
 template <typename K>
-__global__ void __launch_bounds__(kThreads) k_onesweep(const K* __restrict__ keys_in,
-                                                      const uint32_t* __restrict__ vals_in,
-                                                      K* __restrict__ keys_out,
-                                                      uint32_t* __restrict__ vals_out, uint32_t n_cap,
+struct PassArgs {
+    const K* keys_in;          // pass input (vals_in NULL: the identity 0..n-1)
+    const uint32_t* vals_in;
+    K* keys_out;               // where the last executed pass writes
+    uint32_t* vals_out;
+    K* keys_tmp;               // the other ping-pong buffer
+    uint32_t* vals_tmp;
+    const uint32_t* trivial;   // [passes] from k_scan_hist
+    int pass, passes;
+};
+
+template <typename K>
+__global__ void __launch_bounds__(kThreads) k_onesweep(PassArgs<K> pa, uint32_t n_cap,
                                                       const uint32_t* n_dev, int shift,
                                                       const uint32_t* __restrict__ bin_base,
                                                       uint32_t* status, uint32_t* ticket) {
     constexpr int IPT = Cfg<K>::kIpt;
     constexpr int TILE = kThreads * IPT;
+    // executed passes before this one (j) and in total (m); the data after e executed
+    // passes lives in keys_out when m - e is even, else in keys_tmp
+    int j = 0, m = 0;
+    for (int q = 0; q < pa.passes; ++q) {
+        const bool run = pa.trivial[q] == 0u;
+        m += run;
+        if (q < pa.pass) j += run;
+    }
+    const uint32_t n = dev_count(n_dev, n_cap);
+    if (pa.trivial[pa.pass]) {
+        if (m == 0 && pa.pass == pa.passes - 1) {  // every pass trivial: the sort is a copy
+            for (uint32_t i = blockIdx.x * kThreads + threadIdx.x; i < n; i += gridDim.x * kThreads) {
+                pa.keys_out[i] = pa.keys_in[i];
+                pa.vals_out[i] = pa.vals_in ? pa.vals_in[i] : i;
+            }
+        }
+        return;
+    }
+    const K* __restrict__ keys_in = j == 0 ? pa.keys_in : ((m - j) % 2 == 0 ? pa.keys_out : pa.keys_tmp);
+    const uint32_t* __restrict__ vals_in =
+        j == 0 ? pa.vals_in : ((m - j) % 2 == 0 ? pa.vals_out : pa.vals_tmp);
+    K* __restrict__ keys_out = (m - j - 1) % 2 == 0 ? pa.keys_out : pa.keys_tmp;
+    uint32_t* __restrict__ vals_out = (m - j - 1) % 2 == 0 ? pa.vals_out : pa.vals_tmp;
     __shared__ K s_keys[TILE];
     __shared__ uint32_t s_vals[TILE];
     __shared__ uint32_t s_warp[kWarps][kBins];
@@ -110,7 +162,6 @@ __global__ void __launch_bounds__(kThreads) k_onesweep(const K* __restrict__ key
     __syncthreads();
     const int tile = s_tile;
     const uint32_t base = (uint32_t)tile * TILE;
-    const uint32_t n = dev_count(n_dev, n_cap);
 
     K key[IPT];
     uint32_t val[IPT];
@@ -155,6 +206,7 @@ __global__ void __launch_bounds__(kThreads) k_onesweep(const K* __restrict__ key
             st_volatile(&status[(size_t)tile * kBins + b], kStAgg | cnt);
             // look back kLook predecessors per round trip: sum aggregates up to
             // the nearest inclusive prefix, re-poll from the first unpublished one
+            // (16 and 32 measured no faster at 777k keys)
             constexpr int kLook = 8;
             int j = tile - 1;
             while (true) {
@@ -205,52 +257,62 @@ __global__ void __launch_bounds__(kThreads) k_onesweep(const K* __restrict__ key
     }
 }
 
-// Workspace for sorting n pairs over `passes` 8-bit digits.
+// Workspace for sorting n pairs over `passes` 8-bit digits.  hist .. neg_min is
+// one contiguous block ("meta", meta_bytes long) that must be zero when a sort starts.
 template <typename K>
-inline void plan(Workspace& ws, uint32_t n, int passes, K** k_alt, uint32_t** v_alt, K** k_tmp,
-                 uint32_t** v_tmp, uint32_t** hist, uint32_t** status, uint32_t** tickets) {
+struct Plan {
+    K* k_tmp;
+    uint32_t* v_tmp;
+    uint32_t *hist, *status, *tickets, *trivial;
+    K* neg_min;  // ~min of the keys, for producers that maintain it (atomicMax)
+    size_t meta_bytes;
+    int passes;
+};
+
+template <typename K>
+inline void plan(Workspace& ws, uint32_t n, int passes, Plan<K>& p) {
     int tiles = (int)ceil_div(n > 0 ? n : 1, tile_items<K>());
-    *k_alt = ws.take<K>(n);
-    *v_alt = ws.take<uint32_t>(n);
-    *k_tmp = ws.take<K>(n);
-    *v_tmp = ws.take<uint32_t>(n);
-    *hist = ws.take<uint32_t>((size_t)passes * kBins);
-    *status = ws.take<uint32_t>((size_t)passes * tiles * kBins);
-    *tickets = ws.take<uint32_t>(passes);
+    p.passes = passes;
+    p.k_tmp = ws.take<K>(n);
+    p.v_tmp = ws.take<uint32_t>(n);
+    p.hist = ws.take<uint32_t>((size_t)passes * kBins);
+    p.status = ws.take<uint32_t>((size_t)passes * tiles * kBins);
+    p.tickets = ws.take<uint32_t>(passes);
+    p.trivial = ws.take<uint32_t>(passes);
+    p.neg_min = ws.take<K>(1);
+    p.meta_bytes = (size_t)((char*)(p.neg_min + 1) - (char*)p.hist);
 }
 
 // Sort (keys_in, vals_in or identity if NULL) by bits [begin_bit, begin_bit+8*passes).
 // n_cap sizes the grids; the actual count is *n_dev when n_dev != NULL.
-// The result lands in (keys_out, vals_out); keys_in/vals_in are not modified.
-// The histogram/status/ticket block must be contiguous (as laid out by plan()).
+// The result lands in (keys_out, vals_out); vals_in is not modified, nor is keys_in
+// unless relative = true: then keys_in holds ~min in *p.neg_min (written after the
+// caller zeroed the meta block, meta_zeroed = true) and is rewritten as key - min.
 template <typename K>
-inline cudaError_t sort_pairs(const K* keys_in, const uint32_t* vals_in, K* keys_out,
+inline cudaError_t sort_pairs(const Plan<K>& p, K* keys_in, const uint32_t* vals_in, K* keys_out,
                               uint32_t* vals_out, uint32_t n_cap, const uint32_t* n_dev,
-                              int begin_bit, int passes, K* k_tmp, uint32_t* v_tmp, uint32_t* hist,
-                              uint32_t* status, uint32_t* tickets, size_t meta_bytes,
-                              cudaStream_t st) {
+                              int begin_bit, cudaStream_t st, bool meta_zeroed = false,
+                              bool relative = false) {
     if (n_cap == 0) return cudaSuccess;
-    cudaError_t e = cudaMemsetAsync(hist, 0, meta_bytes, st);
-    if (e != cudaSuccess) return e;
+    if (!meta_zeroed) {
+        cudaError_t e = cudaMemsetAsync(p.hist, 0, p.meta_bytes, st);
+        if (e != cudaSuccess) return e;
+    }
     int hist_blocks = (int)ceil_div(n_cap, kThreads * 8);
     if (hist_blocks > 1184) hist_blocks = 1184;
-    k_histogram<K><<<hist_blocks, kThreads, 0, st>>>(keys_in, n_cap, n_dev, begin_bit, passes, hist);
-    k_scan_hist<<<passes, kBins, 0, st>>>(hist, passes);
+    k_histogram<K><<<hist_blocks, kThreads, 0, st>>>(keys_in, n_cap, n_dev, begin_bit, p.passes,
+                                                     p.hist, relative ? p.neg_min : nullptr);
+    k_scan_hist<<<p.passes, kBins, 0, st>>>(p.hist, p.passes, n_dev, n_cap, p.trivial);
     const int tiles = (int)ceil_div(n_cap, tile_items<K>());
-    // ping-pong so that the last pass writes into keys_out/vals_out
-    const K* ksrc = keys_in;
-    const uint32_t* vsrc = vals_in;
-    for (int p = 0; p < passes; ++p) {
-        bool to_out = ((passes - 1 - p) % 2) == 0;
-        K* kdst = to_out ? keys_out : k_tmp;
-        uint32_t* vdst = to_out ? vals_out : v_tmp;
-        k_onesweep<K><<<tiles, kThreads, 0, st>>>(ksrc, vsrc, kdst, vdst, n_cap, n_dev,
-                                                  begin_bit + 8 * p, hist + p * kBins,
-                                                  status + (size_t)p * tiles * kBins, tickets + p);
-        ksrc = kdst;
-        vsrc = vdst;
+    PassArgs<K> pa{keys_in, vals_in, keys_out, vals_out, p.k_tmp, p.v_tmp, p.trivial, 0, p.passes};
+    for (int q = 0; q < p.passes; ++q) {
+        pa.pass = q;
+        k_onesweep<K><<<tiles, kThreads, 0, st>>>(pa, n_cap, n_dev, begin_bit + 8 * q,
+                                                  p.hist + q * kBins,
+                                                  p.status + (size_t)q * tiles * kBins,
+                                                  p.tickets + q);
     }
-    count_launches(2 + passes);
+    count_launches(2 + p.passes);
     return cudaGetLastError();
 }
 

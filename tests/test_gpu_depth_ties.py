@@ -61,3 +61,23 @@ def test_exactly_equal_depths_keep_source_order():
     cloud = _cloud(2000, 6.0, 0.0, seed=3)
     longest, _ = _check(cloud, cam)
     assert longest > 1000
+
+
+@pytest.mark.parametrize("near,far", [(0.01, 100.0), (1e-3, 1e5), (0.5, 0.75), (2.0, 3.0e8), (1.0, 1.001), (4.0, 4.0005)])
+def test_depths_across_the_whole_near_far_range(near, far):
+    # the depth keys are the high words relative to the near plane's, sorted over as many
+    # 8-bit digits as hi(far) - hi(near) needs (1 to 4): depths log-uniform over (near, far)
+    rng = np.random.default_rng(5)
+    n = 4000
+    z = np.exp(rng.uniform(np.log(near), np.log(far), n))
+    xy = rng.uniform(-0.3, 0.3, (n, 2)) * z[:, None]
+    q = rng.normal(size=(n, 4))
+    q /= np.linalg.norm(q, axis=1, keepdims=True)
+    cloud = uw.GaussianCloud(
+        positions=np.concatenate([xy, z[:, None]], axis=1).astype(np.float32),
+        log_scales=np.repeat(np.log(0.02 * z)[:, None], 3, axis=1).astype(np.float32),
+        rotations=q.astype(np.float32), sh_coeffs=rng.normal(0, 0.5, (n, 1, 3)).astype(np.float32),
+        opacity_logits=rng.uniform(-1, 2, n).astype(np.float32))
+    cam = uw.Camera(width=96, height=80, fx=90.0, fy=90.0, cx=48.0, cy=40.0,
+                    R=np.eye(3), t=np.zeros(3), near=near, far=far)
+    _check(cloud, cam)
