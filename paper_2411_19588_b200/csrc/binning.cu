@@ -78,7 +78,10 @@ __global__ void __launch_bounds__(kThreads) k_scan_u32(const uint32_t* __restric
     }
     unsigned long long tot;
     unsigned long long ex = block_exclusive_sum<kThreads, unsigned long long>(sum, s_scan, &tot);
-    if (threadIdx.x == 0) s_base = lookback_exclusive(status, tile, tot);
+    if (threadIdx.x < 32) {
+        const unsigned long long b = lookback_exclusive(status, tile, tot);
+        if (threadIdx.x == 0) s_base = b;
+    }
     __syncthreads();
     unsigned long long run = s_base + ex;
 #pragma unroll

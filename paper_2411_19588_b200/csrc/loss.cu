@@ -50,6 +50,12 @@ __device__ __forceinline__ float2 mul2(float2 a, float2 b) {
     return *reinterpret_cast<float2*>(&d);
 }
 
+__device__ __forceinline__ float rcp_approx(float x) {
+    float y;
+    asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+    return y;
+}
+
 // 4-byte asynchronous global -> shared copy; ok = false writes a zero
 __device__ __forceinline__ void cp_async4(float* sdst, const float* gsrc, bool ok) {
     const unsigned s = (unsigned)__cvta_generic_to_shared(sdst);
@@ -97,7 +103,8 @@ __global__ void __launch_bounds__(kThreads, 3) k_ssim_moments(const float* __res
     const int x0 = blockIdx.x * kT, y0 = blockIdx.y * kT;  // valid-window origin == image pixel
     const int VW = W - 2 * kR, VH = H - 2 * kR;
     const size_t plane = (size_t)VH * VW;
-    // stage rows of kP*C contiguous floats (coalesced): one warp per row
+    // stage rows of kP*C contiguous floats (coalesced): one warp per row, every
+    // copy asynchronous so all of the patch's loads are in flight at once
     {
         const int rowlen = kP * C;
         const int lane = threadIdx.x & 31;
@@ -107,24 +114,14 @@ __global__ void __launch_bounds__(kThreads, 3) k_ssim_moments(const float* __res
             const float* ra = img_a + ((size_t)min(gy, H - 1) * W + x0) * C;
             const float* rb = img_b + ((size_t)min(gy, H - 1) * W + x0) * C;
             const bool rok = gy < H;
-            constexpr int kU = (kP * kMaxC + 31) / 32;  // covers the longest row
-            float va[kU], vb[kU];
-#pragma unroll
-            for (int u = 0; u < kU; ++u) {  // all loads in flight before the stores
-                const int q = lane + 32 * u;
+            for (int q = lane; q < rowlen; q += 32) {
                 const bool ok = rok && q < qmax;
-                va[u] = ok ? __ldg(ra + q) : 0.f;
-                vb[u] = ok ? __ldg(rb + q) : 0.f;
-            }
-#pragma unroll
-            for (int u = 0; u < kU; ++u) {
-                const int q = lane + 32 * u;
-                if (q < rowlen) {
-                    sa[r * pitch + q] = va[u];
-                    sb[r * pitch + q] = vb[u];
-                }
+                cp_async4(&sa[r * pitch + q], ok ? ra + q : img_a, ok);
+                cp_async4(&sb[r * pitch + q], ok ? rb + q : img_b, ok);
             }
         }
+        cp_async_commit();
+        cp_async_wait<0>();
     }
     __syncthreads();
     float ssum = 0.f;
@@ -203,13 +200,14 @@ __global__ void __launch_bounds__(kThreads, 3) k_ssim_moments(const float* __res
                 const float A2 = 2.0f * (v12 - u1 * u2) + (float)kC2;
                 const float B1 = u1 * u1 + u2 * u2 + (float)kC1;
                 const float B2 = (v1 - u1 * u1) + (v2 - u2 * u2) + (float)kC2;
-                const float inv = 1.0f / (B1 * B2);
+                // B1 >= C1 and B2 >= C2 (> 0): approximate reciprocals (rel. error ~2^-22)
+                const float r1 = rcp_approx(B1), r2 = rcp_approx(B2);
+                const float inv = r1 * r2;
                 const float S = A1 * A2 * inv;
                 ssum += S;
                 const size_t o = (size_t)oy * VW + ox;
-                maps[(0 * C + ch) * plane + o] =
-                    2.0f * u2 * (A2 - A1) * inv - 2.0f * u1 * S * (1.0f / B1 - 1.0f / B2);
-                maps[(1 * C + ch) * plane + o] = -S / B2;
+                maps[(0 * C + ch) * plane + o] = 2.0f * u2 * (A2 - A1) * inv - 2.0f * u1 * S * (r1 - r2);
+                maps[(1 * C + ch) * plane + o] = -S * r2;
                 maps[(2 * C + ch) * plane + o] = 2.0f * A1 * inv;
             }
         }
@@ -242,16 +240,25 @@ __global__ void __launch_bounds__(kThreads, 3) k_ssim_grad(const float* __restri
     const int VW = W - 2 * kR, VH = H - 2 * kR;
     const size_t plane = (size_t)VH * VW;
     // adj[y][x] = sum_{u,v} w_u w_v M[y+u-2R][x+v-2R], M zero outside the valid grid
-    auto issue = [&](int ch) {
+    auto issue = [&](int ch) {  // one warp per window row (kP = 42 columns: 2 per lane)
         Win& dst = sbuf[ch & 1];
-        for (int i = threadIdx.x; i < kP * kP; i += kThreads) {
-            const int r = i / kP, c = i - r * kP;
-            const int my = y0 + r - 2 * kR, mx = x0 + c - 2 * kR;
-            const bool ok = my >= 0 && my < VH && mx >= 0 && mx < VW;
-            const size_t o = ok ? (size_t)my * VW + mx : 0;
+        const int lane = threadIdx.x & 31;
+        const float* m0 = maps + (size_t)(0 * C + ch) * plane;
+        const float* m1 = maps + (size_t)(1 * C + ch) * plane;
+        const float* m2 = maps + (size_t)(2 * C + ch) * plane;
+        for (int r = threadIdx.x >> 5; r < kP; r += kThreads / 32) {
+            const int my = y0 + r - 2 * kR;
+            const bool rok = my >= 0 && my < VH;
 #pragma unroll
-            for (int m = 0; m < 3; ++m)
-                cp_async4(&dst[m][r][c], maps + (m * C + ch) * plane + o, ok);
+            for (int c = lane; c < 64; c += 32) {
+                if (c >= kP) break;
+                const int mx = x0 + c - 2 * kR;
+                const bool ok = rok && mx >= 0 && mx < VW;
+                const size_t o = ok ? (size_t)my * VW + mx : 0;
+                cp_async4(&dst[0][r][c], m0 + o, ok);
+                cp_async4(&dst[1][r][c], m1 + o, ok);
+                cp_async4(&dst[2][r][c], m2 + o, ok);
+            }
         }
         cp_async_commit();
     };

@@ -142,7 +142,10 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) k_preprocess(uws_cloud c
     }
     unsigned long long total;
     unsigned long long ex = block_exclusive_sum<kThreads, unsigned long long>(cnt, s_scan, &total);
-    if (threadIdx.x == 0) s_base = lookback_exclusive(status, tile, total);
+    if (threadIdx.x < 32) {
+        const unsigned long long b = lookback_exclusive(status, tile, total);
+        if (threadIdx.x == 0) s_base = b;
+    }
     __syncthreads();
     unsigned long long row = s_base + ex;
 #pragma unroll

@@ -21,26 +21,38 @@ __device__ __forceinline__ void st_volatile(unsigned long long* p, unsigned long
 __device__ __forceinline__ unsigned ld_volatile(const unsigned* p) { return *(const volatile unsigned*)p; }
 __device__ __forceinline__ void st_volatile(unsigned* p, unsigned v) { *(volatile unsigned*)p = v; }
 
-// Called by ONE thread of block `tile`: publishes the block aggregate, walks
-// back over predecessors and returns the exclusive prefix of this block.
+// Called by ALL lanes of ONE warp of block `tile`: publishes the block aggregate,
+// walks back over the predecessors 32 at a time (lane l reads tile - 1 - l - 32k)
+// and returns the exclusive prefix of this block in every lane.  A window is
+// consumed up to its first inclusive prefix, or up to its first unpublished
+// predecessor (then re-polled from there).
 __device__ __forceinline__ unsigned long long lookback_exclusive(unsigned long long* status, int tile,
                                                                  unsigned long long aggregate) {
+    const int lane = threadIdx.x & 31;
     if (tile == 0) {
-        st_volatile(&status[0], kLbInc | aggregate);
+        if (lane == 0) st_volatile(&status[0], kLbInc | aggregate);
         return 0;
     }
-    st_volatile(&status[tile], kLbAgg | aggregate);
+    if (lane == 0) st_volatile(&status[tile], kLbAgg | aggregate);
     unsigned long long excl = 0;
-    int j = tile - 1;
+    int j = tile - 1;  // newest predecessor not yet summed
     while (true) {
-        unsigned long long s = ld_volatile(&status[j]);
-        unsigned long long flag = s >> 62;
-        if (flag == 0) continue;
-        excl += s & kLbMask;
-        if (flag == 2) break;
-        --j;
+        const int k = j - lane;
+        const unsigned long long s = k >= 0 ? ld_volatile(&status[k]) : kLbInc;  // before tile 0: 0
+        const unsigned flag = (unsigned)(s >> 62);
+        const unsigned inc = __ballot_sync(0xffffffffu, flag == 2);
+        const unsigned nready = __ballot_sync(0xffffffffu, flag == 0);
+        const int m = inc ? __ffs(inc) - 1 : 31;                   // last lane of the window
+        const unsigned win = m == 31 ? 0xffffffffu : ((2u << m) - 1u);
+        const int take = (nready & win) ? __ffs(nready & win) - 1 : m + 1;  // lanes [0, take)
+        unsigned long long v = lane < take ? (s & kLbMask) : 0ull;
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+        excl += v;
+        if (take == m + 1 && inc) break;
+        j -= take;
     }
-    st_volatile(&status[tile], kLbInc | (excl + aggregate));
+    if (lane == 0) st_volatile(&status[tile], kLbInc | (excl + aggregate));
     return excl;
 }
 
