@@ -89,6 +89,13 @@ typedef struct uws_raster_out {
     int32_t* last;         /* [H][W] consumed prefix length of the tile list (backward context) */
     float* attenuation;    /* optional [H][W][3] exp(-B_d z) */
     float* backscatter;    /* optional [H][W][3] B_inf (1 - exp(-B_b z)) */
+    /* optional (row-list path): the first tile_rows_cap rows each tile staged, in
+     * list order, so the backward reads its consumed prefix instead of filtering
+     * the row lists again; NULL to skip.  tile_rows [tiles][tile_rows_cap],
+     * tile_nrows [tiles] = rows stored (written by uws_raster_fwd_rows). */
+    int32_t* tile_rows;
+    int32_t* tile_nrows;
+    int32_t tile_rows_cap;
 } uws_raster_out;
 
 /* Adam hyper-parameters for one apply_gradients call (optim.py:69-120).

@@ -41,7 +41,8 @@ class ProjectedC(ctypes.Structure):
 class RasterOutC(ctypes.Structure):
     _fields_ = [("color", c_void_p), ("color_clean", c_void_p), ("depth", c_void_p),
                 ("weight", c_void_p), ("final_T", c_void_p), ("count", c_void_p),
-                ("last", c_void_p), ("attenuation", c_void_p), ("backscatter", c_void_p)]
+                ("last", c_void_p), ("attenuation", c_void_p), ("backscatter", c_void_p),
+                ("tile_rows", c_void_p), ("tile_nrows", c_void_p), ("tile_rows_cap", c_int32)]
 
 
 class AdamParamsC(ctypes.Structure):

@@ -42,6 +42,9 @@ struct BwdArgs {
     const int32_t* entries;
     const int32_t* row_start;    // ... or tile-row lists filtered on the fly
     const uint2* row_items;
+    const int32_t* tile_rows;    // the forward's staged rows per tile (optional)
+    const int32_t* tile_nrows;
+    int tile_rows_cap;
     int width, height, gx;
     const float* medium;
     const float* color_clean;
@@ -175,7 +178,11 @@ __global__ void __launch_bounds__(kThreads, MINB) k_raster_bwd(BwdArgs a) {
     static_assert(sizeof(Rec) == 64, "record layout");
     const int nbatch = (maxlast + kBatch - 1) / kBatch;
     int rend = 0, stride = 1;
-    if (ROWS && nbatch > 0) {
+    // the forward stored this tile's consumed prefix: no filtering of the row lists
+    const int32_t* saved = (ROWS && a.tile_rows && maxlast <= a.tile_nrows[tile])
+                               ? a.tile_rows + (size_t)tile * a.tile_rows_cap
+                               : nullptr;
+    if (ROWS && nbatch > 0 && !saved) {
         // pass 1 over the row list: where does each batch of tile entries start?
         const int rs = a.row_start[ty];
         rend = a.row_start[ty + 1];
@@ -208,7 +215,7 @@ __global__ void __launch_bounds__(kThreads, MINB) k_raster_bwd(BwdArgs a) {
         const int lo = bi * kBatch;
         const int nb = min(kBatch, maxlast - lo);
         __syncthreads();
-        if (ROWS) {
+        if (ROWS && !saved) {
             // pass 2: re-collect this batch's rows from its recorded start
             const int mk = bi / stride;
             int cur = sMarkCur[mk];
@@ -224,8 +231,9 @@ __global__ void __launch_bounds__(kThreads, MINB) k_raster_bwd(BwdArgs a) {
             const int i = threadIdx.x + s * kThreads;
             if (i < nb) {
                 Rec& r = sRec[i];
-                stage_entry(a.splat, ROWS ? sRow[i] : a.entries[start + lo + i], ox, oy, r.A, r.B,
-                            r.C);
+                const int row =
+                    ROWS ? (saved ? saved[lo + i] : sRow[i]) : a.entries[start + lo + i];
+                stage_entry(a.splat, row, ox, oy, r.A, r.B, r.C);
                 // exact x-ranges of the pass region within each warp's band rows
                 PassRegion pr;
                 pr.init(r.A, r.B);
@@ -375,6 +383,9 @@ extern "C" int uws_raster_bwd(const uws_projected* proj, const int32_t* offsets,
     a.medium_acc = medium_acc;
     a.row_start = nullptr;
     a.row_items = nullptr;
+    a.tile_rows = nullptr;
+    a.tile_nrows = nullptr;
+    a.tile_rows_cap = 0;
     k_raster_bwd<false, 12><<<a.gx * gy, kThreads, 0, as_stream(stream)>>>(a);
     UWS_CHECK_LAUNCH("k_raster_bwd");
     return UWS_OK;
@@ -397,6 +408,9 @@ extern "C" int uws_raster_bwd_rows(const uws_projected* proj, const int32_t* row
     a.entries = nullptr;
     a.row_start = row_start;
     a.row_items = (const uint2*)row_items;
+    a.tile_rows = fwd->tile_rows;
+    a.tile_nrows = fwd->tile_nrows;
+    a.tile_rows_cap = fwd->tile_rows_cap;
     a.width = cam->width;
     a.height = cam->height;
     a.gx = (int)ceil_div(cam->width, kTile);

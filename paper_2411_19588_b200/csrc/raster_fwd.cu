@@ -129,6 +129,8 @@ __global__ void __launch_bounds__(kRasterThreads / PX, 4 * PX) k_raster_fwd(FwdA
             const int i = threadIdx.x + s * kThreads;
             if (i < n) {
                 const int row = ROWS ? sRow[i] : a.entries[start + base + i];
+                if (ROWS && a.out.tile_rows && base + i < a.out.tile_rows_cap)
+                    a.out.tile_rows[(size_t)tile * a.out.tile_rows_cap + base + i] = row;
                 StageA sa;
                 StageB sb;
                 StageC sc;
@@ -226,6 +228,8 @@ __global__ void __launch_bounds__(kRasterThreads / PX, 4 * PX) k_raster_fwd(FwdA
             nst = rem;
         }
     }
+    if (ROWS && a.out.tile_rows && threadIdx.x == 0)
+        a.out.tile_nrows[tile] = min(base, a.out.tile_rows_cap);
 #pragma unroll
     for (int j = 0; j < PX; ++j) {
         if (!inside[j]) continue;
@@ -299,6 +303,8 @@ extern "C" int uws_raster_fwd_rows(const uws_projected* proj, const int32_t* row
                 "uws_raster_fwd_rows: missing output buffer");
     UWS_REQUIRE(medium == nullptr || out->color_clean != nullptr,
                 "uws_raster_fwd_rows: underwater mode needs color_clean");
+    UWS_REQUIRE(out->tile_rows == nullptr || (out->tile_nrows && out->tile_rows_cap > 0),
+                "uws_raster_fwd_rows: tile_rows needs tile_nrows and a positive cap");
     FwdArgs a;
     a.splat = proj->splat;
     a.exact = proj->exact;

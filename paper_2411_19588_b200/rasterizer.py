@@ -155,21 +155,36 @@ class RenderOutput:
     attenuation_map: Optional[torch.Tensor] = None
     backscatter_map: Optional[torch.Tensor] = None
     rows: Optional[RowLists] = None               # row lists the forward composited from
+    # backward context of the row-list path: the rows each tile staged (first
+    # TILE_ROWS_CAP per tile) and how many were stored
+    tile_rows: Optional[torch.Tensor] = None
+    tile_nrows: Optional[torch.Tensor] = None
 
     def c_struct(self) -> _lib.RasterOutC:
+        cap = self.tile_rows.shape[1] if self.tile_rows is not None else 0
         return _lib.RasterOutC(_lib.ptr(self.color), _lib.ptr(self.color_clean),
                                _lib.ptr(self.depth), _lib.ptr(self.weight),
                                _lib.ptr(self.final_transmittance), _lib.ptr(self.count),
                                _lib.ptr(self.last), _lib.ptr(self.attenuation_map),
-                               _lib.ptr(self.backscatter_map))
+                               _lib.ptr(self.backscatter_map), _lib.ptr(self.tile_rows),
+                               _lib.ptr(self.tile_nrows), cap)
 
 
-def _alloc_output(H, W, dev, mode, medium_maps):
+# staged rows kept per tile for the backward (the consumed prefix is ~140 rows on
+# average at 1M Gaussians 1080p; tiles that consumed more re-filter the row lists)
+TILE_ROWS_CAP = 1024
+
+
+def _alloc_output(H, W, dev, mode, medium_maps, tile_rows=True):
     f = dict(dtype=torch.float32, device=dev)
     out = RenderOutput(color=torch.empty(H, W, 3, **f), depth=torch.empty(H, W, **f),
                        weight=torch.empty(H, W, **f), final_transmittance=torch.empty(H, W, **f),
                        count=torch.empty(H, W, dtype=torch.int32, device=dev), mode=mode,
                        last=torch.empty(H, W, dtype=torch.int32, device=dev))
+    if tile_rows:
+        tiles = ((H + TILE_SIZE - 1) // TILE_SIZE) * ((W + TILE_SIZE - 1) // TILE_SIZE)
+        out.tile_rows = torch.empty(tiles, TILE_ROWS_CAP, dtype=torch.int32, device=dev)
+        out.tile_nrows = torch.empty(tiles, dtype=torch.int32, device=dev)
     if mode == "underwater":
         out.color_clean = torch.empty(H, W, 3, **f)
         if medium_maps:
@@ -182,7 +197,7 @@ def composite(proj: ProjectedCloud, bins: TileBins, cam, medium: Optional[Medium
               mode: str = "clean", medium_maps: bool = False) -> RenderOutput:
     """Run the compositing kernel on existing projection + bins."""
     cam = Camera.from_any(cam)
-    out = _alloc_output(cam.height, cam.width, proj.device, mode, medium_maps)
+    out = _alloc_output(cam.height, cam.width, proj.device, mode, medium_maps, tile_rows=False)
     pc, cc, oc = proj.c_struct(), cam.c_struct(), out.c_struct()
     med = _lib.ptr(medium.flat) if mode == "underwater" else 0
     _lib.call("uws_raster_fwd", ctypes.byref(pc), _lib.ptr(bins.offsets), _lib.ptr(bins.entries),
@@ -205,7 +220,7 @@ def render(cloud: GaussianCloud, cam, medium: Optional[MediumParams] = None,
     cam = Camera.from_any(cam)
     proj = project_cloud(cloud, cam, with_geometry=False)
     rows = bin_rows(proj, cam.width, cam.height)
-    out = _alloc_output(cam.height, cam.width, proj.device, mode, medium_maps)
+    out = _alloc_output(cam.height, cam.width, proj.device, mode, medium_maps, tile_rows=retain)
     pc, cc, oc = proj.c_struct(), cam.c_struct(), out.c_struct()
     med = _lib.ptr(medium.flat) if mode == "underwater" else 0
     _lib.call("uws_raster_fwd_rows", ctypes.byref(pc), _lib.ptr(rows.row_start),

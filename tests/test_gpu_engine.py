@@ -209,3 +209,48 @@ def test_tile_list_backward_matches_row_list_backward(name):
         bufs.append(np_(uw.backward_render(out, dL, s.cloud, med, 0.1).flat).astype(np.float64))
     a, b = bufs
     assert np.abs(a - b).max() <= 1e-5 * max(np.abs(b).max(), 1e-30)
+
+
+@pytest.mark.parametrize("name", ["survey2k", "opaque3k"])
+def test_forward_stored_rows_are_the_tile_list_prefix(name):
+    """tile_rows[t, :tile_nrows[t]] is the head of tile t's list in the reference order
+    (the rows the forward staged, reused by the backward)."""
+    g = load(name)
+    s, cam = _state(g)
+    med = s.medium if g.mode == "underwater" else None
+    out = uw.render(s.cloud, cam, med, g.mode)
+    offs = np_(out.bins.offsets).astype(np.int64)
+    ent = np_(out.bins.entries).astype(np.int64)
+    rows, nrows = np_(out.tile_rows), np_(out.tile_nrows)
+    last = np_(out.last)
+    assert nrows.shape[0] == offs.shape[0] - 1 and (nrows > 0).any()
+    gx = (cam.width + 15) // 16
+    for t in range(nrows.shape[0]):
+        n = int(nrows[t])
+        assert n <= offs[t + 1] - offs[t]
+        np.testing.assert_array_equal(rows[t, :n], ent[offs[t]:offs[t] + n])
+        ty, tx = divmod(t, gx)
+        consumed = last[16 * ty:16 * ty + 16, 16 * tx:16 * tx + 16].max()
+        assert consumed <= n or n == uw.rasterizer.TILE_ROWS_CAP
+
+
+@pytest.mark.parametrize("name", ["survey2k", "opaque3k"])
+def test_backward_from_stored_rows_matches_refiltering(name, monkeypatch):
+    """The backward reading the forward's stored rows == re-filtering the row lists,
+    also when a small cap sends the longer tiles down the re-filtering path."""
+    g = load(name)
+    s, cam = _state(g)
+    med = s.medium if g.mode == "underwater" else None
+    gt = torch.as_tensor(g.gt, dtype=torch.float32).cuda()
+    outs = [uw.render(s.cloud, cam, med, g.mode)]
+    monkeypatch.setattr(uw.rasterizer, "TILE_ROWS_CAP", 8)
+    outs.append(uw.render(s.cloud, cam, med, g.mode))
+    assert outs[1].tile_rows.shape[1] == 8
+    outs.append(uw.render(s.cloud, cam, med, g.mode))
+    outs[2].tile_rows = outs[2].tile_nrows = None      # re-filter every tile
+    bufs = []
+    for out in outs:
+        _, dL = uw.total_loss(out.color, gt, med, 0.3, 0.1)
+        bufs.append(np_(uw.backward_render(out, dL, s.cloud, med, 0.1).flat).astype(np.float64))
+    for a in bufs[:2]:
+        assert np.abs(a - bufs[2]).max() <= 1e-5 * max(np.abs(bufs[2]).max(), 1e-30)
