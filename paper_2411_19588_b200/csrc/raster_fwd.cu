@@ -21,6 +21,7 @@ namespace uws {
 namespace {
 
 constexpr int kBatch = 256;
+constexpr int kFirstFill = 128;
 constexpr int kListPad = 4;                    // per-warp lists are walked 4 entries at a time
 constexpr int kFwdPx = 2;                      // pixels per thread (measured: 1 and 4 are slower)
 
@@ -112,8 +113,11 @@ __global__ void __launch_bounds__(kRasterThreads / PX, 4 * PX) k_raster_fwd(FwdA
         if (__syncthreads_count(!alive()) == kThreads) break;
         int n;
         if (ROWS) {
-            // fill the staging list with >= 256 rows of this tile (or all that remain)
-            while (nst < kBatch && cur < end) {
+            // fill the staging list with >= kFirstFill rows of this tile for the first
+            // batch (most tiles saturate within ~150 entries: less filtering), then
+            // >= kBatch rows (or all that remain)
+            const int fill = base == 0 ? kFirstFill : kBatch;
+            while (nst < fill && cur < end) {
                 nst += filter_chunk<kThreads>(a.row_items, cur, end, tx, sRow, nst,
                                               kBatch + kChunk, sScan);
                 cur += kChunk;
