@@ -81,6 +81,7 @@ __global__ void __launch_bounds__(kThreads, MINB) k_adam_cloud(float* __restrict
                                                          float* __restrict__ Gr, int64_t n,
                                                          int nb_flat, uws_adam_params hp,
                                                          AdamCtl ctl) {
+    // launched serially (no pdl_entry): the per-CTA L1 invalidation costs more here
     const bool skip = ctl.skip && *ctl.skip > 0.0f;
     if ((int)blockIdx.x < nb_flat) {
         const int64_t n10 = 10 * n;
@@ -169,6 +170,7 @@ __global__ void __launch_bounds__(kThreads, 4) k_adam_cloud4(float* __restrict__
                                                              float* __restrict__ V,
                                                              float* __restrict__ Gr, int64_t n,
                                                              uws_adam_params hp, AdamCtl ctl) {
+    // launched serially (no pdl_entry): the per-CTA L1 invalidation costs more here
     const int64_t t = (int64_t)blockIdx.x * kThreads + threadIdx.x;
     const int64_t groups = 14 * n / 4;
     if (t >= groups) return;
@@ -224,6 +226,7 @@ __global__ void __launch_bounds__(kThreads, 4) k_adam_cloud4(float* __restrict__
 
 __global__ void k_adam_medium(float* __restrict__ P, float* __restrict__ M, float* __restrict__ V,
                               float* __restrict__ Gr, uws_adam_params hp, AdamCtl ctl) {
+    pdl_entry();
     const int v = threadIdx.x;
     if (v >= 16) return;
     const bool skip = ctl.skip && *ctl.skip > 0.0f;
@@ -268,7 +271,7 @@ extern "C" int uws_adam_step(float* params, float* exp_avg, float* exp_avg_sq, f
                     "uws_adam_step: null medium buffer");
         AdamCtl mctl = ctl;
         mctl.zero_grads = 0;
-        k_adam_medium<<<1, 32, 0, st>>>(medium_params, medium_exp_avg, medium_exp_avg_sq,
+        launch(k_adam_medium, dim3(1), dim3(32), 0, st, medium_params, medium_exp_avg, medium_exp_avg_sq,
                                         medium_grads, *hp, mctl);
         UWS_CHECK_LAUNCH("k_adam_medium");
     }
@@ -278,14 +281,14 @@ extern "C" int uws_adam_step(float* params, float* exp_avg, float* exp_avg_sq, f
                              ((uintptr_t)params | (uintptr_t)exp_avg | (uintptr_t)exp_avg_sq |
                               (uintptr_t)grads) % 16 == 0;
         if (aligned) {
-            k_adam_cloud4<<<(unsigned)ceil_div(14 * n / 4, kThreads), kThreads, 0, st>>>(
+            launch_serial(k_adam_cloud4, dim3((unsigned)ceil_div(14 * n / 4, kThreads)), dim3(kThreads), 0, st, 
                 params, exp_avg, exp_avg_sq, grads, n, *hp, ctl);
             UWS_CHECK_LAUNCH("k_adam_cloud4");
         } else {
             constexpr int kEpt = 2;
             const int nb_flat = (int)ceil_div(10 * n, kThreads * kEpt);
             const int nb_rot = (int)ceil_div(n, kThreads);
-            k_adam_cloud<kEpt, 4><<<(unsigned)(nb_flat + nb_rot), kThreads, 0, st>>>(
+            launch_serial(k_adam_cloud<kEpt, 4>, dim3((unsigned)(nb_flat + nb_rot)), dim3(kThreads), 0, st, 
                 params, exp_avg, exp_avg_sq, grads, n, nb_flat, *hp, ctl);
             UWS_CHECK_LAUNCH("k_adam_cloud");
         }
@@ -294,8 +297,8 @@ extern "C" int uws_adam_step(float* params, float* exp_avg, float* exp_avg_sq, f
         // medium slots and pad zeroed after every reader is done; the skip
         // counter (slot 9) is left alone: non-zero it keeps skipping later
         // steps until the host has handled the skip and cleared it
-        UWS_CUDA(cudaMemsetAsync(medium_grads, 0, 9 * sizeof(float), st));
-        UWS_CUDA(cudaMemsetAsync(medium_grads + 10, 0, 6 * sizeof(float), st));
+        UWS_CUDA(zero_async(medium_grads, 9 * sizeof(float), st));
+        UWS_CUDA(zero_async(medium_grads + 10, 6 * sizeof(float), st));
     }
     return UWS_OK;
 }

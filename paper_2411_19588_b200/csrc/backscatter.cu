@@ -105,6 +105,7 @@ __device__ double np_sum(const double* a, int n) {  // n <= 256
 }
 
 __global__ void k_bs_init(Hdr* hdr) {
+    pdl_entry();
     for (int i = threadIdx.x; i < kMaxEdges; i += blockDim.x) hdr->counts[i] = 0;
     if (threadIdx.x == 0) {
         hdr->zmin = ~0ull;
@@ -119,6 +120,7 @@ __global__ void __launch_bounds__(kThreads) k_bs_resize(const float* __restrict_
                                                         int th, int tw, double* __restrict__ rgb,
                                                         double* __restrict__ zout,
                                                         uint64_t* __restrict__ key, Hdr* hdr) {
+    pdl_entry();
     const uint32_t P = (uint32_t)th * (uint32_t)tw;
     const uint32_t p = blockIdx.x * kThreads + threadIdx.x;
     unsigned long long zk_min = ~0ull, zk_max = 0ull;
@@ -184,6 +186,7 @@ __global__ void __launch_bounds__(kThreads) k_bs_resize(const float* __restrict_
 // cluster_range over linspace(min, max, ne) (backscatter.py:82-97, 115-117)
 __global__ void __launch_bounds__(kThreads) k_bs_label(const double* __restrict__ z, uint32_t P,
                                                        int ne, Hdr* hdr, uint32_t* __restrict__ lab) {
+    pdl_entry();
     __shared__ double edges[kMaxEdges];
     __shared__ uint32_t cnt[kMaxEdges];
     const double lo = from_key(hdr->zmin), hi = from_key(hdr->zmax);
@@ -223,6 +226,7 @@ __global__ void __launch_bounds__(kThreads) k_bs_label(const double* __restrict_
 
 __global__ void k_bs_gather(const uint32_t* __restrict__ lab, const uint32_t* __restrict__ idx,
                             uint32_t P, uint32_t* __restrict__ out) {
+    pdl_entry();
     const uint32_t q = blockIdx.x * blockDim.x + threadIdx.x;
     if (q < P) out[q] = lab[idx[q]];
 }
@@ -232,6 +236,7 @@ __global__ void __launch_bounds__(kThreads) k_bs_pick(const uint32_t* __restrict
                                                       const uint32_t* __restrict__ idx, uint32_t P,
                                                       const Hdr* hdr, double p_dark,
                                                       uint32_t* __restrict__ pick) {
+    pdl_entry();
     __shared__ uint32_t start[kMaxEdges], quota[kMaxEdges];
     if (threadIdx.x == 0) {
         uint32_t s = 0;
@@ -258,6 +263,7 @@ __global__ void __launch_bounds__(1024) k_bs_compact(const uint32_t* __restrict_
                                                      double* __restrict__ dz,
                                                      double* __restrict__ drgb,
                                                      double* __restrict__ dark_out, Hdr* hdr) {
+    pdl_entry();
     __shared__ uint32_t tmp[1024 / 32 + 1];
     uint32_t base = 0;
     for (uint32_t c0 = 0; c0 < P; c0 += 1024) {
@@ -382,6 +388,7 @@ __global__ void __launch_bounds__(kFitThreads) k_bs_fit(const double* __restrict
                                                         const Hdr* hdr, int ni,
                                                         double* __restrict__ result,
                                                         float* __restrict__ guide) {
+    pdl_entry();
     __shared__ double edges[kMaxEdges];
     __shared__ unsigned long long best_v[kMaxEdges][3];
     __shared__ uint32_t best_j[kMaxEdges][3];
@@ -658,29 +665,29 @@ extern "C" int uws_estimate_backscatter(const float* image, const void* depth, i
     UWS_REQUIRE(ws.ok(), "uws_estimate_backscatter: workspace too small");
     const uint32_t P = p.P;
     const int blocks = (int)ceil_div(P, kThreads);
-    k_bs_init<<<1, kThreads, 0, st>>>(p.hdr);
+    launch(k_bs_init, dim3(1), dim3(kThreads), 0, st, p.hdr);
     UWS_CHECK_LAUNCH("k_bs_init");
     if (depth_is_raw)
-        k_bs_resize<true><<<blocks, kThreads, 0, st>>>(image, depth, h, w, p.th, p.tw, p.rgb, p.z,
+        launch(k_bs_resize<true>, dim3(blocks), dim3(kThreads), 0, st, image, depth, h, w, p.th, p.tw, p.rgb, p.z,
                                                        p.key, p.hdr);
     else
-        k_bs_resize<false><<<blocks, kThreads, 0, st>>>(image, depth, h, w, p.th, p.tw, p.rgb, p.z,
+        launch(k_bs_resize<false>, dim3(blocks), dim3(kThreads), 0, st, image, depth, h, w, p.th, p.tw, p.rgb, p.z,
                                                         p.key, p.hdr);
     UWS_CHECK_LAUNCH("k_bs_resize");
-    k_bs_label<<<blocks, kThreads, 0, st>>>(p.z, P, cfg->edges_num, p.hdr, p.lab);
+    launch(k_bs_label, dim3(blocks), dim3(kThreads), 0, st, p.z, P, cfg->edges_num, p.hdr, p.lab);
     UWS_CHECK_LAUNCH("k_bs_label");
     // stable by RGB sum (pixel order on ties), then stable by cluster
     UWS_CUDA(radix::sort_pairs<uint64_t>(p.r64, p.key, nullptr, p.key_sorted, p.idx_sorted, P,
                                          nullptr, 0, st));
-    k_bs_gather<<<blocks, kThreads, 0, st>>>(p.lab, p.idx_sorted, P, p.lab_g);
+    launch(k_bs_gather, dim3(blocks), dim3(kThreads), 0, st, p.lab, p.idx_sorted, P, p.lab_g);
     UWS_CHECK_LAUNCH("k_bs_gather");
     UWS_CUDA(radix::sort_pairs<uint32_t>(p.r32, p.lab_g, p.idx_sorted, p.lab_sorted, p.idx_final, P,
                                          nullptr, 0, st));
-    k_bs_pick<<<blocks, kThreads, 0, st>>>(p.lab_sorted, p.idx_final, P, p.hdr, cfg->p_dark, p.pick);
+    launch(k_bs_pick, dim3(blocks), dim3(kThreads), 0, st, p.lab_sorted, p.idx_final, P, p.hdr, cfg->p_dark, p.pick);
     UWS_CHECK_LAUNCH("k_bs_pick");
-    k_bs_compact<<<1, 1024, 0, st>>>(p.pick, p.z, p.rgb, P, p.dz, p.drgb, dark, p.hdr);
+    launch(k_bs_compact, dim3(1), dim3(1024), 0, st, p.pick, p.z, p.rgb, P, p.dz, p.drgb, dark, p.hdr);
     UWS_CHECK_LAUNCH("k_bs_compact");
-    k_bs_fit<<<1, kFitThreads, 0, st>>>(p.rgb, P, p.dz, p.drgb, p.hdr, cfg->intervals_num, result,
+    launch(k_bs_fit, dim3(1), dim3(kFitThreads), 0, st, p.rgb, P, p.dz, p.drgb, p.hdr, cfg->intervals_num, result,
                                         medium_guide);
     UWS_CHECK_LAUNCH("k_bs_fit");
     return UWS_OK;

@@ -62,6 +62,7 @@ __global__ void __launch_bounds__(kThreads) k_scan_u32(const uint32_t* __restric
                                                        uint32_t* total,
                                                        unsigned long long* status,
                                                        unsigned* ticket) {
+    pdl_entry();
     __shared__ int s_tile;
     __shared__ unsigned long long s_scan[kThreads / 32 + 1];
     __shared__ unsigned long long s_base;
@@ -164,6 +165,7 @@ __global__ void __launch_bounds__(kThreads) k_band_count(const uint32_t* __restr
                                                          int nbands, uint32_t nblk,
                                                          uint32_t* __restrict__ m_band,
                                                          unsigned long long* totals) {
+    pdl_entry();
     __shared__ int diff[kWarpsB][kMaxBands + 1];
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const uint32_t k = (uint32_t)*k_dev;
@@ -222,6 +224,7 @@ __global__ void __launch_bounds__(kThreads) k_band_scatter(const uint32_t* __res
                                                            const uint32_t* __restrict__ m_band_base,
                                                            const int32_t* __restrict__ overflow,
                                                            uint2* __restrict__ seg) {
+    pdl_entry();
     __shared__ int diff[kWarpsB][kMaxBands + 1];
     if (*overflow) return;
     const uint32_t k = (uint32_t)*k_dev;
@@ -258,6 +261,7 @@ __global__ void __launch_bounds__(kThreads) k_band_scatter(const uint32_t* __res
 __global__ void k_bin_guard(const unsigned long long* __restrict__ totals, uint64_t e_cap,
                             uint64_t s_cap, int32_t* __restrict__ overflow,
                             float* __restrict__ skip_counter) {
+    pdl_entry();
     if (threadIdx.x == 0) {
         const bool ovf = totals[0] > e_cap || totals[1] > s_cap;
         *overflow = ovf ? 1 : 0;
@@ -272,6 +276,7 @@ __global__ void k_bin_guard(const unsigned long long* __restrict__ totals, uint6
 __global__ void k_row_starts(const uint32_t* __restrict__ band_base, int nbands, uint32_t nblk_r,
                              const unsigned long long* __restrict__ totals,
                              const int32_t* __restrict__ overflow, int32_t* __restrict__ row_start) {
+    pdl_entry();
     const bool ovf = *overflow != 0;
     for (int y = threadIdx.x; y <= nbands; y += blockDim.x)
         row_start[y] = ovf ? 0 : (y < nbands ? (int32_t)band_base[(size_t)y * nblk_r]
@@ -286,6 +291,7 @@ __global__ void __launch_bounds__(kThreads) k_seg_blocks(const uint32_t* __restr
                                                          uint32_t* __restrict__ blk_start,
                                                          uint32_t* __restrict__ blk_band,
                                                          uint32_t* __restrict__ band_seg_start) {
+    pdl_entry();
     __shared__ uint32_t s_tmp[kThreads / 32 + 1];
     const int y = threadIdx.x;
     const bool ovf = *overflow != 0;
@@ -390,6 +396,7 @@ __global__ void __launch_bounds__(kThreads) k_cell_count(const uint2* __restrict
                                                          const uint32_t* __restrict__ blk_band,
                                                          const uint32_t* __restrict__ band_seg_start,
                                                          int nbands, uint32_t* __restrict__ m_cell) {
+    pdl_entry();
     __shared__ int diff[kWarpsB][kBand * kXS];
     const uint32_t nblocks = blk_start[nbands];
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -420,6 +427,7 @@ __global__ void __launch_bounds__(kThreads) k_cell_bandscan(uint32_t* __restrict
                                                             int gy,
                                                             const uint32_t* __restrict__ blk_start,
                                                             uint32_t* __restrict__ tile_count) {
+    pdl_entry();
     const int band = blockIdx.x;
     const uint32_t b0 = blk_start[band], b1 = blk_start[band + 1];
     const int ncell = kBand * gx;
@@ -458,6 +466,7 @@ __global__ void __launch_bounds__(kThreads) k_cell_scatter(const uint2* __restri
                                                            const uint32_t* __restrict__ m_cell,
                                                            const int32_t* __restrict__ offsets,
                                                            int32_t* __restrict__ entries) {
+    pdl_entry();
     __shared__ int diff[kWarpsB][kBand * kXS];
     __shared__ int s_loc[kBand * kMaxGX + 1];   // local run start per cell
     __shared__ int s_dst[kBand * kMaxGX];       // global run start per cell
@@ -651,7 +660,7 @@ extern "C" int uws_bin_count(const uws_projected* proj, int64_t k_cap, const uws
     grid_of(cam, &gx, &gy, &nbands);
     UWS_REQUIRE(gx <= kMaxGX && nbands <= kMaxBands, "uws_bin_count: image larger than 4096 px");
     cudaStream_t st = as_stream(stream);
-    UWS_CUDA(cudaMemsetAsync(totals, 0, 2 * sizeof(int64_t), st));
+    UWS_CUDA(zero_async(totals, 2 * sizeof(int64_t), st));
     if (k_cap == 0) return UWS_OK;
     Workspace ws(count_ws, count_bytes);
     CountPlan p;
@@ -662,23 +671,23 @@ extern "C" int uws_bin_count(const uws_projected* proj, int64_t k_cap, const uws
     // 0. stable order of the rows by (float64 depth bits, row): radix sort of the
     //    high words (4 passes), then the runs of equal high words by the low word
     const uint64_t* dbits = (const uint64_t*)proj->depth;
-    UWS_CUDA(cudaMemsetAsync(p.rs.hist, 0, p.rs.meta_bytes, st));
-    depth_sort::k_depth_hi<<<(unsigned)ceil_div(kc, 256), 256, 0, st>>>(dbits, k_dev, kc, p.keys_hi,
+    UWS_CUDA(zero_async(p.rs.hist, p.rs.meta_bytes, st));
+    launch(depth_sort::k_depth_hi, dim3((unsigned)ceil_div(kc, 256)), dim3(256), 0, st, dbits, k_dev, kc, p.keys_hi,
                                                                        p.long_cnt, p.rs.neg_min);
     UWS_CHECK_LAUNCH("k_depth_hi");
     UWS_CUDA(radix::sort_pairs<uint32_t>(p.rs, p.keys_hi, nullptr, p.keys_hi_sorted, p.sorted_rows,
                                          kc, k_dev, 0, st, /*meta_zeroed=*/true, /*relative=*/true));
-    depth_sort::k_tie_fix<<<(unsigned)ceil_div(kc, 256), 256, 0, st>>>(
+    launch(depth_sort::k_tie_fix, dim3((unsigned)ceil_div(kc, 256)), dim3(256), 0, st, 
         p.keys_hi_sorted, p.sorted_rows, dbits, k_dev, kc, p.long_cnt, p.long_list);
     UWS_CHECK_LAUNCH("k_tie_fix");
-    depth_sort::k_tie_fix_warp<<<148, 256, 0, st>>>(p.keys_hi_sorted, p.sorted_rows, dbits, k_dev,
+    launch(depth_sort::k_tie_fix_warp, dim3(148), dim3(256), 0, st, p.keys_hi_sorted, p.sorted_rows, dbits, k_dev,
                                                     kc, p.long_cnt, p.long_list, p.huge_list);
     UWS_CHECK_LAUNCH("k_tie_fix_warp");
-    depth_sort::k_tie_fix_long<<<32, depth_sort::kLongThreads, 0, st>>>(
+    launch(depth_sort::k_tie_fix_long, dim3(32), dim3(depth_sort::kLongThreads), 0, st, 
         p.keys_hi_sorted, p.sorted_rows, dbits, k_dev, kc, p.long_cnt, p.huge_list, p.rs.v_tmp);
     UWS_CHECK_LAUNCH("k_tie_fix_long");
     // 1a. per-block band histograms + totals (E entries, S band items)
-    k_band_count<<<p.nblk_r, kThreads, 0, st>>>(p.sorted_rows, (const short4*)proj->rect,
+    launch(k_band_count, dim3(p.nblk_r), dim3(kThreads), 0, st, p.sorted_rows, (const short4*)proj->rect,
                                                 proj->num_visible, nbands, p.nblk_r, p.m_band,
                                                 (unsigned long long*)totals);
     UWS_CHECK_LAUNCH("k_band_count");
@@ -698,8 +707,8 @@ extern "C" int uws_bin_emit(const uws_projected* proj, int64_t k_cap, int64_t e_
     grid_of(cam, &gx, &gy, &nbands);
     const int n_tiles = gx * gy;
     if (k_cap == 0) {
-        UWS_CUDA(cudaMemsetAsync(offsets, 0, sizeof(int32_t) * (n_tiles + 1), st));
-        UWS_CUDA(cudaMemsetAsync(overflow, 0, sizeof(int32_t), st));
+        UWS_CUDA(zero_async(offsets, sizeof(int32_t) * (n_tiles + 1), st));
+        UWS_CUDA(zero_async(overflow, sizeof(int32_t), st));
         return UWS_OK;
     }
     Workspace w1(count_ws, count_bytes);
@@ -713,20 +722,20 @@ extern "C" int uws_bin_emit(const uws_projected* proj, int64_t k_cap, int64_t e_
     const unsigned long long* tot = (const unsigned long long*)totals;
     const size_t n1 = (size_t)nbands * cp.nblk_r, n2 = (size_t)n_tiles;
     const size_t t1 = ceil_div(n1, kThreads * kScanIpt), t2 = ceil_div(n2, kThreads * kScanIpt);
-    UWS_CUDA(cudaMemsetAsync(ep.status, 0, (char*)(ep.tickets + 2) - (char*)ep.status, st));
-    k_bin_guard<<<1, 32, 0, st>>>(tot, (uint64_t)e_cap, (uint64_t)s_cap, overflow, skip_counter);
+    UWS_CUDA(zero_async(ep.status, (char*)(ep.tickets + 2) - (char*)ep.status, st));
+    launch(k_bin_guard, dim3(1), dim3(32), 0, st, tot, (uint64_t)e_cap, (uint64_t)s_cap, overflow, skip_counter);
     UWS_CHECK_LAUNCH("k_bin_guard");
     // 1b. band-list bases: exclusive scan of m_band in (band, block) order
-    k_scan_u32<<<(unsigned)t1, kThreads, 0, st>>>(cp.m_band, cp.m_band, (uint32_t)n1, nullptr,
+    launch(k_scan_u32, dim3((unsigned)t1), dim3(kThreads), 0, st, cp.m_band, cp.m_band, (uint32_t)n1, nullptr,
                                                   ep.status, ep.tickets);
     UWS_CHECK_LAUNCH("k_scan_u32(bands)");
     // 1c. stable scatter rank order -> band lists
-    k_band_scatter<<<cp.nblk_r, kThreads, 0, st>>>(cp.sorted_rows, (const short4*)proj->rect,
+    launch(k_band_scatter, dim3(cp.nblk_r), dim3(kThreads), 0, st, cp.sorted_rows, (const short4*)proj->rect,
                                                    proj->num_visible, nbands, cp.nblk_r, cp.m_band,
                                                    overflow, ep.seg);
     UWS_CHECK_LAUNCH("k_band_scatter");
     // 2a. block table of the band lists (all zero on overflow: later stages no-op)
-    k_seg_blocks<<<1, kThreads, 0, st>>>(cp.m_band, nbands, cp.nblk_r, tot, overflow, ep.blk_start,
+    launch(k_seg_blocks, dim3(1), dim3(kThreads), 0, st, cp.m_band, nbands, cp.nblk_r, tot, overflow, ep.blk_start,
                                          ep.blk_band, ep.band_seg_start);
     UWS_CHECK_LAUNCH("k_seg_blocks");
     // level-2 kernels loop over blocks (count known only on the device):
@@ -738,13 +747,13 @@ extern "C" int uws_bin_emit(const uws_projected* proj, int64_t k_cap, int64_t e_
         cudaDeviceGetAttribute(&n_sm, cudaDevAttrMultiProcessorCount, dev);
     }
     const unsigned grid2 = (unsigned)std::min<uint32_t>(ep.max_blocks, (uint32_t)n_sm * 4u);
-    k_cell_count<<<grid2, kThreads, 0, st>>>(ep.seg, (const short4*)proj->rect, gx, ep.blk_start,
+    launch(k_cell_count, dim3(grid2), dim3(kThreads), 0, st, ep.seg, (const short4*)proj->rect, gx, ep.blk_start,
                                              ep.blk_band, ep.band_seg_start, nbands, ep.m_cell);
     UWS_CHECK_LAUNCH("k_cell_count");
-    k_cell_bandscan<<<nbands, kThreads, 0, st>>>(ep.m_cell, gx, gy, ep.blk_start, ep.tile_count);
+    launch(k_cell_bandscan, dim3(nbands), dim3(kThreads), 0, st, ep.m_cell, gx, gy, ep.blk_start, ep.tile_count);
     UWS_CHECK_LAUNCH("k_cell_bandscan");
     // 2b. CSR ranges = exclusive scan of the per-tile counts (tile = ty*gx + tx)
-    k_scan_u32<<<(unsigned)t2, kThreads, 0, st>>>(ep.tile_count, (uint32_t*)offsets, (uint32_t)n2,
+    launch(k_scan_u32, dim3((unsigned)t2), dim3(kThreads), 0, st, ep.tile_count, (uint32_t*)offsets, (uint32_t)n2,
                                                   (uint32_t*)offsets + n2, ep.status + t1,
                                                   ep.tickets + 1);
     UWS_CHECK_LAUNCH("k_scan_u32(tiles)");
@@ -755,7 +764,7 @@ extern "C" int uws_bin_emit(const uws_projected* proj, int64_t k_cap, int64_t e_
                                       kStageCap * (int)sizeof(int32_t)));
         attr_set = true;
     }
-    k_cell_scatter<<<grid2, kThreads, kStageCap * sizeof(int32_t), st>>>(
+    launch(k_cell_scatter, dim3(grid2), dim3(kThreads), kStageCap * sizeof(int32_t), st, 
         ep.seg, (const short4*)proj->rect, gx, gy, ep.blk_start, ep.blk_band, ep.band_seg_start,
         nbands, ep.m_cell, offsets, entries);
     UWS_CHECK_LAUNCH("k_cell_scatter");
@@ -774,8 +783,8 @@ extern "C" int uws_bin_rows(const uws_projected* proj, int64_t k_cap, int64_t s_
     int gx, gy, nbands;
     grid_of(cam, &gx, &gy, &nbands);
     if (k_cap == 0) {
-        UWS_CUDA(cudaMemsetAsync(row_start, 0, sizeof(int32_t) * (gy + 1), st));
-        UWS_CUDA(cudaMemsetAsync(overflow, 0, sizeof(int32_t), st));
+        UWS_CUDA(zero_async(row_start, sizeof(int32_t) * (gy + 1), st));
+        UWS_CUDA(zero_async(overflow, sizeof(int32_t), st));
         return UWS_OK;
     }
     UWS_REQUIRE(row_items != nullptr, "uws_bin_rows: row_items is required");
@@ -786,18 +795,18 @@ extern "C" int uws_bin_rows(const uws_projected* proj, int64_t k_cap, int64_t s_
     const unsigned long long* tot = (const unsigned long long*)totals;
     const size_t n1 = (size_t)nbands * cp.nblk_r;
     const size_t t1 = ceil_div(n1, kThreads * kScanIpt);
-    UWS_CUDA(cudaMemsetAsync(cp.rstat, 0, (char*)(cp.rticket + 1) - (char*)cp.rstat, st));
+    UWS_CUDA(zero_async(cp.rstat, (char*)(cp.rticket + 1) - (char*)cp.rstat, st));
     // E is irrelevant here (no tile lists are materialised): only S is checked
-    k_bin_guard<<<1, 32, 0, st>>>(tot, ~0ull, (uint64_t)s_cap, overflow, skip_counter);
+    launch(k_bin_guard, dim3(1), dim3(32), 0, st, tot, ~0ull, (uint64_t)s_cap, overflow, skip_counter);
     UWS_CHECK_LAUNCH("k_bin_guard");
-    k_scan_u32<<<(unsigned)t1, kThreads, 0, st>>>(cp.m_band, cp.m_band, (uint32_t)n1, nullptr,
+    launch(k_scan_u32, dim3((unsigned)t1), dim3(kThreads), 0, st, cp.m_band, cp.m_band, (uint32_t)n1, nullptr,
                                                   cp.rstat, cp.rticket);
     UWS_CHECK_LAUNCH("k_scan_u32(rows)");
-    k_band_scatter<<<cp.nblk_r, kThreads, 0, st>>>(cp.sorted_rows, (const short4*)proj->rect,
+    launch(k_band_scatter, dim3(cp.nblk_r), dim3(kThreads), 0, st, cp.sorted_rows, (const short4*)proj->rect,
                                                    proj->num_visible, nbands, cp.nblk_r, cp.m_band,
                                                    overflow, row_items);
     UWS_CHECK_LAUNCH("k_band_scatter");
-    k_row_starts<<<1, 256, 0, st>>>(cp.m_band, nbands, cp.nblk_r, tot, overflow, row_start);
+    launch(k_row_starts, dim3(1), dim3(256), 0, st, cp.m_band, nbands, cp.nblk_r, tot, overflow, row_start);
     UWS_CHECK_LAUNCH("k_row_starts");
     return UWS_OK;
 }

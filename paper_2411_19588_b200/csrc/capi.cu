@@ -22,6 +22,24 @@ int cuda_fail(cudaError_t e, const char* what) {
     return UWS_ECUDA;
 }
 
+__global__ void k_zero_words(uint32_t* __restrict__ p, size_t words) {
+    pdl_entry();
+    for (size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x; i < words;
+         i += (size_t)gridDim.x * blockDim.x)
+        p[i] = 0u;
+}
+
+cudaError_t zero_async(void* ptr, size_t bytes, cudaStream_t st) {
+    if (bytes == 0) return cudaSuccess;
+    if (((uintptr_t)ptr | bytes) % 4 != 0) return cudaErrorInvalidValue;
+    const size_t words = bytes / 4;
+    const unsigned blocks = (unsigned)(words < (size_t)148 * 4 * 256 ? ceil_div((int64_t)words, 256)
+                                                                     : 148 * 4);
+    launch(k_zero_words, dim3(blocks), dim3(256), 0, st, (uint32_t*)ptr, words);
+    count_launches(1);
+    return cudaGetLastError();
+}
+
 }  // namespace uws
 
 extern "C" const char* uws_version(void) { return "uwsplat_b200 0.1.0 (sm_100a)"; }

@@ -6,6 +6,7 @@
 #include <stdint.h>
 
 #include <string>
+#include <utility>
 
 #include "../../include/uwsplat_b200.h"
 
@@ -63,6 +64,60 @@ int cuda_fail(cudaError_t e, const char* what);
     } while (0)
 
 inline int64_t ceil_div(int64_t a, int64_t b) { return (a + b - 1) / b; }
+
+// Programmatic dependent launch.  Kernels launched with launch() (programmatic
+// stream serialization) start with pdl_entry(): it lets the NEXT kernel in the
+// stream be launched as soon as all of this grid's CTAs are resident (its CTAs
+// fill the SMs this grid's tail frees), and blocks until the PREVIOUS grid has
+// completed and its writes are visible.  Because every such kernel waits before
+// it reads anything, completion stays transitive along the stream (kernel N+1
+// starts its work only after N, which started only after N-1, ...).
+// The wait does not drop L1 lines that the previous grid's CTAs loaded on this SM
+// while this CTA was already resident (e.g. a counter line that other CTAs then
+// changed with atomics: measured stale), hence the acquire fence, which
+// invalidates the SM's L1 (CCTL.IVALL) after the wait.
+__device__ __forceinline__ void pdl_entry() {
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+    asm volatile("griddepcontrol.wait;" ::: "memory");
+    asm volatile("fence.acquire.gpu;" ::: "memory");
+}
+
+template <bool PDL, typename... P, typename... A>
+inline void launch_ex(void (*kernel)(P...), dim3 grid, dim3 block, size_t smem, cudaStream_t st,
+                      A&&... args) {
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = grid;
+    cfg.blockDim = block;
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = st;
+    cfg.attrs = attr;
+    cfg.numAttrs = PDL ? 1 : 0;
+    (void)cudaLaunchKernelEx(&cfg, kernel, std::forward<A>(args)...);  // errors: cudaGetLastError
+}
+
+template <typename... P, typename... A>
+inline void launch(void (*kernel)(P...), dim3 grid, dim3 block, size_t smem, cudaStream_t st,
+                   A&&... args) {
+    launch_ex<true>(kernel, grid, block, smem, st, std::forward<A>(args)...);
+}
+
+// Zero `bytes` bytes at `ptr` (4-byte aligned) on the device.  Used instead of
+// cudaMemsetAsync inside the launch chains: a memset between two programmatically
+// serialized kernels does not order the second one after it (a kernel launched
+// right after a memset could run before the memset had landed).
+cudaError_t zero_async(void* ptr, size_t bytes, cudaStream_t st);
+
+// Launch after the previous grid has fully drained: for a kernel that depends on
+// the L1 / shared-memory split its SMs are configured with (an early-launched
+// grid inherits the previous kernel's carveout on SMs that never go idle).
+template <typename... P, typename... A>
+inline void launch_serial(void (*kernel)(P...), dim3 grid, dim3 block, size_t smem,
+                          cudaStream_t st, A&&... args) {
+    launch_ex<false>(kernel, grid, block, smem, st, std::forward<A>(args)...);
+}
 
 inline size_t align_up(size_t x, size_t a = 256) { return (x + a - 1) / a * a; }
 

@@ -49,6 +49,7 @@ __global__ void __launch_bounds__(kThreads) k_dens_classify(
     const float* __restrict__ P, int64_t n, const float* __restrict__ grad_accum,
     const int32_t* __restrict__ obs, double grad_thr, double size_thr, double min_opacity,
     unsigned char* __restrict__ codes, unsigned long long* __restrict__ blk_counts) {
+    pdl_entry();
     __shared__ unsigned long long s_tmp[kThreads / 32 + 1];
     const Fields F{n};
     unsigned keep = 0, clone = 0, split = 0;
@@ -86,6 +87,7 @@ __global__ void __launch_bounds__(kThreads) k_dens_classify(
 __global__ void __launch_bounds__(1024) k_dens_scan(const unsigned long long* __restrict__ blk_counts,
                                                      int nblk, long long* __restrict__ blk_off,
                                                      long long* __restrict__ totals) {
+    pdl_entry();
     __shared__ long long s_tmp[3][1024 / 32 + 1];
     long long run[3] = {0, 0, 0};
     for (int c0 = 0; c0 < nblk; c0 += 1024) {
@@ -142,6 +144,7 @@ __global__ void __launch_bounds__(kThreads) k_dens_apply(
     int64_t n, const unsigned char* __restrict__ codes, const long long* __restrict__ blk_off,
     const double* __restrict__ samples, double log_factor, int64_t n_keep, int64_t n_clone,
     int64_t n_split, float* __restrict__ P2, float* __restrict__ M2, float* __restrict__ V2) {
+    pdl_entry();
     __shared__ unsigned long long s_tmp[kThreads / 32 + 1];
     const Fields A{n};
     const Fields B{n_keep + n_clone + 2 * n_split};
@@ -206,6 +209,7 @@ __global__ void __launch_bounds__(kThreads) k_dens_apply(
 
 __global__ void k_reset_opacity(float* __restrict__ P, float* __restrict__ M,
                                 float* __restrict__ V, int64_t n, float value) {
+    pdl_entry();
     const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= n) return;
     P[13 * n + i] = value;
@@ -250,18 +254,18 @@ extern "C" int uws_densify_classify(const float* params, int64_t n, const float*
     UWS_REQUIRE(n == 0 || (params && grad_accum && obs_count), "uws_densify_classify: null buffer");
     cudaStream_t st = as_stream(stream);
     if (n == 0) {
-        UWS_CUDA(cudaMemsetAsync(totals, 0, 3 * sizeof(int64_t), st));
+        UWS_CUDA(zero_async(totals, 3 * sizeof(int64_t), st));
         return UWS_OK;
     }
     Workspace ws(workspace, workspace_bytes);
     DensPlan p;
     plan_dens(ws, n, p);
     UWS_REQUIRE(ws.ok(), "uws_densify_classify: workspace too small");
-    k_dens_classify<<<p.nblk, kThreads, 0, st>>>(params, n, grad_accum, obs_count, grad_threshold,
+    launch(k_dens_classify, dim3(p.nblk), dim3(kThreads), 0, st, params, n, grad_accum, obs_count, grad_threshold,
                                                  size_threshold, min_opacity, p.codes,
                                                  p.blk_counts);
     UWS_CHECK_LAUNCH("k_dens_classify");
-    k_dens_scan<<<1, 1024, 0, st>>>(p.blk_counts, p.nblk, p.blk_off, (long long*)totals);
+    launch(k_dens_scan, dim3(1), dim3(1024), 0, st, p.blk_counts, p.nblk, p.blk_off, (long long*)totals);
     UWS_CHECK_LAUNCH("k_dens_scan");
     return UWS_OK;
 }
@@ -283,7 +287,7 @@ extern "C" int uws_densify_apply(const float* params, const float* exp_avg,
     DensPlan p;
     plan_dens(ws, n, p);
     UWS_REQUIRE(ws.ok(), "uws_densify_apply: workspace too small");
-    k_dens_apply<<<p.nblk, kThreads, 0, as_stream(stream)>>>(
+    launch(k_dens_apply, dim3(p.nblk), dim3(kThreads), 0, as_stream(stream), 
         params, exp_avg, exp_avg_sq, n, p.codes, p.blk_off, samples, log_split_factor, n_keep,
         n_clone, n_split, new_params, new_exp_avg, new_exp_avg_sq);
     UWS_CHECK_LAUNCH("k_dens_apply");
@@ -295,7 +299,7 @@ extern "C" int uws_reset_opacities(float* params, float* exp_avg, float* exp_avg
     UWS_REQUIRE(n >= 0 && (n == 0 || (params && exp_avg && exp_avg_sq)),
                 "uws_reset_opacities: bad argument");
     if (n == 0) return UWS_OK;
-    k_reset_opacity<<<(unsigned)ceil_div(n, 256), 256, 0, as_stream(stream)>>>(params, exp_avg,
+    launch(k_reset_opacity, dim3((unsigned)ceil_div(n, 256)), dim3(256), 0, as_stream(stream), params, exp_avg,
                                                                                exp_avg_sq, n, value);
     UWS_CHECK_LAUNCH("k_reset_opacity");
     return UWS_OK;

@@ -36,6 +36,7 @@ __global__ void __launch_bounds__(256) k_depth_hi(const uint64_t* __restrict__ d
                                                   const uint32_t* __restrict__ n_dev, uint32_t n_cap,
                                                   uint32_t* __restrict__ keys, uint32_t* long_cnt,
                                                   uint32_t* neg_min) {
+    pdl_entry();
     __shared__ uint32_t s_min[8];
     const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
     if (i < 2) long_cnt[i] = 0;  // [0] runs > kShortRun, [1] runs > kWarpRun
@@ -59,6 +60,7 @@ __global__ void k_tie_fix(const uint32_t* __restrict__ keys, uint32_t* __restric
                           const uint64_t* __restrict__ depth_bits, const uint32_t* __restrict__ n_dev,
                           uint32_t n_cap, uint32_t* __restrict__ long_cnt,
                           uint32_t* __restrict__ long_list) {
+    pdl_entry();
     const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
     const uint32_t n = min(*n_dev, n_cap);
     if (i >= n) return;
@@ -109,6 +111,7 @@ __global__ void __launch_bounds__(256) k_tie_fix_warp(
     const uint32_t* __restrict__ keys, uint32_t* __restrict__ rows,
     const uint64_t* __restrict__ depth_bits, const uint32_t* __restrict__ n_dev, uint32_t n_cap,
     uint32_t* __restrict__ cnt, const uint32_t* __restrict__ list, uint32_t* __restrict__ huge) {
+    pdl_entry();
     const uint32_t n = min(*n_dev, n_cap);
     const uint32_t runs = cnt[0];
     const int lane = threadIdx.x & 31;
@@ -150,6 +153,7 @@ __global__ void __launch_bounds__(kLongThreads) k_tie_fix_long(
     const uint64_t* __restrict__ depth_bits, const uint32_t* __restrict__ n_dev, uint32_t n_cap,
     const uint32_t* __restrict__ long_cnt, const uint32_t* __restrict__ long_list,  // runs > 32
     uint32_t* __restrict__ tmp) {
+    pdl_entry();
     constexpr int W = kLongThreads / 32;
     __shared__ uint32_t s_base[256];
     __shared__ uint32_t s_wc[W][257];

@@ -93,6 +93,7 @@ __global__ void __launch_bounds__(kThreads, 3) k_ssim_moments(const float* __res
                                                               int H, int W, int C_,
                                                               float* __restrict__ maps,
                                                               double* __restrict__ part_s) {
+    // launched serially (no pdl_entry): the per-CTA L1 invalidation costs more here
     const int C = CT > 0 ? CT : C_;
     extern __shared__ float smem[];
     const int pitch = kP * C + 1;
@@ -228,6 +229,7 @@ __global__ void __launch_bounds__(kThreads, 3) k_ssim_grad(const float* __restri
                                                            float k_ssim, float k_l1,
                                                            float* __restrict__ grad,
                                                            double* __restrict__ part_l1) {
+    // launched serially (no pdl_entry): measured faster
     // double-buffered derivative-map windows [2][3][kP][kP+1] (cp.async: the next
     // channel's window streams in while this channel is filtered), then hs
     extern __shared__ float smem[];
@@ -357,6 +359,7 @@ __global__ void __launch_bounds__(kThreads) k_loss_finalize(const double* __rest
                                                             const float* medium, int has_guidance,
                                                             double lam_s, double lam_g,
                                                             double* result, float* nonfinite) {
+    pdl_entry();
     __shared__ double rs[kThreads], rl[kThreads];
     double s = 0, l = 0;
     for (int i = threadIdx.x; i < n_s; i += kThreads) s += part_s[i];
@@ -474,21 +477,21 @@ extern "C" int uws_loss_fwd_bwd(const float* rendered, const float* gt, int32_t 
     }
     dim3 g1((unsigned)ceil_div(vw, kT), (unsigned)ceil_div(vh, kT));
     if (c == 3)
-        k_ssim_moments<3><<<g1, kThreads, smem1, st>>>(rendered, gt, h, w, c, p.maps, p.part_s);
+        launch_serial(k_ssim_moments<3>, dim3(g1), dim3(kThreads), smem1, st, rendered, gt, h, w, c, p.maps, p.part_s);
     else
-        k_ssim_moments<0><<<g1, kThreads, smem1, st>>>(rendered, gt, h, w, c, p.maps, p.part_s);
+        launch_serial(k_ssim_moments<0>, dim3(g1), dim3(kThreads), smem1, st, rendered, gt, h, w, c, p.maps, p.part_s);
     UWS_CHECK_LAUNCH("k_ssim_moments");
     dim3 g2((unsigned)ceil_div(w, kT), (unsigned)ceil_div(h, kT));
     const float k_ssim = (float)(lambda_ssim * (-1.0 / n_win));
     const float k_l1 = (float)((1.0 - lambda_ssim) / n_px);
     if (c == 3)
-        k_ssim_grad<3><<<g2, kThreads, kGradSmem, st>>>(rendered, gt, h, w, c, p.maps, k_ssim,
+        launch_serial(k_ssim_grad<3>, dim3(g2), dim3(kThreads), kGradSmem, st, rendered, gt, h, w, c, p.maps, k_ssim,
                                                         k_l1, dL_dC, p.part_l1);
     else
-        k_ssim_grad<0><<<g2, kThreads, kGradSmem, st>>>(rendered, gt, h, w, c, p.maps, k_ssim,
+        launch_serial(k_ssim_grad<0>, dim3(g2), dim3(kThreads), kGradSmem, st, rendered, gt, h, w, c, p.maps, k_ssim,
                                                         k_l1, dL_dC, p.part_l1);
     UWS_CHECK_LAUNCH("k_ssim_grad");
-    k_loss_finalize<<<1, kThreads, 0, st>>>(p.part_s, p.n_s, p.part_l1, p.n_l1, n_px, n_win, medium,
+    launch(k_loss_finalize, dim3(1), dim3(kThreads), 0, st, p.part_s, p.n_s, p.part_l1, p.n_l1, n_px, n_win, medium,
                                             has_guidance, lambda_ssim, lambda_guide, result,
                                             nonfinite);
     UWS_CHECK_LAUNCH("k_loss_finalize");

@@ -125,6 +125,7 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) k_preprocess(uws_cloud c
                                                                      int gy,
                                                                      unsigned long long* status,
                                                                      unsigned* ticket) {
+    // launched serially (no pdl_entry): the per-CTA L1 invalidation costs more here
     __shared__ int s_tile;
     __shared__ unsigned long long s_scan[kThreads / 32 + 1];
     __shared__ unsigned long long s_base;
@@ -178,7 +179,7 @@ extern "C" int uws_preprocess_fwd(const uws_cloud* cloud, const uws_camera* cam,
     UWS_REQUIRE(out->num_visible != nullptr, "uws_preprocess_fwd: num_visible is required");
     cudaStream_t st = as_stream(stream);
     if (cloud->n == 0) {
-        UWS_CUDA(cudaMemsetAsync(out->num_visible, 0, sizeof(int32_t), st));
+        UWS_CUDA(zero_async(out->num_visible, sizeof(int32_t), st));
         return UWS_OK;
     }
     int gx = (int)ceil_div(cam->width, kTile), gy = (int)ceil_div(cam->height, kTile);
@@ -188,8 +189,8 @@ extern "C" int uws_preprocess_fwd(const uws_cloud* cloud, const uws_camera* cam,
     auto* status = ws.take<unsigned long long>(blocks);
     auto* ticket = ws.take<unsigned>(1);
     UWS_REQUIRE(ws.ok(), "uws_preprocess_fwd: workspace too small");
-    UWS_CUDA(cudaMemsetAsync(status, 0, (char*)(ticket + 1) - (char*)status, st));
-    k_preprocess<<<(unsigned)blocks, kThreads, 0, st>>>(*cloud, *cam, *out, gx, gy, status, ticket);
+    UWS_CUDA(zero_async(status, (char*)(ticket + 1) - (char*)status, st));
+    launch_serial(k_preprocess, dim3((unsigned)blocks), dim3(kThreads), 0, st, *cloud, *cam, *out, gx, gy, status, ticket);
     UWS_CHECK_LAUNCH("k_preprocess");
     return UWS_OK;
 }

@@ -56,6 +56,7 @@ __global__ void __launch_bounds__(kThreads) k_histogram(K* __restrict__ keys, ui
                                                        const uint32_t* n_dev, int begin_bit,
                                                        int passes, uint32_t* __restrict__ hist,
                                                        const K* __restrict__ neg_min) {
+    pdl_entry();
     __shared__ uint32_t h[8 * kBins];
     for (int i = threadIdx.x; i < passes * kBins; i += kThreads) h[i] = 0;
     __syncthreads();
@@ -95,6 +96,7 @@ __global__ void __launch_bounds__(kThreads) k_histogram(K* __restrict__ keys, ui
 static __global__ void __launch_bounds__(kBins) k_scan_hist(uint32_t* hist, int passes,
                                                             const uint32_t* n_dev, uint32_t n_cap,
                                                             uint32_t* trivial) {
+    pdl_entry();
     __shared__ uint32_t tmp[kBins / 32 + 1];
     const int p = blockIdx.x;
     const uint32_t n = dev_count(n_dev, n_cap);
@@ -123,6 +125,7 @@ __global__ void __launch_bounds__(kThreads) k_onesweep(PassArgs<K> pa, uint32_t 
                                                       const uint32_t* n_dev, int shift,
                                                       const uint32_t* __restrict__ bin_base,
                                                       uint32_t* status, uint32_t* ticket) {
+    pdl_entry();
     constexpr int IPT = Cfg<K>::kIpt;
     constexpr int TILE = kThreads * IPT;
     // executed passes before this one (j) and in total (m); the data after e executed
@@ -295,19 +298,19 @@ inline cudaError_t sort_pairs(const Plan<K>& p, K* keys_in, const uint32_t* vals
                               bool relative = false) {
     if (n_cap == 0) return cudaSuccess;
     if (!meta_zeroed) {
-        cudaError_t e = cudaMemsetAsync(p.hist, 0, p.meta_bytes, st);
+        cudaError_t e = zero_async(p.hist, p.meta_bytes, st);
         if (e != cudaSuccess) return e;
     }
     int hist_blocks = (int)ceil_div(n_cap, kThreads * 8);
     if (hist_blocks > 1184) hist_blocks = 1184;
-    k_histogram<K><<<hist_blocks, kThreads, 0, st>>>(keys_in, n_cap, n_dev, begin_bit, p.passes,
+    launch(k_histogram<K>, dim3(hist_blocks), dim3(kThreads), 0, st, keys_in, n_cap, n_dev, begin_bit, p.passes,
                                                      p.hist, relative ? p.neg_min : nullptr);
-    k_scan_hist<<<p.passes, kBins, 0, st>>>(p.hist, p.passes, n_dev, n_cap, p.trivial);
+    launch(k_scan_hist, dim3(p.passes), dim3(kBins), 0, st, p.hist, p.passes, n_dev, n_cap, p.trivial);
     const int tiles = (int)ceil_div(n_cap, tile_items<K>());
     PassArgs<K> pa{keys_in, vals_in, keys_out, vals_out, p.k_tmp, p.v_tmp, p.trivial, 0, p.passes};
     for (int q = 0; q < p.passes; ++q) {
         pa.pass = q;
-        k_onesweep<K><<<tiles, kThreads, 0, st>>>(pa, n_cap, n_dev, begin_bit + 8 * q,
+        launch(k_onesweep<K>, dim3(tiles), dim3(kThreads), 0, st, pa, n_cap, n_dev, begin_bit + 8 * q,
                                                   p.hist + q * kBins,
                                                   p.status + (size_t)q * tiles * kBins,
                                                   p.tickets + q);

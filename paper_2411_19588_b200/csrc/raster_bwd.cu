@@ -85,6 +85,7 @@ constexpr int kMaxMarks = 64;   // recorded batch starts per tile (row-list sour
 
 template <bool ROWS, int MINB>
 __global__ void __launch_bounds__(kThreads, MINB) k_raster_bwd(BwdArgs a) {
+    // launched serially (no pdl_entry): the per-CTA L1 invalidation costs more here
     __shared__ int sMarkCur[ROWS ? kMaxMarks : 1], sMarkSkip[ROWS ? kMaxMarks : 1];
     __shared__ int sScan[kWarps];
     struct __align__(16) Rec {
@@ -386,7 +387,7 @@ extern "C" int uws_raster_bwd(const uws_projected* proj, const int32_t* offsets,
     a.tile_rows = nullptr;
     a.tile_nrows = nullptr;
     a.tile_rows_cap = 0;
-    k_raster_bwd<false, 12><<<a.gx * gy, kThreads, 0, as_stream(stream)>>>(a);
+    launch_serial(k_raster_bwd<false, 12>, dim3(a.gx * gy), dim3(kThreads), 0, as_stream(stream), a);
     UWS_CHECK_LAUNCH("k_raster_bwd");
     return UWS_OK;
 }
@@ -423,7 +424,7 @@ extern "C" int uws_raster_bwd_rows(const uws_projected* proj, const int32_t* row
     a.dL = dL_dC;
     a.screen = screen_grads;
     a.medium_acc = medium_acc;
-    k_raster_bwd<true, 12><<<a.gx * gy, kThreads, 0, as_stream(stream)>>>(a);
+    launch_serial(k_raster_bwd<true, 12>, dim3(a.gx * gy), dim3(kThreads), 0, as_stream(stream), a);
     UWS_CHECK_LAUNCH("k_raster_bwd_rows");
     return UWS_OK;
 }

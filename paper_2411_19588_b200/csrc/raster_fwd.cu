@@ -54,6 +54,7 @@ __device__ __forceinline__ unsigned band_mask(float ylo, float yhi) {
 // C*dy*dy term; each pixel's power is the same float expression as in K8.
 template <bool ROWS, int PX>
 __global__ void __launch_bounds__(kRasterThreads / PX, 4 * PX) k_raster_fwd(FwdArgs a) {
+    // launched serially (no pdl_entry): the per-CTA L1 invalidation costs more here
     constexpr int kThreads = kRasterThreads / PX;
     constexpr int kWarps = kThreads / 32;
     constexpr int kBandRows = kTile / kWarps;
@@ -294,7 +295,7 @@ extern "C" int uws_raster_fwd(const uws_projected* proj, const int32_t* offsets,
     a.far_plane = (float)cam->far_plane;
     a.medium = medium;
     a.out = *out;
-    k_raster_fwd<false, kFwdPx><<<a.gx * gy, kRasterThreads / kFwdPx, 0, as_stream(stream)>>>(a);
+    launch_serial(k_raster_fwd<false, kFwdPx>, dim3(a.gx * gy), dim3(kRasterThreads / kFwdPx), 0, as_stream(stream), a);
     UWS_CHECK_LAUNCH("k_raster_fwd");
     return UWS_OK;
 }
@@ -323,7 +324,7 @@ extern "C" int uws_raster_fwd_rows(const uws_projected* proj, const int32_t* row
     a.far_plane = (float)cam->far_plane;
     a.medium = medium;
     a.out = *out;
-    k_raster_fwd<true, kFwdPx><<<a.gx * gy, kRasterThreads / kFwdPx, 0, as_stream(stream)>>>(a);
+    launch_serial(k_raster_fwd<true, kFwdPx>, dim3(a.gx * gy), dim3(kRasterThreads / kFwdPx), 0, as_stream(stream), a);
     UWS_CHECK_LAUNCH("k_raster_fwd_rows");
     return UWS_OK;
 }

@@ -62,3 +62,25 @@ def test_struct_layouts_match_header():
     assert ctypes.sizeof(_lib.ProjectedC) == 8 * 8
     assert ctypes.sizeof(_lib.RasterOutC) == 11 * 8 + 8  # 11 pointers, int32 cap + padding
     assert ctypes.sizeof(_lib.AdamParamsC) == 45 * 8
+
+
+def test_pdl_launched_kernels_wait_first():
+    """Every kernel launched with programmatic dependent launch (launch(...)) starts
+    with pdl_entry() -- a PDL-launched kernel that does not wait could read its
+    predecessor's outputs early -- and kernels launched serially need not."""
+    import glob
+    import re
+    src = ""
+    for f in sorted(glob.glob(os.path.join(ROOT, "paper_2411_19588_b200", "csrc", "*.cu*"))):
+        src += open(f).read() + "\n"
+    launched = {k for k in re.findall(r"[^_\w]launch\((?:\w+::)*(\w+)", src) if k.startswith("k_")}
+    assert len(launched) >= 15
+    bodies = {}
+    for m in re.finditer(r"__global__\s+void\s+(?:__launch_bounds__\([^)]*\)\s*)?(\w+)\s*\([^;{]*?\)\s*\{",
+                         src, flags=re.S):
+        bodies.setdefault(m.group(1), []).append(src[m.end():m.end() + 200])
+    for name in launched:
+        assert name in bodies, name
+        for b in bodies[name]:
+            first = b.strip().split(";")[0]
+            assert first == "pdl_entry()", (name, first)
