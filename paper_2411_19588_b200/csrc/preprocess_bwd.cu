@@ -19,7 +19,7 @@ namespace {
 constexpr int kThreads = 128;
 
 template <bool ACC>  // add into the gradient buffer (else store: it is known to be zero)
-__global__ void __launch_bounds__(kThreads, 6) k_preprocess_bwd(uws_cloud cl, uws_camera cam,
+__global__ void __launch_bounds__(kThreads, 5) k_preprocess_bwd(uws_cloud cl, uws_camera cam,
                                                              const int32_t* __restrict__ src_index,
                                                              const double* __restrict__ exact,
                                                              const int32_t* __restrict__ k_dev,
