@@ -139,12 +139,12 @@ __global__ void __launch_bounds__(kThreads, MINB) k_raster_bwd(BwdArgs a) {
             maxl = max(maxl, mylast[p]);
             if (a.medium) {
                 const float d = a.depth[pix];
-                const float z = 2.0f / (1.0f + expf(-(float)kLogisticRate * d)) - 1.0f;
+                const float z = 2.0f / (1.0f + __expf(-(float)kLogisticRate * d)) - 1.0f;
 #pragma unroll
                 for (int ch = 0; ch < 3; ++ch) {
                     const float dl = a.dL[3 * pix + ch];
-                    const float att = expf(-a.medium[ch] * z);
-                    const float ebs = expf(-a.medium[6 + ch] * z);
+                    const float att = __expf(-a.medium[ch] * z);
+                    const float ebs = __expf(-a.medium[6 + ch] * z);
                     G[p][ch] = dl * att;
                     med[ch] += dl * a.color_clean[3 * pix + ch] * (-z) * att;   // d attenuation
                     med[3 + ch] += dl * (1.0f - ebs);                            // d water_color

@@ -255,11 +255,11 @@ __global__ void __launch_bounds__(kRasterThreads / PX, 4 * PX) k_raster_fwd(FwdA
             continue;
         }
         // underwater epilogue: z = logistic(depth); C*exp(-Bd z) + Binf (1 - exp(-Bb z))
-        const float z = 2.0f / (1.0f + expf(-(float)kLogisticRate * depth)) - 1.0f;
+        const float z = 2.0f / (1.0f + __expf(-(float)kLogisticRate * depth)) - 1.0f;
 #pragma unroll
         for (int ch = 0; ch < 3; ++ch) {
-            const float att = expf(-a.medium[ch] * z);
-            const float bs = a.medium[3 + ch] * (1.0f - expf(-a.medium[6 + ch] * z));
+            const float att = __expf(-a.medium[ch] * z);
+            const float bs = a.medium[3 + ch] * (1.0f - __expf(-a.medium[6 + ch] * z));
             a.out.color[3 * pix + ch] = c3[ch] * att + bs;
             a.out.color_clean[3 * pix + ch] = c3[ch];
             if (a.out.attenuation) a.out.attenuation[3 * pix + ch] = att;
