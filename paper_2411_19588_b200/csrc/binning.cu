@@ -8,10 +8,10 @@
 // produced by two levels of STABLE bucketing of the depth-sorted rows, so
 // every tile entry is written exactly once and no E-sized key is ever read
 // back:
-//   0. stable order of the K visible rows by the bit pattern of their float64
-//      depth (positive doubles order like their bits; rows are in source
-//      order, so stability yields the source-index tie-break): radix sort of
-//      the high words + run fix-up (depth_sort.cuh);
+//   0. order of the K visible rows by (bit pattern of their float64 depth,
+//      row) -- positive doubles order like their bits, and the row is the
+//      reference's source-index tie-break: the high words are bucketed, then
+//      every bucket is sorted (depth_bucket.cuh);
 //   1. rank order -> tile-ROW lists (kBand = 1 tile row per band): each
 //      Gaussian is appended, in rank order, to the list of every tile row its
 //      rectangle touches, as an 8-byte item (row, column span).  The training
@@ -29,8 +29,7 @@
 // entries in shared memory so each tile run leaves the SM as coalesced stores.
 #include <algorithm>
 
-#include "depth_sort.cuh"
-#include "radix.cuh"
+#include "depth_bucket.cuh"
 
 namespace uws {
 namespace {
@@ -568,34 +567,41 @@ __global__ void __launch_bounds__(kThreads) k_cell_scatter(const uint2* __restri
 // workspace plans
 // ---------------------------------------------------------------------------
 struct CountPlan {
-    uint32_t* keys_hi;            // high words of the depth bits (sort input)
-    uint32_t* keys_hi_sorted;
-    uint32_t* sorted_rows;
-    uint32_t* long_cnt;           // [0] runs of equal high words longer than kShortRun, [1] > 32
-    uint32_t* long_list;
-    uint32_t* huge_list;
+    uint32_t* keys_hi;            // high words of the depth bits
+    uint32_t* sorted_rows;        // rows in (depth, row) order
+    uint32_t* tmp;                // scratch rows (long-bucket counting sort)
+    depth_bucket::Meta* meta;     // -- zeroed per call: meta, scan status, bucket counts --
+    unsigned* bticket;
+    unsigned long long* bstat;
+    uint32_t* bcount;             // [kBuckets]
+    uint32_t* bstart;             // [kBuckets] starts, then ends
+    uint32_t* wlist;              // buckets sorted by a warp / by a CTA
+    uint32_t* clist;
     uint32_t* m_band;             // [nbands][nblk_r] counts, scanned in place
     unsigned long long* rstat;    // look-back status of the band scan (row-list path)
     unsigned* rticket;
-    radix::Plan<uint32_t> rs;
     uint32_t nblk_r;
 };
 
-constexpr int kDepthPasses = 4;  // 8-bit digits of the depth's high word
+constexpr uint32_t kBucketScanTiles = depth_bucket::kBuckets / (kThreads * kScanIpt);
+static_assert(depth_bucket::kBuckets % (kThreads * kScanIpt) == 0, "bucket scan tiling");
 
 void plan_count(Workspace& ws, uint32_t k, int nbands, CountPlan& p) {
     const uint32_t kk = k > 0 ? k : 1;
     p.nblk_r = (uint32_t)ceil_div(kk, kBlockItems);
     p.keys_hi = ws.take<uint32_t>(kk);
-    p.keys_hi_sorted = ws.take<uint32_t>(kk);
     p.sorted_rows = ws.take<uint32_t>(kk);
-    p.long_cnt = ws.take<uint32_t>(2);
-    p.long_list = ws.take<uint32_t>(kk / (depth_sort::kShortRun + 1) + 1);
-    p.huge_list = ws.take<uint32_t>(kk / (depth_sort::kWarpRun + 1) + 1);
+    p.tmp = ws.take<uint32_t>(kk);
+    p.meta = ws.take<depth_bucket::Meta>(1);
+    p.bticket = ws.take<unsigned>(1);
+    p.bstat = ws.take<unsigned long long>(kBucketScanTiles);
+    p.bcount = ws.take<uint32_t>(depth_bucket::kBuckets);
+    p.bstart = ws.take<uint32_t>(depth_bucket::kBuckets);
+    p.wlist = ws.take<uint32_t>(kk / (depth_bucket::kThreadRun + 1) + 1);
+    p.clist = ws.take<uint32_t>(kk / 33 + 1);
     p.m_band = ws.take<uint32_t>((size_t)nbands * p.nblk_r);
     p.rstat = ws.take<unsigned long long>(ceil_div((size_t)nbands * p.nblk_r, kThreads * kScanIpt));
     p.rticket = ws.take<unsigned>(1);
-    radix::plan<uint32_t>(ws, kk, kDepthPasses, p.rs);
 }
 
 struct EmitPlan {
@@ -668,24 +674,32 @@ extern "C" int uws_bin_count(const uws_projected* proj, int64_t k_cap, const uws
     UWS_REQUIRE(ws.ok(), "uws_bin_count: workspace too small");
     const uint32_t kc = (uint32_t)k_cap;
     const uint32_t* k_dev = (const uint32_t*)proj->num_visible;
-    // 0. stable order of the rows by (float64 depth bits, row): radix sort of the
-    //    high words (4 passes), then the runs of equal high words by the low word
+    // 0. order of the rows by (float64 depth bits, row): bucket the high words,
+    //    then sort each bucket (depth_bucket.cuh)
     const uint64_t* dbits = (const uint64_t*)proj->depth;
-    UWS_CUDA(zero_async(p.rs.hist, p.rs.meta_bytes, st));
-    launch(depth_sort::k_depth_hi, dim3((unsigned)ceil_div(kc, 256)), dim3(256), 0, st, dbits, k_dev, kc, p.keys_hi,
-                                                                       p.long_cnt, p.rs.neg_min);
-    UWS_CHECK_LAUNCH("k_depth_hi");
-    UWS_CUDA(radix::sort_pairs<uint32_t>(p.rs, p.keys_hi, nullptr, p.keys_hi_sorted, p.sorted_rows,
-                                         kc, k_dev, 0, st, /*meta_zeroed=*/true, /*relative=*/true));
-    launch(depth_sort::k_tie_fix, dim3((unsigned)ceil_div(kc, 256)), dim3(256), 0, st, 
-        p.keys_hi_sorted, p.sorted_rows, dbits, k_dev, kc, p.long_cnt, p.long_list);
-    UWS_CHECK_LAUNCH("k_tie_fix");
-    launch(depth_sort::k_tie_fix_warp, dim3(148), dim3(256), 0, st, p.keys_hi_sorted, p.sorted_rows, dbits, k_dev,
-                                                    kc, p.long_cnt, p.long_list, p.huge_list);
-    UWS_CHECK_LAUNCH("k_tie_fix_warp");
-    launch(depth_sort::k_tie_fix_long, dim3(32), dim3(depth_sort::kLongThreads), 0, st, 
-        p.keys_hi_sorted, p.sorted_rows, dbits, k_dev, kc, p.long_cnt, p.huge_list, p.rs.v_tmp);
-    UWS_CHECK_LAUNCH("k_tie_fix_long");
+    namespace db = depth_bucket;
+    const unsigned kb = (unsigned)ceil_div(kc, 256);
+    UWS_CUDA(zero_async(p.meta, (char*)(p.bcount + db::kBuckets) - (char*)p.meta, st));
+    launch(db::k_hi_minmax, dim3(kb), dim3(256), 0, st, dbits, k_dev, kc, p.keys_hi, p.meta);
+    UWS_CHECK_LAUNCH("k_hi_minmax");
+    launch(db::k_bucket_count, dim3(kb), dim3(256), 0, st, (const uint32_t*)p.keys_hi, k_dev, kc,
+           (const db::Meta*)p.meta, p.bcount);
+    UWS_CHECK_LAUNCH("k_bucket_count");
+    launch(k_scan_u32, dim3(kBucketScanTiles), dim3(kThreads), 0, st, (const uint32_t*)p.bcount,
+           p.bstart, db::kBuckets, (uint32_t*)nullptr, p.bstat, p.bticket);
+    UWS_CHECK_LAUNCH("k_scan_u32");
+    launch(db::k_bucket_scatter, dim3(kb), dim3(256), 0, st, (const uint32_t*)p.keys_hi, k_dev, kc,
+           (const db::Meta*)p.meta, p.bstart, p.sorted_rows);
+    UWS_CHECK_LAUNCH("k_bucket_scatter");
+    launch(db::k_bucket_fix, dim3(db::kBuckets / 256), dim3(256), 0, st, (const uint32_t*)p.bstart,
+           dbits, p.sorted_rows, p.meta, p.wlist, p.clist);
+    UWS_CHECK_LAUNCH("k_bucket_fix");
+    launch(db::k_bucket_warp, dim3(148), dim3(256), 0, st, (const uint32_t*)p.bstart, dbits,
+           p.sorted_rows, (const db::Meta*)p.meta, (const uint32_t*)p.wlist);
+    UWS_CHECK_LAUNCH("k_bucket_warp");
+    launch(db::k_bucket_cta, dim3(64), dim3(db::kCtaThreads), 0, st, (const uint32_t*)p.bstart, dbits,
+           p.sorted_rows, (const db::Meta*)p.meta, (const uint32_t*)p.clist, p.tmp);
+    UWS_CHECK_LAUNCH("k_bucket_cta");
     // 1a. per-block band histograms + totals (E entries, S band items)
     launch(k_band_count, dim3(p.nblk_r), dim3(kThreads), 0, st, p.sorted_rows, (const short4*)proj->rect,
                                                 proj->num_visible, nbands, p.nblk_r, p.m_band,

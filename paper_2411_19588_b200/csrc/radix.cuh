@@ -9,9 +9,7 @@
 // Passes whose digit is the same for every key are identity permutations; the
 // histogram shows them before any pass runs, so their kernels exit at once and
 // the remaining passes pick their ping-pong buffers from the per-pass flags so
-// that the last executed pass still lands in the output.  Optionally the keys
-// are first made relative to their minimum (a producer-maintained ~min word),
-// which turns the high digits of clustered keys (depths of one scene) trivial.
+// that the last executed pass still lands in the output.
 #pragma once
 
 #include "scan.cuh"
@@ -50,12 +48,10 @@ __device__ __forceinline__ uint32_t dev_count(const uint32_t* n_dev, uint32_t n_
     return n < n_cap ? n : n_cap;
 }
 
-// keys are rewritten in place as key - min when neg_min (holding ~min) is given
 template <typename K>
-__global__ void __launch_bounds__(kThreads) k_histogram(K* __restrict__ keys, uint32_t n_cap,
+__global__ void __launch_bounds__(kThreads) k_histogram(const K* __restrict__ keys, uint32_t n_cap,
                                                        const uint32_t* n_dev, int begin_bit,
-                                                       int passes, uint32_t* __restrict__ hist,
-                                                       const K* __restrict__ neg_min) {
+                                                       int passes, uint32_t* __restrict__ hist) {
     pdl_entry();
     __shared__ uint32_t h[8 * kBins];
     for (int i = threadIdx.x; i < passes * kBins; i += kThreads) h[i] = 0;
@@ -63,15 +59,10 @@ __global__ void __launch_bounds__(kThreads) k_histogram(K* __restrict__ keys, ui
     const uint32_t n = dev_count(n_dev, n_cap);
     const unsigned lt = lanemask_lt();
     const uint32_t stride = gridDim.x * kThreads;
-    const K kmin = neg_min ? K(~*neg_min) : K(0);
     for (uint32_t base = blockIdx.x * kThreads; base < n; base += stride) {
         uint32_t i = base + threadIdx.x;
         bool valid = i < n;
         K key = valid ? keys[i] : K(0);
-        if (neg_min && valid) {
-            key -= kmin;
-            keys[i] = key;
-        }
         const unsigned vmask = __ballot_sync(0xffffffffu, valid);
         if (vmask == 0) continue;  // whole warp past the end (lane 0 would index bin 256)
         for (int p = 0; p < passes; ++p) {
@@ -260,14 +251,13 @@ __global__ void __launch_bounds__(kThreads) k_onesweep(PassArgs<K> pa, uint32_t 
     }
 }
 
-// Workspace for sorting n pairs over `passes` 8-bit digits.  hist .. neg_min is
+// Workspace for sorting n pairs over `passes` 8-bit digits.  hist .. trivial is
 // one contiguous block ("meta", meta_bytes long) that must be zero when a sort starts.
 template <typename K>
 struct Plan {
     K* k_tmp;
     uint32_t* v_tmp;
     uint32_t *hist, *status, *tickets, *trivial;
-    K* neg_min;  // ~min of the keys, for producers that maintain it (atomicMax)
     size_t meta_bytes;
     int passes;
 };
@@ -282,29 +272,23 @@ inline void plan(Workspace& ws, uint32_t n, int passes, Plan<K>& p) {
     p.status = ws.take<uint32_t>((size_t)passes * tiles * kBins);
     p.tickets = ws.take<uint32_t>(passes);
     p.trivial = ws.take<uint32_t>(passes);
-    p.neg_min = ws.take<K>(1);
-    p.meta_bytes = (size_t)((char*)(p.neg_min + 1) - (char*)p.hist);
+    p.meta_bytes = (size_t)((char*)(p.trivial + passes) - (char*)p.hist);
 }
 
 // Sort (keys_in, vals_in or identity if NULL) by bits [begin_bit, begin_bit+8*passes).
 // n_cap sizes the grids; the actual count is *n_dev when n_dev != NULL.
-// The result lands in (keys_out, vals_out); vals_in is not modified, nor is keys_in
-// unless relative = true: then keys_in holds ~min in *p.neg_min (written after the
-// caller zeroed the meta block, meta_zeroed = true) and is rewritten as key - min.
+// The result lands in (keys_out, vals_out); keys_in/vals_in are not modified.
 template <typename K>
-inline cudaError_t sort_pairs(const Plan<K>& p, K* keys_in, const uint32_t* vals_in, K* keys_out,
-                              uint32_t* vals_out, uint32_t n_cap, const uint32_t* n_dev,
-                              int begin_bit, cudaStream_t st, bool meta_zeroed = false,
-                              bool relative = false) {
+inline cudaError_t sort_pairs(const Plan<K>& p, const K* keys_in, const uint32_t* vals_in,
+                              K* keys_out, uint32_t* vals_out, uint32_t n_cap,
+                              const uint32_t* n_dev, int begin_bit, cudaStream_t st) {
     if (n_cap == 0) return cudaSuccess;
-    if (!meta_zeroed) {
-        cudaError_t e = zero_async(p.hist, p.meta_bytes, st);
-        if (e != cudaSuccess) return e;
-    }
+    cudaError_t e = zero_async(p.hist, p.meta_bytes, st);
+    if (e != cudaSuccess) return e;
     int hist_blocks = (int)ceil_div(n_cap, kThreads * 8);
     if (hist_blocks > 1184) hist_blocks = 1184;
     launch(k_histogram<K>, dim3(hist_blocks), dim3(kThreads), 0, st, keys_in, n_cap, n_dev, begin_bit, p.passes,
-                                                     p.hist, relative ? p.neg_min : nullptr);
+                                                     p.hist);
     launch(k_scan_hist, dim3(p.passes), dim3(kBins), 0, st, p.hist, p.passes, n_dev, n_cap, p.trivial);
     const int tiles = (int)ceil_div(n_cap, tile_items<K>());
     PassArgs<K> pa{keys_in, vals_in, keys_out, vals_out, p.k_tmp, p.v_tmp, p.trivial, 0, p.passes};

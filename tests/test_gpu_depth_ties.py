@@ -81,3 +81,32 @@ def test_depths_across_the_whole_near_far_range(near, far):
     cam = uw.Camera(width=96, height=80, fx=90.0, fy=90.0, cx=48.0, cy=40.0,
                     R=np.eye(3), t=np.zeros(3), near=near, far=far)
     _check(cloud, cam)
+
+
+def test_one_huge_bucket_of_equal_depths():
+    # > 2048 rows in one depth bucket: the stable 12-pass counting sort of k_bucket_cta
+    cam = uw.Camera(width=128, height=96, fx=120.0, fy=120.0, cx=64.0, cy=48.0,
+                    R=np.eye(3), t=np.zeros(3))
+    longest, _ = _check(_cloud(6000, 6.0, 0.0, seed=4), cam)
+    assert longest > 2048
+
+
+def test_buckets_of_every_size_class():
+    # depths quantised to a few float32 values: buckets of 2..8 (thread), 9..32 (warp),
+    # 33..2048 (CTA bitonic) rows side by side
+    rng = np.random.default_rng(8)
+    sizes = [2, 5, 8, 9, 20, 32, 33, 100, 700, 1500]
+    z = np.concatenate([np.full(s, 5.0 + 0.25 * k) for k, s in enumerate(sizes)])
+    n = z.size
+    xy = rng.uniform(-0.3, 0.3, (n, 2)) * z[:, None]
+    q = rng.normal(size=(n, 4))
+    q /= np.linalg.norm(q, axis=1, keepdims=True)
+    perm = rng.permutation(n)
+    cloud = uw.GaussianCloud(
+        positions=np.concatenate([xy, z[:, None]], axis=1)[perm].astype(np.float32),
+        log_scales=np.full((n, 3), np.log(0.02), dtype=np.float32),
+        rotations=q.astype(np.float32), sh_coeffs=rng.normal(0, 0.5, (n, 1, 3)).astype(np.float32),
+        opacity_logits=rng.uniform(-1, 2, n).astype(np.float32))
+    cam = uw.Camera(width=96, height=80, fx=90.0, fy=90.0, cx=48.0, cy=40.0,
+                    R=np.eye(3), t=np.zeros(3))
+    _check(cloud, cam)
