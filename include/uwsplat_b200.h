@@ -189,6 +189,9 @@ int uws_loss_fwd_bwd(const float* rendered, const float* gt, int32_t h, int32_t 
 int uws_raster_bwd(const uws_projected* proj, const int32_t* offsets, const int32_t* entries,
                    const uws_camera* cam, const float* medium, const uws_raster_out* fwd,
                    const float* dL_dC, float* screen_grads, double* medium_acc, void* stream);
+/* _rows variant: reads each tile's consumed prefix from fwd->tile_rows when the
+ * forward stored it (tile_rows != NULL and the prefix fits the cap), else
+ * filters the row lists again. */
 int uws_raster_bwd_rows(const uws_projected* proj, const int32_t* row_start,
                         const void* row_items, const uws_camera* cam, const float* medium,
                         const uws_raster_out* fwd, const float* dL_dC, float* screen_grads,
