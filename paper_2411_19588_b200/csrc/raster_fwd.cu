@@ -183,6 +183,7 @@ __global__ void __launch_bounds__(kRasterThreads / PX, 4 * PX) k_raster_fwd(FwdA
                 const float4 p1 = lds128(ra + 16u);
                 const float dy = fy - p0.y;
                 const float qy = p1.x * dy * dy;
+                const float4 c = lds128(ra + 32u);
 #pragma unroll
                 for (int j = 0; j < PX; ++j) {
                     const float dx = fx[j] - p0.x;
@@ -193,10 +194,9 @@ __global__ void __launch_bounds__(kRasterThreads / PX, 4 * PX) k_raster_fwd(FwdA
                         if (power < p1.z)  // near the 1/255 floor (rare): float64 in the guard band
                             take = araw >= kFloorHi ||
                                    (araw >= kFloorLo &&
-                                    alpha_raw_f64_cold(a.splat, a.exact, __float_as_int(lds128(ra + 32u).w),
+                                    alpha_raw_f64_cold(a.splat, a.exact, __float_as_int(c.w),
                                                        ox + lx0 + j, py) >= kFloor);
                         if (take) {
-                            const float4 c = lds128(ra + 32u);
                             const float alpha = fminf(araw, kClampF);
                             const float w = alpha * T[j];
                             cr[j] = fmaf(w, c.x, cr[j]);
