@@ -20,6 +20,7 @@ same workload, extrapolated to a full step.
 from __future__ import annotations
 
 import argparse
+import re
 import glob
 import json
 import os
@@ -75,7 +76,12 @@ def kernel_traffic(stage):
             "uws_adam_step": "k_adam_cloud", "uws_loss_fwd_bwd": "k_ssim"}.get(stage)
     if kern is None:
         return None
-    caps = sorted(glob.glob(os.path.join(ROOT, "profiles", "r*", "kernel_traffic*.json")))
+    def version(path):  # (round, capture) numerically: r01/kernel_traffic_v10 after _v9
+        nums = [int(x) for x in re.findall(r"\d+", os.path.relpath(path, ROOT))]
+        return nums
+
+    caps = sorted(glob.glob(os.path.join(ROOT, "profiles", "r*", "kernel_traffic*.json")),
+                  key=version)
     if not caps:
         return None
     try:
