@@ -229,6 +229,15 @@ int uws_adam_step(float* params, float* exp_avg, float* exp_avg_sq, float* grads
                   float* medium_params, float* medium_exp_avg, float* medium_exp_avg_sq,
                   float* medium_grads, const uws_adam_params* hp, const float* skip,
                   float* grad_accum, int32_t* obs_count, int32_t zero_grads, void* stream);
+/* The cloud part of uws_adam_step for the float4 groups [group_begin, group_end)
+ * of the 14n parameter scalars (even n, 16-byte aligned buffers), so an update
+ * can follow a gradient all-reduce chunk by chunk; the densification statistics
+ * of Gaussian t are folded by the range holding group t.  The medium part is
+ * uws_adam_step with n = 0. */
+int uws_adam_step_range(float* params, float* exp_avg, float* exp_avg_sq, float* grads, int64_t n,
+                        const uws_adam_params* hp, const float* skip, float* grad_accum,
+                        int32_t* obs_count, int32_t zero_grads, int64_t group_begin,
+                        int64_t group_end, void* stream);
 
 /* ---- densification (replaces optim.densify_and_prune :132-198 and
  *      reset_opacities :201-207).  Two phases around one host read: classify

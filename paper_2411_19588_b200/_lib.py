@@ -94,6 +94,9 @@ _SIGS = {
     "uws_adam_step": (c_int, [c_void_p, c_void_p, c_void_p, c_void_p, c_int64, c_void_p,
                               c_void_p, c_void_p, c_void_p, POINTER(AdamParamsC), c_void_p,
                               c_void_p, c_void_p, c_int32, c_void_p]),
+    "uws_adam_step_range": (c_int, [c_void_p, c_void_p, c_void_p, c_void_p, c_int64,
+                                    POINTER(AdamParamsC), c_void_p, c_void_p, c_void_p, c_int32,
+                                    c_int64, c_int64, c_void_p]),
     "uws_densify_workspace_size": (c_int, [c_int64, POINTER(c_size_t)]),
     "uws_densify_classify": (c_int, [c_void_p, c_int64, c_void_p, c_void_p, c_double, c_double,
                                      c_double, c_void_p, c_void_p, c_size_t, c_void_p]),

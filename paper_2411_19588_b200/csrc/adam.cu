@@ -169,11 +169,12 @@ __global__ void __launch_bounds__(kThreads, 4) k_adam_cloud4(float* __restrict__
                                                              float* __restrict__ M,
                                                              float* __restrict__ V,
                                                              float* __restrict__ Gr, int64_t n,
-                                                             uws_adam_params hp, AdamCtl ctl) {
+                                                             uws_adam_params hp, AdamCtl ctl,
+                                                             int64_t g_begin, int64_t g_end) {
     // launched serially (no pdl_entry): the per-CTA L1 invalidation costs more here
-    const int64_t t = (int64_t)blockIdx.x * kThreads + threadIdx.x;
-    const int64_t groups = 14 * n / 4;
-    if (t >= groups) return;
+    // groups [g_begin, g_end) of the 14n/4 (all of them for a whole step)
+    const int64_t t = g_begin + (int64_t)blockIdx.x * kThreads + threadIdx.x;
+    if (t >= g_end) return;
     const bool skip = ctl.skip && *ctl.skip > 0.0f;
     if (t < n) {
         if (!skip && ctl.grad_accum) {
@@ -281,8 +282,9 @@ extern "C" int uws_adam_step(float* params, float* exp_avg, float* exp_avg_sq, f
                              ((uintptr_t)params | (uintptr_t)exp_avg | (uintptr_t)exp_avg_sq |
                               (uintptr_t)grads) % 16 == 0;
         if (aligned) {
-            launch_serial(k_adam_cloud4, dim3((unsigned)ceil_div(14 * n / 4, kThreads)), dim3(kThreads), 0, st, 
-                params, exp_avg, exp_avg_sq, grads, n, *hp, ctl);
+            launch_serial(k_adam_cloud4, dim3((unsigned)ceil_div(14 * n / 4, kThreads)),
+                          dim3(kThreads), 0, st, params, exp_avg, exp_avg_sq, grads, n, *hp, ctl,
+                          (int64_t)0, 14 * n / 4);
             UWS_CHECK_LAUNCH("k_adam_cloud4");
         } else {
             constexpr int kEpt = 2;
@@ -300,5 +302,27 @@ extern "C" int uws_adam_step(float* params, float* exp_avg, float* exp_avg_sq, f
         UWS_CUDA(zero_async(medium_grads, 9 * sizeof(float), st));
         UWS_CUDA(zero_async(medium_grads + 10, 6 * sizeof(float), st));
     }
+    return UWS_OK;
+}
+
+extern "C" int uws_adam_step_range(float* params, float* exp_avg, float* exp_avg_sq, float* grads,
+                                   int64_t n, const uws_adam_params* hp, const float* skip,
+                                   float* grad_accum, int32_t* obs_count, int32_t zero_grads,
+                                   int64_t group_begin, int64_t group_end, void* stream) {
+    UWS_REQUIRE(hp != nullptr && n > 0 && n % 2 == 0, "uws_adam_step_range: needs an even n > 0");
+    UWS_REQUIRE(params && exp_avg && exp_avg_sq && grads, "uws_adam_step_range: null cloud buffer");
+    UWS_REQUIRE(((uintptr_t)params | (uintptr_t)exp_avg | (uintptr_t)exp_avg_sq |
+                 (uintptr_t)grads) % 16 == 0,
+                "uws_adam_step_range: buffers must be 16-byte aligned");
+    UWS_REQUIRE((grad_accum == nullptr) == (obs_count == nullptr),
+                "uws_adam_step_range: grad_accum and obs_count go together");
+    UWS_REQUIRE(0 <= group_begin && group_begin <= group_end && group_end <= 14 * n / 4,
+                "uws_adam_step_range: group range out of bounds");
+    if (group_end == group_begin) return UWS_OK;
+    AdamCtl ctl{skip, grad_accum, obs_count, zero_grads};
+    launch_serial(k_adam_cloud4, dim3((unsigned)ceil_div(group_end - group_begin, kThreads)),
+                  dim3(kThreads), 0, as_stream(stream), params, exp_avg, exp_avg_sq, grads, n, *hp,
+                  ctl, group_begin, group_end);
+    UWS_CHECK_LAUNCH("k_adam_cloud4");
     return UWS_OK;
 }

@@ -38,7 +38,7 @@ import torch
 from . import _lib
 from .backward import GradientBuffer
 from .losses import total_loss_device
-from .optim import OptimConfig, apply_gradients_device, rollback_steps
+from .optim import OptimConfig, apply_gradients_device, range_chunks, rollback_steps
 from .projection import ProjectedCloud, preprocess_into
 from .rasterizer import RenderOutput, RowLists, _alloc_output
 from .scene import Camera, TrainState
@@ -236,18 +236,41 @@ class StepEngine:
         cur.wait_event(slot.copied)
         for i, (cam, gt) in enumerate(slot.views):
             self._view(cam, gt, slot.stats, i)
+        chunks = None
         if self.dist is not None and self.world > 1:
-            # one NCCL all-reduce of [grads | medium | skip counter | pad]
-            self.dist.all_reduce(self.grads.flat, group=self.group)
+            chunks = self._all_reduce_gradients()
         # the skip counter is read by the Adam launch (and kept while non-zero): keep a copy
         slot.stats[-1:].copy_(self.grads.nonfinite)
         saved = self.state.iteration
         self.state.iteration = slot.iteration
-        apply_gradients_device(self.state, self.grads, self.cfg, self.spatial_scale)
+        apply_gradients_device(self.state, self.grads, self.cfg, self.spatial_scale, chunks=chunks)
         self.state.iteration = saved
         slot.host.copy_(slot.stats, non_blocking=True)
         slot.done.record(cur)
         slot.free.record(cur)
+
+    # gradient all-reduce split against the cloud update (multi-GPU)
+    ALLREDUCE_PARTS = 4
+
+    def _all_reduce_gradients(self):
+        """Sum the flat gradient buffer over the ranks.  The medium/skip tail and the
+        densification statistics are reduced first (the medium update and the skip
+        test read them); the 14n parameter gradients follow in ALLREDUCE_PARTS
+        asynchronous NCCL all-reduces, and each range of the Adam update waits only
+        for its own part, so the update of range c overlaps the reduction of c+1.
+        Returns the chunk list for ``apply_gradients_device`` (None: one blocking
+        all-reduce, then the single launch)."""
+        flat, n, d, g = self.grads.flat, self.n, self.dist, self.group
+        parts = range_chunks(self.state, self.grads, self.ALLREDUCE_PARTS)
+        if parts is None:
+            d.all_reduce(flat, group=g)
+            return None
+        head = [d.all_reduce(flat[16 * n:], group=g, async_op=True),
+                d.all_reduce(flat[14 * n:16 * n], group=g, async_op=True)]
+        works = [d.all_reduce(flat[4 * g0:4 * g1], group=g, async_op=True) for g0, g1 in parts]
+        for w in head:
+            w.wait()
+        return [(g0, g1, w.wait) for (g0, g1), w in zip(parts, works)]
 
     def _read(self, slot: "_Slot"):
         slot.done.synchronize()

@@ -134,20 +134,47 @@ def apply_gradients(state: TrainState, buf, cfg: OptimConfig, spatial_scale: flo
 
 
 def apply_gradients_device(state: TrainState, buf, cfg: OptimConfig, spatial_scale: float = 1.0,
-                           zero_grads: bool = True) -> _lib.AdamParamsC:
+                           zero_grads: bool = True, chunks=None) -> _lib.AdamParamsC:
     """Engine form: skip on device when buf.nonfinite > 0, accumulate the
     densification statistics and leave ``buf`` zeroed.  Advances the step
     counters; the caller rolls them back (``rollback_steps``) if the device
-    reported a skip."""
+    reported a skip.
+
+    ``chunks`` (optional, see ``range_chunks``): [(group_begin, group_end, wait)]
+    covering the cloud's float4 groups; the medium update runs first, then each
+    range after its ``wait()`` (e.g. the all-reduce of that part of the buffer),
+    with results identical to the single launch."""
     cloud, medium = state.cloud, state.medium
     hp = adam_hparams(state, cfg, spatial_scale)
+    st = _lib.stream_handle()
+    zg = 1 if zero_grads else 0
+    n = len(cloud) if chunks is None else 0
     _lib.call("uws_adam_step", _lib.ptr(cloud.flat), _lib.ptr(state.exp_avg),
-              _lib.ptr(state.exp_avg_sq), _lib.ptr(buf.flat), len(cloud), _lib.ptr(medium.flat),
+              _lib.ptr(state.exp_avg_sq), _lib.ptr(buf.flat), n, _lib.ptr(medium.flat),
               _lib.ptr(state.medium_exp_avg), _lib.ptr(state.medium_exp_avg_sq),
               _lib.ptr(buf.medium), ctypes.byref(hp), _lib.ptr(buf.nonfinite),
-              _lib.ptr(state.grad_accum), _lib.ptr(state.obs_count), 1 if zero_grads else 0,
-              _lib.stream_handle())
+              _lib.ptr(state.grad_accum), _lib.ptr(state.obs_count), zg, st)
+    for g0, g1, wait in chunks or ():
+        if wait is not None:
+            wait()
+        _lib.call("uws_adam_step_range", _lib.ptr(cloud.flat), _lib.ptr(state.exp_avg),
+                  _lib.ptr(state.exp_avg_sq), _lib.ptr(buf.flat), len(cloud), ctypes.byref(hp),
+                  _lib.ptr(buf.nonfinite), _lib.ptr(state.grad_accum), _lib.ptr(state.obs_count),
+                  zg, int(g0), int(g1), st)
     return hp
+
+
+def range_chunks(state: TrainState, buf, parts: int):
+    """Float4-group ranges [(g0, g1)] splitting the cloud update into ``parts``
+    launches, or None when the range form does not apply (odd n or buffers not
+    16-byte aligned: the single launch then takes its scalar path)."""
+    n = len(state.cloud)
+    ptrs = (state.cloud.flat, state.exp_avg, state.exp_avg_sq, buf.flat)
+    if n == 0 or n % 2 or any(t.data_ptr() % 16 for t in ptrs):
+        return None
+    groups = 14 * n // 4
+    parts = max(1, min(parts, groups))
+    return [(groups * c // parts, groups * (c + 1) // parts) for c in range(parts)]
 
 
 def rollback_steps(state: TrainState) -> None:

@@ -87,3 +87,54 @@ def test_shard_views_partition():
         shards = [shard_views(views, r, world) for r in range(world)]
         assert sorted(sum(shards, [])) == views
         assert {len(s) for s in shards} == {64 // world}
+
+
+def _chunked_worker(rank, world, port, q, n):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    from types import SimpleNamespace
+    from paper_2411_19588_b200.engine import StepEngine
+    gen = torch.Generator().manual_seed(100 + rank)
+    flat = torch.randn(16 * n + 16, generator=gen)
+    mine = flat.clone()
+    class Cloud:
+        flat = torch.zeros(14 * n)
+
+        def __len__(self):
+            return n
+
+    state = SimpleNamespace(cloud=Cloud(), exp_avg=torch.zeros(14 * n),
+                            exp_avg_sq=torch.zeros(14 * n))
+    fake = SimpleNamespace(grads=SimpleNamespace(flat=flat), n=n, dist=dist, group=None,
+                           state=state, ALLREDUCE_PARTS=3)
+    chunks = StepEngine._all_reduce_gradients(fake)
+    groups = []
+    for g0, g1, wait in chunks:
+        wait()
+        groups.append((g0, g1))
+    q.put((rank, mine.numpy(), flat.numpy(), groups))
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+def test_chunked_gradient_allreduce_covers_the_buffer():
+    """The engine's split all-reduce (medium/skip tail and statistics first, then the
+    parameter gradients in parts that the range-wise Adam waits for) sums every slot."""
+    n = 1000
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_chunked_worker, args=(r, 2, port, q, n)) for r in range(2)]
+    for p in procs:
+        p.start()
+    got = dict((r, (a, b, g)) for r, a, b, g in (q.get(timeout=240) for _ in range(2)))
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    total = got[0][0] + got[1][0]
+    for r in (0, 1):
+        np.testing.assert_allclose(got[r][1], total, rtol=1e-6, atol=1e-6)
+    groups = got[0][2]
+    assert groups[0][0] == 0 and groups[-1][1] == 14 * n // 4 and len(groups) == 3
+    assert all(a[1] == b[0] for a, b in zip(groups, groups[1:]))

@@ -254,3 +254,34 @@ def test_backward_from_stored_rows_matches_refiltering(name, monkeypatch):
         bufs.append(np_(uw.backward_render(out, dL, s.cloud, med, 0.1).flat).astype(np.float64))
     for a in bufs[:2]:
         assert np.abs(a - bufs[2]).max() <= 1e-5 * max(np.abs(bufs[2]).max(), 1e-30)
+
+
+@pytest.mark.parametrize("parts", [1, 3, 7])
+def test_range_update_equals_single_launch(parts):
+    """The cloud update split into group ranges (as after a chunked all-reduce) gives the
+    single launch's parameters, moments, densification statistics and zeroed buffer."""
+    from paper_2411_19588_b200.optim import apply_gradients_device, range_chunks
+    g = load("survey2k")
+    results = []
+    for chunked in (False, True):
+        s, _ = _state(g)
+        s.iteration = 7
+        n = len(s.cloud)
+        buf = uw.GradientBuffer(n, s.cloud.device)
+        gen = torch.Generator(device="cuda").manual_seed(3)
+        buf.flat[:14 * n] = torch.randn(14 * n, device="cuda", generator=gen) * 1e-3
+        buf.flat[14 * n:15 * n] = torch.rand(n, device="cuda", generator=gen)
+        buf.flat[15 * n:16 * n] = (torch.rand(n, device="cuda", generator=gen) > 0.3).float()
+        buf.flat[16 * n:16 * n + 9] = torch.randn(9, device="cuda", generator=gen) * 1e-2
+        for _ in range(2):   # second step: non-zero moments
+            chunks = None
+            if chunked:
+                chunks = [(a, b, None) for a, b in range_chunks(s, buf, parts)]
+            apply_gradients_device(s, buf, uw.OptimConfig(), 1.0, chunks=chunks)
+            buf.flat[:14 * n] = torch.randn(14 * n, device="cuda", generator=gen) * 1e-3
+            buf.flat[15 * n:16 * n] = 1.0
+        results.append([np_(t).copy() for t in (s.cloud.flat, s.exp_avg, s.exp_avg_sq,
+                                                s.grad_accum, s.obs_count, s.medium.flat,
+                                                buf.flat[14 * n:])])
+    for a, b in zip(*results):
+        np.testing.assert_array_equal(a, b)
