@@ -258,18 +258,24 @@ class StepEngine:
         test read them); the 14n parameter gradients follow in ALLREDUCE_PARTS
         asynchronous NCCL all-reduces, and each range of the Adam update waits only
         for its own part, so the update of range c overlaps the reduction of c+1.
-        Returns the chunk list for ``apply_gradients_device`` (None: one blocking
-        all-reduce, then the single launch)."""
+        Returns the chunk list for ``apply_gradients_device`` (None when the range
+        form does not apply: every part has been waited for, then the single launch)."""
         flat, n, d, g = self.grads.flat, self.n, self.dist, self.group
-        parts = range_chunks(self.state, self.grads, self.ALLREDUCE_PARTS)
-        if parts is None:
-            d.all_reduce(flat, group=g)
-            return None
+        # the same collectives on every rank (they depend on n only) ...
+        parts = [(14 * n * c // self.ALLREDUCE_PARTS // 4, 14 * n * (c + 1) // self.ALLREDUCE_PARTS // 4)
+                 for c in range(self.ALLREDUCE_PARTS)]
+        parts[-1] = (parts[-1][0], (14 * n + 3) // 4)
         head = [d.all_reduce(flat[16 * n:], group=g, async_op=True),
                 d.all_reduce(flat[14 * n:16 * n], group=g, async_op=True)]
-        works = [d.all_reduce(flat[4 * g0:4 * g1], group=g, async_op=True) for g0, g1 in parts]
+        works = [d.all_reduce(flat[4 * g0:min(4 * g1, 14 * n)], group=g, async_op=True)
+                 for g0, g1 in parts]
         for w in head:
             w.wait()
+        # ... and the range-wise update only where it applies (even n, aligned buffers)
+        if range_chunks(self.state, self.grads, 1) is None:
+            for w in works:
+                w.wait()
+            return None
         return [(g0, g1, w.wait) for (g0, g1), w in zip(parts, works)]
 
     def _read(self, slot: "_Slot"):

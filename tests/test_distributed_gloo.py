@@ -110,7 +110,7 @@ def _chunked_worker(rank, world, port, q, n):
                            state=state, ALLREDUCE_PARTS=3)
     chunks = StepEngine._all_reduce_gradients(fake)
     groups = []
-    for g0, g1, wait in chunks:
+    for g0, g1, wait in chunks or ():
         wait()
         groups.append((g0, g1))
     q.put((rank, mine.numpy(), flat.numpy(), groups))
@@ -118,10 +118,11 @@ def _chunked_worker(rank, world, port, q, n):
     dist.destroy_process_group()
 
 
-def test_chunked_gradient_allreduce_covers_the_buffer():
+@pytest.mark.parametrize("n", [1000, 1001])
+def test_chunked_gradient_allreduce_covers_the_buffer(n):
     """The engine's split all-reduce (medium/skip tail and statistics first, then the
-    parameter gradients in parts that the range-wise Adam waits for) sums every slot."""
-    n = 1000
+    parameter gradients in parts that the range-wise Adam waits for) sums every slot;
+    odd n (no range-wise update) issues the same collectives and waits for all."""
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
@@ -136,5 +137,8 @@ def test_chunked_gradient_allreduce_covers_the_buffer():
     for r in (0, 1):
         np.testing.assert_allclose(got[r][1], total, rtol=1e-6, atol=1e-6)
     groups = got[0][2]
+    if n % 2:
+        assert groups == []
+        return
     assert groups[0][0] == 0 and groups[-1][1] == 14 * n // 4 and len(groups) == 3
     assert all(a[1] == b[0] for a, b in zip(groups, groups[1:]))
