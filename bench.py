@@ -283,8 +283,8 @@ def run_gpu(args):
 
     # render FPS (BASELINE.json's second metric): the forward alone -- preprocess,
     # depth sort, tile-row lists, compositing with the medium epilogue -- per frame
-    # through StepEngine.render (one host read of the overflow flag per frame), at C3
-    # and at C5's 1M Gaussians @ 3840x2160
+    # through StepEngine.render_async (a frame stream: each frame's overflow flag is
+    # read once the next frame is queued), at C3 and at C5's 1M Gaussians @ 3840x2160
     render_fps = {}
     for name, (rw, rh) in ((("C3 1M 1920x1080", (W, H)), ("C5 1M 3840x2160", (3840, 2160)))
                            if not args.no_render_fps else ()):
@@ -298,7 +298,8 @@ def run_gpu(args):
         t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         t0.record()
         for _ in range(nfr):
-            eng.render(rcam)
+            eng.render_async(rcam)
+        eng.render_flush()
         t1.record()
         barrier()
         fms = t0.elapsed_time(t1) / nfr

@@ -96,6 +96,12 @@ class StepEngine:
         # device copies of host ground-truth images
         self._slots = [_Slot(max_views, dev) for _ in range(2)]
         self._render_stats = torch.zeros(_ST_SIZE + 2, dtype=torch.float64, device=dev)
+        # render_async: two frame records, the pending (queued, unchecked) frame
+        self._async_stats = torch.zeros(2, _ST_SIZE + 2, dtype=torch.float64, device=dev)
+        self._async_flag = torch.zeros(2, 2, dtype=torch.int32).pin_memory()
+        self._async_done = [torch.cuda.Event(), torch.cuda.Event()]
+        self._async_frames = 0
+        self._async_pending = None
         self._k = 0
         self._pending = None
         self.copy_stream = torch.cuda.Stream(device=dev)
@@ -157,6 +163,42 @@ class StepEngine:
         _lib.call("uws_raster_fwd_rows", ctypes.byref(pc), _lib.ptr(self.row_start),
                   _lib.ptr(self.row_items), ctypes.byref(cc), med, ctypes.byref(oc), st)
         return cc, pc, oc, rec
+
+    def render_async(self, cam, mode: str = "underwater") -> RenderOutput:
+        """Queue one render-only frame without waiting for it (a frame stream).
+
+        The row-list overflow flag of the PREVIOUS queued frame is read after this
+        one is queued, so the host never idles the GPU between frames.  The
+        returned buffers hold the most recent frame once ``render_flush()`` has
+        returned; if a frame overflowed its row lists, the lists are grown and
+        the most recent frame is rendered again, synchronously."""
+        cam = Camera.from_any(cam)
+        if self._pending is None:
+            self._sync_cloud()
+        k = self._async_frames % 2
+        self._async_frames += 1
+        stats = self._async_stats[k]
+        stats.zero_()
+        self._forward(cam, stats, 0, mode, train=False)
+        # the frame's overflow flag to pinned memory, behind the frame's kernels
+        self._async_flag[k].copy_(stats[_ST_OVF:_ST_OVF + 1].view(torch.int32), non_blocking=True)
+        self._async_done[k].record()
+        prev, self._async_pending = self._async_pending, (cam, mode, k)
+        self.out.mode = mode
+        if prev is not None and self._async_overflowed(prev[2]):
+            self.render_flush()
+        return self.last_render()
+
+    def render_flush(self) -> RenderOutput:
+        """Check the last queued frame (re-rendering it if its row lists overflowed)."""
+        frame, self._async_pending = self._async_pending, None
+        if frame is not None and self._async_overflowed(frame[2]):
+            return self.render(frame[0], frame[1])
+        return self.last_render()
+
+    def _async_overflowed(self, k: int) -> bool:
+        self._async_done[k].synchronize()   # waits for that frame only
+        return int(self._async_flag[k, 0]) != 0
 
     def render(self, cam, mode: str = "underwater") -> RenderOutput:
         """Render-only path (no host sync before the caller reads the image).

@@ -285,3 +285,24 @@ def test_range_update_equals_single_launch(parts):
                                                 buf.flat[14 * n:])])
     for a, b in zip(*results):
         np.testing.assert_array_equal(a, b)
+
+
+@pytest.mark.parametrize("capacity", [None, 64])
+def test_render_async_stream_matches_render(capacity):
+    """A queued frame stream (render_async + render_flush) leaves the most recent
+    frame in the output buffers, identical to a synchronous render -- also when the
+    row lists overflow and are grown mid-stream."""
+    g = load("survey2k")
+    s, cam = _state(g)
+    ref = uw.StepEngine(s, cam.width, cam.height, uw.OptimConfig())
+    want = {k: np_(v).copy() for k, v in vars(ref.render(cam)).items()
+            if isinstance(v, torch.Tensor) and k in ("color", "depth", "final_transmittance")}
+    kw = {} if capacity is None else {"entry_capacity": capacity}
+    eng = uw.StepEngine(s, cam.width, cam.height, uw.OptimConfig(), **kw)
+    other = uw.Camera.look_at((0.5, -0.2, -1.0), (0, 0, 5), width=cam.width, height=cam.height,
+                              fx=cam.fx, fy=cam.fy)
+    for c in (other, cam, other, cam):
+        eng.render_async(c)
+    out = eng.render_flush()
+    for k, v in want.items():
+        np.testing.assert_array_equal(np_(getattr(out, k)), v)
