@@ -19,7 +19,8 @@ for n, (W, H) in ((3_000_000, (1920, 1080)), (1_000_000, (3840, 2160)), (5_000_0
     ms = t0.elapsed_time(t1) / 5
     f0 = torch.cuda.Event(enable_timing=True); f1 = torch.cuda.Event(enable_timing=True)
     eng.render(cam); torch.cuda.synchronize(); f0.record()
-    for _ in range(5): eng.render(cam)
+    for _ in range(5): eng.render_async(cam)
+    eng.render_flush()
     f1.record(); torch.cuda.synchronize()
     print(f"N={n} {W}x{H}: step {ms:.3f} ms ({W*H/ms/1e3:.0f} Mpix/s) reruns={r.reruns} skipped={last.skipped} "
           f"loss={last.total:.4f} render {f0.elapsed_time(f1)/5:.3f} ms, mem {torch.cuda.max_memory_allocated()/1e9:.1f} GB", flush=True)
