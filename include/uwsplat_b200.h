@@ -17,7 +17,7 @@
  *   - Every call returns UWS_OK (0) or an error code and records a message
  *     retrievable with uws_last_error() (thread-local).
  *   - Per-Gaussian parameters are float32 structure-of-arrays exactly as the
- *     reference GaussianCloud stores them (scene.py:123-147).
+ *     reference GaussianCloud stores them (scene.py:90-147).
  */
 #ifndef UWSPLAT_B200_H
 #define UWSPLAT_B200_H
@@ -36,7 +36,7 @@ extern "C" {
 
 #define UWS_TILE 16
 
-/* Pinhole camera (reference: scene.py:222-278, Camera).  R is row-major
+/* Pinhole camera (reference: scene.py:190-245, Camera).  R is row-major
  * world->view, x_view = R x + t.  tan_fov = 0.5*width/fx. */
 typedef struct uws_camera {
     int32_t width, height;
@@ -46,7 +46,7 @@ typedef struct uws_camera {
     double near_plane, far_plane;
 } uws_camera;
 
-/* GaussianCloud fields (scene.py:130-137), float32 SoA, device pointers. */
+/* GaussianCloud fields (scene.py:97-105), float32 SoA, device pointers. */
 typedef struct uws_cloud {
     const float* positions;       /* [n][3] */
     const float* log_scales;      /* [n][3] */
@@ -96,6 +96,13 @@ typedef struct uws_raster_out {
     int32_t* tile_rows;
     int32_t* tile_nrows;
     int32_t tile_rows_cap;
+    /* optional exact-transmittance pass: the float32 walk decides T >= 1e-4
+     * (rasterizer.py:169) in float32; pixels whose T lands within +-0.2 % of
+     * 1e-4 are listed in fix_pixels [H*W] and re-walked in float64, so count,
+     * last and the T decision equal the reference's.  fix_count: device
+     * int32[2], zero on entry and left zero on exit.  NULL to skip. */
+    int32_t* fix_pixels;
+    int32_t* fix_count;
 } uws_raster_out;
 
 /* Adam hyper-parameters for one apply_gradients call (optim.py:69-120).
@@ -132,8 +139,10 @@ int uws_preprocess_fwd(const uws_cloud* cloud, const uws_camera* cam, uws_projec
  *      uws_bin_emit builds the tile lists by two levels of stable bucketing
  *      -- rank order -> tile-row lists -> tile lists -- and the CSR ranges.
  *      If E > e_cap or S > s_cap it sets *overflow = 1, writes all-zero
- *      offsets (empty lists) and nothing else -- and, if skip_counter is
- *      given, adds 65536 to it so a following uws_adam_step is a no-op; the
+ *      offsets (empty lists) and nothing else -- and, if skip_counter (device
+ *      float[2] = {non-finite count, overflow count}, the gradient buffer's
+ *      slots 16n+9, 16n+10) is given, adds 1 to skip_counter[1] so a
+ *      following uws_adam_step is a no-op; the
  *      caller grows its buffers to the totals and re-runs.  count_ws is sized with (k_cap, 0) and must
  *      be the same buffer in both calls; emit_ws with (k_cap, s_cap). */
 int uws_bin_workspace_size(int64_t k_cap, int64_t s_cap, int32_t n_tiles_x, int32_t n_tiles_y,
@@ -201,7 +210,7 @@ int uws_raster_bwd_rows(const uws_projected* proj, const int32_t* row_start,
  *      _quat_backward :166-181).  grads: float32 flat buffer laid out as
  *      [positions 3n | log_scales 3n | rotations 4n | sh 3n | opacity n |
  *       mean2d_grad_norm n | observed n | medium 9 | non-finite counter |
- *       pad 6], accumulated (+=); K is read from proj->num_visible.
+ *       overflow counter | pad 5], accumulated (+=); K is read from proj->num_visible.
  *      screen_grads and medium_acc are consumed and left zeroed.  The
  *      guidance subgradient lambda_guide*sign(.) is added into the medium
  *      slots (backward.py:270-274).  nonfinite (optional device float) is
@@ -215,16 +224,17 @@ int uws_preprocess_bwd(const uws_cloud* cloud, const uws_camera* cam, const uws_
                        float* grads, float* nonfinite, int32_t accumulate, void* stream);
 
 /* ---- optimizer (replaces optim.apply_gradients :98-120 / adam_step :69-83,
- *      GaussianCloud.normalize_rotations scene.py:165-167 and
- *      MediumParams.clamp_ scene.py:207-211).  params/m/v: 14n floats in the
+ *      GaussianCloud.normalize_rotations scene.py:132-134 and
+ *      MediumParams.clamp_ scene.py:174-178).  params/m/v: 14n floats in the
  *      field layout above; grads: the flat gradient buffer; medium_*: 9
  *      floats (medium_grads = grads + 16n).  Optional step control for the
  *      device-resident training loop (pipeline.py:182-192): skip (device
- *      float) > 0 turns the update into a no-op; grad_accum/obs_count
- *      receive the densification statistics; zero_grads leaves the
- *      gradient buffer zeroed for the next step except the skip counter
- *      (medium_grads[9]), which stays set after a skip so that steps already
- *      queued behind it skip as well, until the caller clears it. ------ */
+ *      float[2] = {non-finite count, overflow count}) with either > 0 turns
+ *      the update into a no-op; grad_accum/obs_count receive the
+ *      densification statistics; zero_grads leaves the gradient buffer
+ *      zeroed for the next step except the skip counters (medium_grads[9],
+ *      [10]), which stay set after a skip so that steps already queued
+ *      behind it skip as well, until the caller clears them. ------ */
 int uws_adam_step(float* params, float* exp_avg, float* exp_avg_sq, float* grads, int64_t n,
                   float* medium_params, float* medium_exp_avg, float* medium_exp_avg_sq,
                   float* medium_grads, const uws_adam_params* hp, const float* skip,

@@ -60,7 +60,7 @@ def _sigmoid(x):
 
 
 def rotmat_from_quat(q):
-    """wxyz quaternion -> rotation matrix; normalizes first (scene.py:65-81)."""
+    """wxyz quaternion -> rotation matrix; normalizes first (scene.py:32-48)."""
     q = np.asarray(q, dtype=np.float64)
     q = q / np.linalg.norm(q, axis=-1, keepdims=True)
     w, x, y, z = (q[..., i] for i in range(4))
@@ -237,16 +237,29 @@ def tile_lists(proj, width, height, tiles=None):
     if K == 0:
         return np.zeros(n_tiles + 1, np.int64), np.zeros(0, np.int64)
     r = tile_rect(proj.mean2d, proj.radius, (gx, gy))
+    rows_of = np.arange(K)
+    if tiles is not None:
+        # only footprints whose rectangle covers a requested tile can emit an
+        # entry for it: enumerate those (same entries, same order, a fraction
+        # of the memory at 4K)
+        tl = np.asarray(tiles, np.int64)
+        txs, tys = tl % gx, tl // gx
+        hit = np.zeros(K, bool)
+        for tx_, ty_ in zip(txs, tys):
+            hit |= (r[:, 0] <= tx_) & (tx_ <= r[:, 2]) & (r[:, 1] <= ty_) & (ty_ <= r[:, 3])
+        rows_of = np.nonzero(hit)[0]
+        r = r[rows_of]
     wx = r[:, 2] - r[:, 0] + 1
     wy = r[:, 3] - r[:, 1] + 1
     cnt = np.maximum(wx, 0) * np.maximum(wy, 0)
     total = int(cnt.sum())
     if total == 0:
         return np.zeros(n_tiles + 1, np.int64), np.zeros(0, np.int64)
-    owner = np.repeat(np.arange(K), cnt)
+    local = np.repeat(np.arange(len(r)), cnt)
     first = np.cumsum(cnt) - cnt
-    k = np.arange(total) - first[owner]
-    tid = (r[owner, 1] + k // wx[owner]) * gx + (r[owner, 0] + k % wx[owner])
+    k = np.arange(total) - first[local]
+    tid = (r[local, 1] + k // wx[local]) * gx + (r[local, 0] + k % wx[local])
+    owner = rows_of[local]
     if tiles is not None:
         sel = np.isin(tid, np.asarray(tiles))
         owner, tid = owner[sel], tid[sel]
@@ -637,7 +650,7 @@ def backward(out, dL_dC, n_source, medium=None, lambda_guide=0.0, tiles=None, sc
 
 
 # ---------------------------------------------------------------------------
-# optimizer (optim.py:55-120, scene.py:165-167, 207-211)
+# optimizer (optim.py:55-120, scene.py:132-134, 207-211)
 # ---------------------------------------------------------------------------
 def position_lr(iteration, lr_init=0.00016, lr_final=0.0000016, delay_mult=0.01,
                 max_steps=30000, spatial_scale=1.0):
@@ -662,13 +675,13 @@ def adam(params, grads, m, v, step, lr, beta1=0.9, beta2=0.999, eps=1e-15):
 
 
 def renormalize(rot):
-    """Quaternion renormalization with a 1e-12 floor (scene.py:165-167)."""
+    """Quaternion renormalization with a 1e-12 floor (scene.py:132-134)."""
     nr = np.linalg.norm(rot.astype(np.float64), axis=1, keepdims=True)
     return (rot / np.maximum(nr, 1e-12)).astype(np.float32)
 
 
 def clamp_medium(att, wat, bsc):
-    """Medium box projection (scene.py:207-211)."""
+    """Medium box projection (scene.py:174-178)."""
     return (np.maximum(att, np.float32(0.0)).astype(np.float32),
             np.clip(wat, 0.0, 1.0).astype(np.float32),
             np.clip(bsc, 0.0, 5.0).astype(np.float32))

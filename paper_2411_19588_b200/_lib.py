@@ -42,7 +42,8 @@ class RasterOutC(ctypes.Structure):
     _fields_ = [("color", c_void_p), ("color_clean", c_void_p), ("depth", c_void_p),
                 ("weight", c_void_p), ("final_T", c_void_p), ("count", c_void_p),
                 ("last", c_void_p), ("attenuation", c_void_p), ("backscatter", c_void_p),
-                ("tile_rows", c_void_p), ("tile_nrows", c_void_p), ("tile_rows_cap", c_int32)]
+                ("tile_rows", c_void_p), ("tile_nrows", c_void_p), ("tile_rows_cap", c_int32),
+                ("fix_pixels", c_void_p), ("fix_count", c_void_p)]
 
 
 class AdamParamsC(ctypes.Structure):

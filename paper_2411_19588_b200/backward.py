@@ -19,15 +19,16 @@ from .rasterizer import RenderOutput
 from .scene import GaussianCloud, MediumParams, flat_views
 
 GRAD_FLOATS_PER_GAUSSIAN = 16   # 14 params + mean2d_grad_norm + observed
-MEDIUM_SLOTS = 16               # 9 medium gradients, the non-finite counter, pad
+MEDIUM_SLOTS = 16               # 9 medium gradients, non-finite + overflow counters, pad
 
 
 class GradientBuffer:
     """Gradients co-indexed with a cloud generation (backward.py:46-69).
 
     One flat float32 device buffer ``[d_params 14n | mean2d_grad_norm n |
-    observed n | medium 9 | pad]`` so multi-view accumulation and the NCCL
-    all-reduce are a single contiguous array.  ``observed`` counts the views
+    observed n | medium 9 | non-finite count | overflow count | pad]`` so
+    multi-view accumulation and the NCCL all-reduce are a single contiguous
+    array (the two device skip counters included).  ``observed`` counts the views
     that saw each Gaussian (the reference's boolean is ``observed > 0``).
     """
 
@@ -48,7 +49,12 @@ class GradientBuffer:
         self.d_attenuation = self.flat[16 * n:16 * n + 3]
         self.d_water_color = self.flat[16 * n + 3:16 * n + 6]
         self.d_backscatter = self.flat[16 * n + 6:16 * n + 9]
-        self.nonfinite = self.flat[16 * n + 9:16 * n + 10]   # device skip counter
+        # device skip counters {non-finite values, row-list overflows}; kernels
+        # that count non-finite values get a pointer to slot 9, the binning
+        # guard and Adam read both slots
+        self.skip_counters = self.flat[16 * n + 9:16 * n + 11]
+        self.nonfinite = self.flat[16 * n + 9:16 * n + 10]
+        self.overflow = self.flat[16 * n + 10:16 * n + 11]
         self.generation = -1
 
     @property

@@ -2,8 +2,8 @@
 //
 // Replaces optim.apply_gradients (optim.py:98-120) -> adam_step (:69-83) for
 // the five cloud tensors and the three medium triplets, followed by
-// GaussianCloud.normalize_rotations (scene.py:165-167) and
-// MediumParams.clamp_ (scene.py:207-211).
+// GaussianCloud.normalize_rotations (scene.py:132-134) and
+// MediumParams.clamp_ (scene.py:174-178).
 //
 // float64 arithmetic with explicitly rounded intrinsics (no FMA contraction)
 // in numpy's operation order; learning rates and bias corrections
@@ -60,7 +60,7 @@ __device__ __forceinline__ void adam1(float& p, float& m, float& v, float g, con
 }
 
 struct AdamCtl {
-    const float* skip;      // device: skip the update when *skip > 0 (non-finite count)
+    const float* skip;      // device float[2] {non-finite, overflow}: skip when either > 0
     float* grad_accum;      // densify statistics (pipeline.py:191-192), may be NULL
     int32_t* obs_count;
     int zero_grads;         // leave the gradient buffer zeroed for the next step
@@ -82,7 +82,7 @@ __global__ void __launch_bounds__(kThreads, MINB) k_adam_cloud(float* __restrict
                                                          int nb_flat, uws_adam_params hp,
                                                          AdamCtl ctl) {
     // launched serially (no pdl_entry): the per-CTA L1 invalidation costs more here
-    const bool skip = ctl.skip && *ctl.skip > 0.0f;
+    const bool skip = ctl.skip && (ctl.skip[0] > 0.0f || ctl.skip[1] > 0.0f);
     if ((int)blockIdx.x < nb_flat) {
         const int64_t n10 = 10 * n;
         const int64_t t0 = (int64_t)blockIdx.x * kThreads * kEpt + threadIdx.x;
@@ -175,7 +175,7 @@ __global__ void __launch_bounds__(kThreads, 4) k_adam_cloud4(float* __restrict__
     // groups [g_begin, g_end) of the 14n/4 (all of them for a whole step)
     const int64_t t = g_begin + (int64_t)blockIdx.x * kThreads + threadIdx.x;
     if (t >= g_end) return;
-    const bool skip = ctl.skip && *ctl.skip > 0.0f;
+    const bool skip = ctl.skip && (ctl.skip[0] > 0.0f || ctl.skip[1] > 0.0f);
     if (t < n) {
         if (!skip && ctl.grad_accum) {
             ctl.grad_accum[t] += Gr[14 * n + t];
@@ -230,11 +230,11 @@ __global__ void k_adam_medium(float* __restrict__ P, float* __restrict__ M, floa
     pdl_entry();
     const int v = threadIdx.x;
     if (v >= 16) return;
-    const bool skip = ctl.skip && *ctl.skip > 0.0f;
+    const bool skip = ctl.skip && (ctl.skip[0] > 0.0f || ctl.skip[1] > 0.0f);
     __syncwarp();
     if (v >= 9 || skip) {
-        // slots 9..15 (non-finite counter + pad) are reset after every step
-        if (ctl.zero_grads) Gr[v] = 0.f;
+        // slots 9, 10 (skip counters) and the pad 11..15 are left to the host
+        // launcher (the counters survive a skip, see uws_adam_step)
         return;
     }
     const int f = 5 + v / 3;
@@ -272,8 +272,11 @@ extern "C" int uws_adam_step(float* params, float* exp_avg, float* exp_avg_sq, f
                     "uws_adam_step: null medium buffer");
         AdamCtl mctl = ctl;
         mctl.zero_grads = 0;
-        launch(k_adam_medium, dim3(1), dim3(32), 0, st, medium_params, medium_exp_avg, medium_exp_avg_sq,
-                                        medium_grads, *hp, mctl);
+        // serial launch: after a multi-GPU all-reduce the stream waits on an event
+        // right before this kernel, and a programmatic (early) launch must not
+        // overtake that wait
+        launch_serial(k_adam_medium, dim3(1), dim3(32), 0, st, medium_params, medium_exp_avg,
+                      medium_exp_avg_sq, medium_grads, *hp, mctl);
         UWS_CHECK_LAUNCH("k_adam_medium");
     }
     if (n > 0) {
@@ -297,10 +300,10 @@ extern "C" int uws_adam_step(float* params, float* exp_avg, float* exp_avg_sq, f
     }
     if (medium_params && zero_grads) {
         // medium slots and pad zeroed after every reader is done; the skip
-        // counter (slot 9) is left alone: non-zero it keeps skipping later
-        // steps until the host has handled the skip and cleared it
+        // counters (slots 9, 10) are left alone: non-zero they keep skipping
+        // later steps until the host has handled the skip and cleared them
         UWS_CUDA(zero_async(medium_grads, 9 * sizeof(float), st));
-        UWS_CUDA(zero_async(medium_grads + 10, 6 * sizeof(float), st));
+        UWS_CUDA(zero_async(medium_grads + 11, 5 * sizeof(float), st));
     }
     return UWS_OK;
 }

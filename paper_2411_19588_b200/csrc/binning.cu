@@ -264,10 +264,11 @@ __global__ void k_bin_guard(const unsigned long long* __restrict__ totals, uint6
     if (threadIdx.x == 0) {
         const bool ovf = totals[0] > e_cap || totals[1] > s_cap;
         *overflow = ovf ? 1 : 0;
-        // overflow is counted in units of 65536 so that, after the gradient
-        // all-reduce, every rank can tell "some rank must re-run" from a
-        // plain non-finite skip (which adds 1)
-        if (ovf && skip_counter) atomicAdd(skip_counter, 65536.0f);
+        // skip_counter = {non-finite count, overflow count}: the overflow has
+        // its own slot so that, after the gradient all-reduce, every rank can
+        // tell "some rank must re-run" from a non-finite skip whatever the
+        // non-finite count
+        if (ovf && skip_counter) atomicAdd(skip_counter + 1, 1.0f);
     }
 }
 

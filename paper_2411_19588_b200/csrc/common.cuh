@@ -20,6 +20,7 @@ constexpr double kMinSigma2 = 9.0;
 // rasterizer.py:27-29
 constexpr double kClamp = 0.99;
 constexpr double kTStop = 1e-4;
+constexpr double kWeightEps = 1e-8;
 // scene.py:22
 constexpr double kSH_C0 = 0.28209479177387814;
 // medium.py:23

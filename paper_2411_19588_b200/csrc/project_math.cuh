@@ -2,7 +2,7 @@
 // (preprocess.cu) and backward (preprocess_bwd.cu) kernels.  Both
 // translation units are compiled with -fmad=false so the expressions below
 // are evaluated exactly as numpy evaluates the reference
-// (projection.py:111-158, scene.py:65-81); numpy's fused matmul inner
+// (projection.py:111-158, scene.py:32-48); numpy's fused matmul inner
 // products are reproduced with explicit __fma_rn in the same order.
 #pragma once
 

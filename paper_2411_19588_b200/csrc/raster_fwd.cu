@@ -24,6 +24,7 @@ constexpr int kBatch = 256;
 constexpr int kFirstFill = 128;
 constexpr int kListPad = 4;                    // per-warp lists are walked 4 entries at a time
 constexpr int kFwdPx = 2;                      // pixels per thread (measured: 1 and 4 are slower)
+constexpr int kFixBlocks = 148 * 2;            // float64 fix-up pass: 8 warps per block
 
 struct FwdArgs {
     const uws_splat* splat;
@@ -35,8 +36,52 @@ struct FwdArgs {
     int width, height, gx;
     float far_plane;
     const float* medium;  // NULL = clean
+    const double* depth64;  // float64 view depths (fix-up pass)
     uws_raster_out out;
 };
+
+// Transmittance band in which the float32 walk's T >= 1e-4 decision may differ
+// from the reference's float64 one.  The float32 alphas carry a relative error
+// of a few 1e-6 (tile-local offsets, ex2.approx), i.e. up to ~2e-4 relative in
+// (1 - alpha) for alpha near the 0.99 clamp; +-2e-3 leaves a 10x margin.  A
+// pixel whose final T, or whose T before its last blend, lands in the band is
+// re-walked in float64 by k_raster_fix.  Each blend lowers T by >= 0.39 %
+// (alpha >= 1/255), so a walk visits the 0.4 %-wide band at most twice and
+// one of those two values is always the final T or the T before the last blend.
+constexpr float kTBandLo = 1e-4f * (1.0f - 2e-3f);
+constexpr float kTBandHi = 1e-4f * (1.0f + 2e-3f);
+
+__device__ __forceinline__ bool t_ambiguous(float t) { return t >= kTBandLo && t <= kTBandHi; }
+
+// Write one pixel's forward outputs, with the underwater epilogue:
+// z = logistic(depth); C exp(-Bd z) + Binf (1 - exp(-Bb z)) (rasterizer.py:244-251)
+__device__ __forceinline__ void store_pixel(const FwdArgs& a, int pix, const float c3[3],
+                                            float depth, float weight, float T, int count,
+                                            int last) {
+    a.out.depth[pix] = depth;
+    a.out.weight[pix] = weight;
+    a.out.final_T[pix] = T;
+    a.out.count[pix] = count;
+    if (a.out.last) a.out.last[pix] = last;
+    if (a.medium == nullptr) {
+#pragma unroll
+        for (int ch = 0; ch < 3; ++ch) {
+            a.out.color[3 * pix + ch] = c3[ch];
+            if (a.out.color_clean) a.out.color_clean[3 * pix + ch] = c3[ch];
+        }
+        return;
+    }
+    const float z = 2.0f / (1.0f + __expf(-(float)kLogisticRate * depth)) - 1.0f;
+#pragma unroll
+    for (int ch = 0; ch < 3; ++ch) {
+        const float att = __expf(-a.medium[ch] * z);
+        const float bs = a.medium[3 + ch] * (1.0f - __expf(-a.medium[6 + ch] * z));
+        a.out.color[3 * pix + ch] = c3[ch] * att + bs;
+        a.out.color_clean[3 * pix + ch] = c3[ch];
+        if (a.out.attenuation) a.out.attenuation[3 * pix + ch] = att;
+        if (a.out.backscatter) a.out.backscatter[3 * pix + ch] = bs;
+    }
+}
 
 // Bit b set <=> the staged box [ylo, yhi] reaches a pixel centre of band b
 // (band b = rows R*b .. R*b + R - 1, nb bands).
@@ -77,6 +122,7 @@ __global__ void __launch_bounds__(kRasterThreads / PX, 4 * PX) k_raster_fwd(FwdA
 
     // pixel state; T = 0 marks a pixel outside the image as finished
     float fx[PX], T[PX], cr[PX], cg[PX], cb[PX], dsum[PX], wsum[PX];
+    float tb[PX];  // T before the last blend (fix-up band test)
     int count[PX], last[PX];
     bool inside[PX];
 #pragma unroll
@@ -85,6 +131,7 @@ __global__ void __launch_bounds__(kRasterThreads / PX, 4 * PX) k_raster_fwd(FwdA
         inside[j] = ox + lx0 + j < a.width && py < a.height;
         T[j] = inside[j] ? 1.0f : 0.0f;
         cr[j] = cg[j] = cb[j] = dsum[j] = wsum[j] = 0.f;
+        tb[j] = 1.0f;
         count[j] = last[j] = 0;
     }
     auto alive = [&]() {
@@ -204,6 +251,7 @@ __global__ void __launch_bounds__(kRasterThreads / PX, 4 * PX) k_raster_fwd(FwdA
                             cb[j] = fmaf(w, c.z, cb[j]);
                             dsum[j] = fmaf(w, p1.w, dsum[j]);
                             wsum[j] += w;
+                            tb[j] = T[j];
                             T[j] = T[j] * (1.0f - alpha);
                             ++count[j];
                             last[j] = rel + idx[u];
@@ -240,30 +288,115 @@ __global__ void __launch_bounds__(kRasterThreads / PX, 4 * PX) k_raster_fwd(FwdA
         if (!inside[j]) continue;
         const int pix = py * a.width + ox + lx0 + j;
         const float depth = count[j] > 0 ? dsum[j] / wsum[j] : a.far_plane;
-        a.out.depth[pix] = depth;
-        a.out.weight[pix] = wsum[j];
-        a.out.final_T[pix] = T[j];
-        a.out.count[pix] = count[j];
-        if (a.out.last) a.out.last[pix] = last[j];
         const float c3[3] = {cr[j], cg[j], cb[j]};
-        if (a.medium == nullptr) {
-#pragma unroll
-            for (int ch = 0; ch < 3; ++ch) {
-                a.out.color[3 * pix + ch] = c3[ch];
-                if (a.out.color_clean) a.out.color_clean[3 * pix + ch] = c3[ch];
-            }
-            continue;
+        store_pixel(a, pix, c3, depth, wsum[j], T[j], count[j], last[j]);
+        if (a.out.fix_pixels && (t_ambiguous(T[j]) || t_ambiguous(tb[j]))) {
+            const int slot = atomicAdd(a.out.fix_count, 1);
+            a.out.fix_pixels[slot] = pix;   // capacity H*W: one slot per pixel at most
         }
-        // underwater epilogue: z = logistic(depth); C*exp(-Bd z) + Binf (1 - exp(-Bb z))
-        const float z = 2.0f / (1.0f + __expf(-(float)kLogisticRate * depth)) - 1.0f;
-#pragma unroll
-        for (int ch = 0; ch < 3; ++ch) {
-            const float att = __expf(-a.medium[ch] * z);
-            const float bs = a.medium[3 + ch] * (1.0f - __expf(-a.medium[6 + ch] * z));
-            a.out.color[3 * pix + ch] = c3[ch] * att + bs;
-            a.out.color_clean[3 * pix + ch] = c3[ch];
-            if (a.out.attenuation) a.out.attenuation[3 * pix + ch] = att;
-            if (a.out.backscatter) a.out.backscatter[3 * pix + ch] = bs;
+    }
+}
+
+// Float64 re-walk of the pixels whose float32 T >= 1e-4 decision was ambiguous
+// (rasterizer.py:166-178 exactly: live_i = T_i >= 1e-4, alpha = min(raw, 0.99),
+// raw < 1/255 -> 0): one warp per pixel, 32 list entries per step (alpha_raw in
+// float64 per lane, then the blend in list order).  The tile's list comes from
+// the CSR tile lists, or the rows the forward stored per tile, or -- past what
+// was stored -- from filtering the tile-row list.  fix_count = {count, ticket}:
+// the last block resets both, so the buffer is zero for the next call.
+template <bool ROWS>
+__global__ void __launch_bounds__(256) k_raster_fix(FwdArgs a) {
+    pdl_entry();
+    const int lane = threadIdx.x & 31;
+    const int nwarps = gridDim.x * (blockDim.x >> 5);
+    const int n = *(volatile int*)a.out.fix_count;
+    for (int i = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); i < n; i += nwarps) {
+        const int pix = a.out.fix_pixels[i];
+        const int py = pix / a.width, px = pix - py * a.width;
+        const int ty = py / kTile, tx = px / kTile, tile = ty * a.gx + tx;
+        // list source: [0, nlist) direct; then (ROWS) the row-list filter
+        const int32_t* list;
+        int nlist;
+        if (ROWS) {
+            list = a.out.tile_rows ? a.out.tile_rows + (size_t)tile * a.out.tile_rows_cap : nullptr;
+            nlist = a.out.tile_rows ? a.out.tile_nrows[tile] : 0;
+        } else {
+            list = a.entries + a.offsets[tile];
+            nlist = a.offsets[tile + 1] - a.offsets[tile];
+        }
+        double T = 1.0, c0 = 0.0, c1 = 0.0, c2 = 0.0, dn = 0.0, ws = 0.0;
+        int count = 0, last = 0;
+        bool done = false;
+        // phase 1: the directly listed entries
+        for (int k0 = 0; k0 < nlist && !done; k0 += 32) {
+            const int k = k0 + lane;
+            const int row = k < nlist ? list[k] : -1;
+            const double ar = row >= 0 ? alpha_raw_f64(a.splat, a.exact, row, px, py) : 0.0;
+            unsigned pass = __ballot_sync(0xffffffffu, row >= 0 && ar >= kFloor);
+            while (pass) {
+                const int b = __ffs(pass) - 1;
+                pass &= pass - 1;
+                if (T < kTStop) { done = true; break; }
+                const double al = fmin(__shfl_sync(0xffffffffu, ar, b), kClamp);
+                const int r = __shfl_sync(0xffffffffu, row, b);
+                const double w = al * T;
+                c0 += w * (double)a.splat[r].r;
+                c1 += w * (double)a.splat[r].g;
+                c2 += w * (double)a.splat[r].b;
+                dn += w * a.depth64[r];
+                ws += w;
+                T *= 1.0 - al;
+                ++count;
+                last = k0 + b + 1;
+            }
+        }
+        // phase 2 (row lists, rare): the tile's entries past the stored ones
+        if (ROWS && !done && T >= kTStop) {
+            int seen = 0;  // matches of this tile so far, in list order
+            const int rend = a.row_start[ty + 1];
+            for (int c = a.row_start[ty]; c < rend && !done; c += 32) {
+                const int q = c + lane;
+                const uint2 it = q < rend ? __ldg(a.row_items + q) : make_uint2(0u, 0xffffu);
+                const bool m = (int)(it.y & 0xffffu) <= tx && tx <= (int)(it.y >> 16);
+                const unsigned bal = __ballot_sync(0xffffffffu, m);
+                const int pos = seen + __popc(bal & lanemask_lt());  // list position if m
+                seen += __popc(bal);
+                const bool mine = m && pos >= nlist;
+                const int row = (int)it.x;
+                const double ar = mine ? alpha_raw_f64(a.splat, a.exact, row, px, py) : 0.0;
+                unsigned pass = __ballot_sync(0xffffffffu, mine && ar >= kFloor);
+                while (pass) {
+                    const int b = __ffs(pass) - 1;
+                    pass &= pass - 1;
+                    if (T < kTStop) { done = true; break; }
+                    const double al = fmin(__shfl_sync(0xffffffffu, ar, b), kClamp);
+                    const int r = __shfl_sync(0xffffffffu, row, b);
+                    const int p = __shfl_sync(0xffffffffu, pos, b);
+                    const double w = al * T;
+                    c0 += w * (double)a.splat[r].r;
+                    c1 += w * (double)a.splat[r].g;
+                    c2 += w * (double)a.splat[r].b;
+                    dn += w * a.depth64[r];
+                    ws += w;
+                    T *= 1.0 - al;
+                    ++count;
+                    last = p + 1;
+                }
+            }
+        }
+        if (lane == 0) {
+            const float c3[3] = {(float)c0, (float)c1, (float)c2};
+            const float depth = ws > kWeightEps ? (float)(dn / ws) : a.far_plane;
+            store_pixel(a, pix, c3, depth, (float)ws, (float)T, count, last);
+        }
+    }
+    // reset {count, ticket} once every block has read the count
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        __threadfence();
+        if (atomicAdd(a.out.fix_count + 1, 1) == (int)gridDim.x - 1) {
+            a.out.fix_count[0] = 0;
+            a.out.fix_count[1] = 0;
         }
     }
 }
@@ -281,6 +414,8 @@ extern "C" int uws_raster_fwd(const uws_projected* proj, const int32_t* offsets,
                 "uws_raster_fwd: missing output buffer");
     UWS_REQUIRE(medium == nullptr || out->color_clean != nullptr,
                 "uws_raster_fwd: underwater mode needs color_clean");
+    UWS_REQUIRE(out->fix_pixels == nullptr || out->fix_count != nullptr,
+                "uws_raster_fwd: fix_pixels needs fix_count");
     FwdArgs a;
     a.splat = proj->splat;
     a.exact = proj->exact;
@@ -294,9 +429,14 @@ extern "C" int uws_raster_fwd(const uws_projected* proj, const int32_t* offsets,
     const int gy = (int)ceil_div(cam->height, kTile);
     a.far_plane = (float)cam->far_plane;
     a.medium = medium;
+    a.depth64 = proj->depth;
     a.out = *out;
     launch_serial(k_raster_fwd<false, kFwdPx>, dim3(a.gx * gy), dim3(kRasterThreads / kFwdPx), 0, as_stream(stream), a);
     UWS_CHECK_LAUNCH("k_raster_fwd");
+    if (out->fix_pixels) {
+        launch(k_raster_fix<false>, dim3(kFixBlocks), dim3(256), 0, as_stream(stream), a);
+        UWS_CHECK_LAUNCH("k_raster_fix");
+    }
     return UWS_OK;
 }
 
@@ -308,6 +448,8 @@ extern "C" int uws_raster_fwd_rows(const uws_projected* proj, const int32_t* row
                 "uws_raster_fwd_rows: missing output buffer");
     UWS_REQUIRE(medium == nullptr || out->color_clean != nullptr,
                 "uws_raster_fwd_rows: underwater mode needs color_clean");
+    UWS_REQUIRE(out->fix_pixels == nullptr || out->fix_count != nullptr,
+                "uws_raster_fwd_rows: fix_pixels needs fix_count");
     UWS_REQUIRE(out->tile_rows == nullptr || (out->tile_nrows && out->tile_rows_cap > 0),
                 "uws_raster_fwd_rows: tile_rows needs tile_nrows and a positive cap");
     FwdArgs a;
@@ -323,8 +465,13 @@ extern "C" int uws_raster_fwd_rows(const uws_projected* proj, const int32_t* row
     const int gy = (int)ceil_div(cam->height, kTile);
     a.far_plane = (float)cam->far_plane;
     a.medium = medium;
+    a.depth64 = proj->depth;
     a.out = *out;
     launch_serial(k_raster_fwd<true, kFwdPx>, dim3(a.gx * gy), dim3(kRasterThreads / kFwdPx), 0, as_stream(stream), a);
     UWS_CHECK_LAUNCH("k_raster_fwd_rows");
+    if (out->fix_pixels) {
+        launch(k_raster_fix<true>, dim3(kFixBlocks), dim3(256), 0, as_stream(stream), a);
+        UWS_CHECK_LAUNCH("k_raster_fix_rows");
+    }
     return UWS_OK;
 }

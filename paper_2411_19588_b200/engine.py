@@ -104,6 +104,9 @@ class StepEngine:
         self._async_pending = None
         self._k = 0
         self._pending = None
+        # parity tests: leave the step's summed gradients in ``grads`` after Adam
+        # (Adam normally consumes and zeroes them)
+        self.keep_gradients = False
         self.copy_stream = torch.cuda.Stream(device=dev)
 
     def _alloc(self, n: int):
@@ -168,10 +171,13 @@ class StepEngine:
         """Queue one render-only frame without waiting for it (a frame stream).
 
         The row-list overflow flag of the PREVIOUS queued frame is read after this
-        one is queued, so the host never idles the GPU between frames.  The
-        returned buffers hold the most recent frame once ``render_flush()`` has
-        returned; if a frame overflowed its row lists, the lists are grown and
-        the most recent frame is rendered again, synchronously."""
+        one is queued, so the host never idles the GPU between frames.  Every
+        frame writes the same output buffers: they hold a valid image only for
+        the most recent frame and only once ``render_flush()`` has returned (a
+        frame that overflowed its row lists is a medium-only image until then;
+        the flush grows the lists and renders the most recent frame again,
+        synchronously).  ``step_async`` and ``refresh_guidance`` flush a
+        pending frame first."""
         cam = Camera.from_any(cam)
         if self._pending is None:
             self._sync_cloud()
@@ -281,18 +287,21 @@ class StepEngine:
         chunks = None
         if self.dist is not None and self.world > 1:
             chunks = self._all_reduce_gradients()
-        # the skip counter is read by the Adam launch (and kept while non-zero): keep a copy
-        slot.stats[-1:].copy_(self.grads.nonfinite)
+        # the skip counters are read by the Adam launch (and kept while non-zero): keep a copy
+        slot.stats[-2:].copy_(self.grads.skip_counters)
         saved = self.state.iteration
         self.state.iteration = slot.iteration
-        apply_gradients_device(self.state, self.grads, self.cfg, self.spatial_scale, chunks=chunks)
+        apply_gradients_device(self.state, self.grads, self.cfg, self.spatial_scale,
+                               zero_grads=not self.keep_gradients, chunks=chunks)
         self.state.iteration = saved
         slot.host.copy_(slot.stats, non_blocking=True)
         slot.done.record(cur)
         slot.free.record(cur)
 
-    # gradient all-reduce split against the cloud update (multi-GPU)
-    ALLREDUCE_PARTS = 4
+    # gradient all-reduce: 1 = one NCCL all-reduce of the whole flat buffer, then
+    # the single Adam launch (the default: the split form below has only been
+    # measured on one GPU); > 1 = split against the range-wise cloud update
+    ALLREDUCE_PARTS = 1
 
     def _all_reduce_gradients(self):
         """Sum the flat gradient buffer over the ranks.  The medium/skip tail and the
@@ -303,6 +312,9 @@ class StepEngine:
         Returns the chunk list for ``apply_gradients_device`` (None when the range
         form does not apply: every part has been waited for, then the single launch)."""
         flat, n, d, g = self.grads.flat, self.n, self.dist, self.group
+        if self.ALLREDUCE_PARTS <= 1:
+            d.all_reduce(flat, group=g)
+            return None
         # the same collectives on every rank (they depend on n only) ...
         parts = [(14 * n * c // self.ALLREDUCE_PARTS // 4, 14 * n * (c + 1) // self.ALLREDUCE_PARTS // 4)
                  for c in range(self.ALLREDUCE_PARTS)]
@@ -329,7 +341,7 @@ class StepEngine:
             tot = s[i * _ST_SIZE + _ST_TOTALS:i * _ST_SIZE + _ST_TOTALS + 2].view(torch.int64)
             need_e = max(need_e, int(tot[0]))   # tile entries (reported only)
             need_s = max(need_s, int(tot[1]))   # row-list items (capacity)
-        return float(s[-1]), need_e, need_s
+        return float(s[-2]), float(s[-1]), need_e, need_s
 
     def _stats(self, slot: "_Slot", skipped: bool, reruns: int, need_e: int) -> EngineStats:
         s, nv = slot.host, len(slot.views)
@@ -346,8 +358,8 @@ class StepEngine:
         which also turns every later launched step into a no-op; the host then
         undoes their step-counter advances, clears the counter, re-runs an
         overflowed step with grown lists and re-launches the later step."""
-        skip_count, need_e, need_s = self._read(slot)
-        if skip_count == 0:
+        nonfinite, overflow, need_e, need_s = self._read(slot)
+        if nonfinite == 0 and overflow == 0:
             return self._stats(slot, False, 0, need_e)
         nxt = self._pending if self._pending is not slot else None
         if self.state.cloud.generation != self.generation:
@@ -357,19 +369,24 @@ class StepEngine:
         rollback_steps(self.state)
         if nxt is not None:
             rollback_steps(self.state)
-        self.grads.nonfinite.zero_()
+        self.grads.skip_counters.zero_()
         reruns = 0
-        while skip_count >= 65536.0 and reruns < 3:
+        # a row-list overflow on any rank: grow to the reported size and re-run
+        # (a step that is also non-finite is then reported as skipped)
+        while overflow > 0 and reruns < 3:
             if need_s > self.s_cap:
                 self._set_capacity(int(need_s * 1.25) + 1024)
             reruns += 1
+            self.grads.flat.zero_()   # (already zero unless keep_gradients)
             self._launch(slot)
-            skip_count, need_e, need_s = self._read(slot)
-            if skip_count > 0:
+            nonfinite, overflow, need_e, need_s = self._read(slot)
+            if nonfinite > 0 or overflow > 0:
                 rollback_steps(self.state)
-                self.grads.nonfinite.zero_()
-        st = self._stats(slot, skip_count > 0, reruns, need_e)
+                self.grads.skip_counters.zero_()
+        st = self._stats(slot, nonfinite > 0 or overflow > 0, reruns, need_e)
         if nxt is not None:
+            if self.keep_gradients:
+                self.grads.flat.zero_()
             self._launch(nxt)
         return st
 
@@ -379,6 +396,8 @@ class StepEngine:
         waiting for it; ground-truth images may be host arrays (copied on a side
         stream while the previous step runs) or device tensors.  Returns the
         stats of the previously launched step (None for the first)."""
+        if self._async_pending is not None:
+            self.render_flush()      # the frame stream shares the step's buffers
         self._sync_cloud()
         slot = self._slots[self._k % 2]
         self._k += 1
@@ -401,6 +420,9 @@ class StepEngine:
         from .backscatter import refresh_guidance
         if self._pending is not None:
             raise RuntimeError("refresh_guidance reads the last step's render: call flush() first")
+        if self._async_pending is not None:
+            raise RuntimeError("refresh_guidance reads the last step's render depth, but a "
+                               "render_async frame has replaced it")
         if not isinstance(gt, torch.Tensor):
             gt = torch.from_numpy(np.ascontiguousarray(gt, dtype=np.float32))
         return refresh_guidance(self.state.medium, gt, self.out.depth, **kw)

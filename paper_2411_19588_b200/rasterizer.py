@@ -159,6 +159,10 @@ class RenderOutput:
     # TILE_ROWS_CAP per tile) and how many were stored
     tile_rows: Optional[torch.Tensor] = None
     tile_nrows: Optional[torch.Tensor] = None
+    # exact T >= 1e-4 decisions: scratch list of the pixels re-walked in float64
+    # and its {count, ticket} pair (zero between calls)
+    fix_pixels: Optional[torch.Tensor] = None
+    fix_count: Optional[torch.Tensor] = None
 
     def c_struct(self) -> _lib.RasterOutC:
         cap = self.tile_rows.shape[1] if self.tile_rows is not None else 0
@@ -167,7 +171,8 @@ class RenderOutput:
                                _lib.ptr(self.final_transmittance), _lib.ptr(self.count),
                                _lib.ptr(self.last), _lib.ptr(self.attenuation_map),
                                _lib.ptr(self.backscatter_map), _lib.ptr(self.tile_rows),
-                               _lib.ptr(self.tile_nrows), cap)
+                               _lib.ptr(self.tile_nrows), cap, _lib.ptr(self.fix_pixels),
+                               _lib.ptr(self.fix_count))
 
 
 # staged rows kept per tile for the backward (the consumed prefix is ~140 rows on
@@ -180,7 +185,9 @@ def _alloc_output(H, W, dev, mode, medium_maps, tile_rows=True):
     out = RenderOutput(color=torch.empty(H, W, 3, **f), depth=torch.empty(H, W, **f),
                        weight=torch.empty(H, W, **f), final_transmittance=torch.empty(H, W, **f),
                        count=torch.empty(H, W, dtype=torch.int32, device=dev), mode=mode,
-                       last=torch.empty(H, W, dtype=torch.int32, device=dev))
+                       last=torch.empty(H, W, dtype=torch.int32, device=dev),
+                       fix_pixels=torch.empty(H * W, dtype=torch.int32, device=dev),
+                       fix_count=torch.zeros(2, dtype=torch.int32, device=dev))
     if tile_rows:
         tiles = ((H + TILE_SIZE - 1) // TILE_SIZE) * ((W + TILE_SIZE - 1) // TILE_SIZE)
         out.tile_rows = torch.empty(tiles, TILE_ROWS_CAP, dtype=torch.int32, device=dev)
@@ -220,7 +227,9 @@ def render(cloud: GaussianCloud, cam, medium: Optional[MediumParams] = None,
     cam = Camera.from_any(cam)
     proj = project_cloud(cloud, cam, with_geometry=False)
     rows = bin_rows(proj, cam.width, cam.height)
-    out = _alloc_output(cam.height, cam.width, proj.device, mode, medium_maps, tile_rows=retain)
+    # the per-tile staged rows are kept even when not retained: the float64
+    # fix-up pass of the T >= 1e-4 decisions reads them
+    out = _alloc_output(cam.height, cam.width, proj.device, mode, medium_maps)
     pc, cc, oc = proj.c_struct(), cam.c_struct(), out.c_struct()
     med = _lib.ptr(medium.flat) if mode == "underwater" else 0
     _lib.call("uws_raster_fwd_rows", ctypes.byref(pc), _lib.ptr(rows.row_start),
@@ -234,6 +243,7 @@ def render(cloud: GaussianCloud, cam, medium: Optional[MediumParams] = None,
         out.proj = None
         out.bins = None
         out.rows = None
+        out.tile_rows = out.tile_nrows = None
     return out
 
 

@@ -1,6 +1,6 @@
 """Scene state on the device: Gaussians, cameras, medium, optimizer state.
 
-Mirrors the reference types (reference: scene.py:94-314) with the same field
+Mirrors the reference types (reference: scene.py:90-371) with the same field
 names and semantics.  Learnable tensors are float32 CUDA tensors; the five
 cloud fields are contiguous slices of ONE flat buffer laid out
 ``[positions 3n | log_scales 3n | rotations 4n | sh_coeffs 3n | opacity n]``
@@ -46,7 +46,7 @@ def _as_f32(a, shape, device):
 
 
 def quat_to_rotmat(q):
-    """wxyz quaternions -> rotation matrices, normalising first (scene.py:65-81)."""
+    """wxyz quaternions -> rotation matrices, normalising first (scene.py:32-48)."""
     q = np.asarray(q, dtype=np.float64)
     q = q / np.linalg.norm(q, axis=-1, keepdims=True)
     w, x, y, z = q[..., 0], q[..., 1], q[..., 2], q[..., 3]
@@ -81,7 +81,7 @@ def flat_views(flat: torch.Tensor, n: int) -> dict:
 
 
 class GaussianCloud:
-    """Device-resident structure-of-arrays Gaussians (reference scene.py:123-180).
+    """Device-resident structure-of-arrays Gaussians (reference scene.py:90-147).
 
     ``generation`` is bumped whenever the set of Gaussians changes.
     """
@@ -159,13 +159,13 @@ class GaussianCloud:
                            _lib.ptr(self.opacity_logits), self._n)
 
     def normalize_rotations(self):
-        """q / max(|q|, 1e-12) (scene.py:165-167); fused into Adam on the hot path."""
+        """q / max(|q|, 1e-12) (scene.py:132-134); fused into Adam on the hot path."""
         q = self.rotations.double()
         nr = torch.sqrt(((q[:, 0] ** 2 + q[:, 1] ** 2) + q[:, 2] ** 2) + q[:, 3] ** 2)
         self.rotations.copy_((q / torch.clamp(nr, min=1e-12)[:, None]).float())
 
     def base_colors(self) -> torch.Tensor:
-        """Clamped degree-0 RGB, float64 (scene.py:169-172)."""
+        """Clamped degree-0 RGB, float64 (scene.py:136-139)."""
         return torch.clamp(self.sh_coeffs[:, 0, :].double() * SH_C0 + 0.5, min=0.0)
 
     def copy(self) -> "GaussianCloud":
@@ -181,7 +181,7 @@ class GaussianCloud:
 
 
 class MediumParams:
-    """Water parameters + optional guidance anchors (scene.py:183-219), on device."""
+    """Water parameters + optional guidance anchors (scene.py:150-187), on device."""
 
     def __init__(self, attenuation, water_color, backscatter, water_color_guide=None,
                  backscatter_guide=None, device=None):
@@ -243,7 +243,7 @@ class MediumParams:
         self._has_wg = self._has_bg = True
 
     def clamp_(self):
-        """Project into the boxes (scene.py:207-211); fused into Adam on the hot path."""
+        """Project into the boxes (scene.py:174-178); fused into Adam on the hot path."""
         self._flat[0:3].clamp_(min=0.0)
         self._flat[3:6].clamp_(*WATER_COLOR_BOUNDS)
         self._flat[6:9].clamp_(*BACKSCATTER_BOUNDS)
@@ -260,7 +260,7 @@ class MediumParams:
 
 @dataclass
 class Camera:
-    """Pinhole camera (scene.py:222-278): x_view = R x_world + t; pixel centres at +0.5."""
+    """Pinhole camera (scene.py:190-245): x_view = R x_world + t; pixel centres at +0.5."""
 
     width: int
     height: int
@@ -331,7 +331,7 @@ class Camera:
 
 
 class AdamSlot:
-    """Moments + step counter of one tensor (scene.py:248-254); views into TrainState buffers."""
+    """Moments + step counter of one tensor (scene.py:248-259); views into TrainState buffers."""
 
     def __init__(self, m: torch.Tensor, v: torch.Tensor):
         self.m = m

@@ -70,3 +70,47 @@ def grad_tolerance_ok(got, ref, rel=1e-3, abs_frac=1e-6):
 
 def np_(t):
     return t.detach().cpu().numpy()
+
+
+def adam_replay(params, grads, medium, iteration, cfg, moments=None, step=1, spatial_scale=1.0):
+    """The reference's apply_gradients (optim.py:98-120) in numpy on float32
+    gradients ``grads`` (dict d_<field> / medium (9,)): returns the updated
+    (params, medium, moments).  ``moments`` = (m, v, medium m, medium v) or None."""
+    from oracle import uwsplat_oracle as O
+    lrs = {"positions": uw.position_lr(iteration, cfg, spatial_scale),
+           "log_scales": cfg.scaling_lr, "rotations": cfg.rotation_lr,
+           "sh_coeffs": cfg.feature_lr, "opacity_logits": cfg.opacity_lr}
+    if moments is None:
+        moments = ({f: np.zeros_like(v) for f, v in params.items()},
+                   {f: np.zeros_like(v) for f, v in params.items()},
+                   {f: np.zeros(3, np.float32) for f in MEDIUM_FIELDS},
+                   {f: np.zeros(3, np.float32) for f in MEDIUM_FIELDS})
+    m, v, mm, mv = moments
+    out = {}
+    for f in FIELDS:
+        out[f], m[f], v[f] = O.adam(params[f], grads["d_" + f], m[f], v[f], step, lrs[f])
+    out["rotations"] = O.renormalize(out["rotations"])
+    new_med = []
+    for j, f in enumerate(MEDIUM_FIELDS):
+        lr = getattr(cfg, uw.optim._LR_FIELDS[f])
+        q, mm[f], mv[f] = O.adam(medium[f], grads["medium"][3 * j:3 * j + 3], mm[f], mv[f],
+                                 step, lr)
+        new_med.append(q)
+    med = dict(zip(MEDIUM_FIELDS, O.clamp_medium(*new_med)))
+    return out, med, (m, v, mm, mv)
+
+
+MEDIUM_FIELDS = ("attenuation", "water_color", "backscatter")
+
+
+def host_state(cloud, medium):
+    """float32 host copies of a device cloud / medium (for adam_replay)."""
+    params = {f: np_(getattr(cloud, f)).copy() for f in FIELDS}
+    med = {f: np_(getattr(medium, f)).copy() for f in MEDIUM_FIELDS}
+    return params, med
+
+
+def host_grads(buf):
+    g = {f: np_(getattr(buf, f)).copy() for f in GRAD_FIELDS}
+    g["medium"] = np_(buf.medium).copy()
+    return g

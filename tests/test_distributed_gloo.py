@@ -89,7 +89,7 @@ def test_shard_views_partition():
         assert {len(s) for s in shards} == {64 // world}
 
 
-def _chunked_worker(rank, world, port, q, n):
+def _chunked_worker(rank, world, port, q, n, parts):
     os.environ["MASTER_ADDR"] = "127.0.0.1"
     os.environ["MASTER_PORT"] = str(port)
     dist.init_process_group("gloo", rank=rank, world_size=world)
@@ -107,7 +107,7 @@ def _chunked_worker(rank, world, port, q, n):
     state = SimpleNamespace(cloud=Cloud(), exp_avg=torch.zeros(14 * n),
                             exp_avg_sq=torch.zeros(14 * n))
     fake = SimpleNamespace(grads=SimpleNamespace(flat=flat), n=n, dist=dist, group=None,
-                           state=state, ALLREDUCE_PARTS=3)
+                           state=state, ALLREDUCE_PARTS=parts)
     chunks = StepEngine._all_reduce_gradients(fake)
     groups = []
     for g0, g1, wait in chunks or ():
@@ -118,15 +118,15 @@ def _chunked_worker(rank, world, port, q, n):
     dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("n", [1000, 1001])
-def test_chunked_gradient_allreduce_covers_the_buffer(n):
+@pytest.mark.parametrize("n,parts", [(1000, 3), (1001, 3), (1000, 1)])
+def test_chunked_gradient_allreduce_covers_the_buffer(n, parts):
     """The engine's split all-reduce (medium/skip tail and statistics first, then the
     parameter gradients in parts that the range-wise Adam waits for) sums every slot;
     odd n (no range-wise update) issues the same collectives and waits for all."""
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
-    procs = [ctx.Process(target=_chunked_worker, args=(r, 2, port, q, n)) for r in range(2)]
+    procs = [ctx.Process(target=_chunked_worker, args=(r, 2, port, q, n, parts)) for r in range(2)]
     for p in procs:
         p.start()
     got = dict((r, (a, b, g)) for r, a, b, g in (q.get(timeout=240) for _ in range(2)))
@@ -137,7 +137,7 @@ def test_chunked_gradient_allreduce_covers_the_buffer(n):
     for r in (0, 1):
         np.testing.assert_allclose(got[r][1], total, rtol=1e-6, atol=1e-6)
     groups = got[0][2]
-    if n % 2:
+    if n % 2 or parts == 1:
         assert groups == []
         return
     assert groups[0][0] == 0 and groups[-1][1] == 14 * n // 4 and len(groups) == 3

@@ -86,8 +86,8 @@ def test_c2_render_sampled_tiles(c2):
     assert np.abs(np_(out.color)[mask] - o.color[mask]).max() < 1e-4
     assert np.abs(np_(out.color_clean)[mask] - o.color_clean[mask]).max() < 1e-4
     np.testing.assert_allclose(np_(out.depth)[mask], o.depth[mask], rtol=1e-5)
-    cnt_diff = np.abs(np_(out.count)[mask] - o.count[mask])
-    assert cnt_diff.max() <= 1 and (cnt_diff > 0).mean() < 1e-3
+    # the T >= 1e-4 decisions are exact (float64 fix-up pass): counts bit-exact
+    np.testing.assert_array_equal(np_(out.count)[mask], o.count[mask])
 
 
 def test_c2_loss_full_frame(c2):
