@@ -92,7 +92,8 @@ typedef struct uws_raster_out {
     /* optional (row-list path): the first tile_rows_cap rows each tile staged, in
      * list order, so the backward reads its consumed prefix instead of filtering
      * the row lists again; NULL to skip.  tile_rows [tiles][tile_rows_cap],
-     * tile_nrows [tiles] = rows stored (written by uws_raster_fwd_rows). */
+     * tile_nrows [tiles] = rows stored (written by uws_raster_fwd_rows), with bit 30
+     * set when the stored rows are the tile's whole list. */
     int32_t* tile_rows;
     int32_t* tile_nrows;
     int32_t tile_rows_cap;
@@ -100,7 +101,8 @@ typedef struct uws_raster_out {
      * (rasterizer.py:169) in float32; pixels whose T lands within +-0.2 % of
      * 1e-4 are listed in fix_pixels [H*W] and re-walked in float64, so count,
      * last and the T decision equal the reference's.  fix_count: device
-     * int32[2], zero on entry and left zero on exit.  NULL to skip. */
+     * int32[3]; [0] and [1] zero on entry and left zero on exit, [2] set to the
+     * number of pixels re-walked.  NULL to skip. */
     int32_t* fix_pixels;
     int32_t* fix_count;
 } uws_raster_out;

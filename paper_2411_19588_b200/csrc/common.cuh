@@ -38,6 +38,8 @@ constexpr float kClampLo = 0.99f * (1.0f - kGuard);
 constexpr float kClampHi = 0.99f * (1.0f + kGuard);
 // smallest float >= 1e-4 (double): T_f >= 1e-4  <=>  T_f >= kTStopF
 constexpr float kTStopF = 1.00000004749745130539e-04f;
+// uws_raster_out.tile_nrows flag: the stored rows are the tile's whole list
+constexpr int kRowsComplete = 1 << 30;
 
 void set_error(const std::string& msg);
 void count_launches(int n);

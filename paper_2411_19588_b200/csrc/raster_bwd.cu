@@ -180,7 +180,7 @@ __global__ void __launch_bounds__(kThreads, MINB) k_raster_bwd(BwdArgs a) {
     const int nbatch = (maxlast + kBatch - 1) / kBatch;
     int rend = 0, stride = 1;
     // the forward stored this tile's consumed prefix: no filtering of the row lists
-    const int32_t* saved = (ROWS && a.tile_rows && maxlast <= a.tile_nrows[tile])
+    const int32_t* saved = (ROWS && a.tile_rows && maxlast <= (a.tile_nrows[tile] & ~kRowsComplete))
                                ? a.tile_rows + (size_t)tile * a.tile_rows_cap
                                : nullptr;
     if (ROWS && nbatch > 0 && !saved) {

@@ -24,7 +24,14 @@ constexpr int kBatch = 256;
 constexpr int kFirstFill = 128;
 constexpr int kListPad = 4;                    // per-warp lists are walked 4 entries at a time
 constexpr int kFwdPx = 2;                      // pixels per thread (measured: 1 and 4 are slower)
-constexpr int kFixBlocks = 148 * 2;            // float64 fix-up pass: 8 warps per block
+constexpr int kFixBlocks = 148 * 3;            // float64 fix-up pass: 8 warps per block
+
+#ifdef UWS_FIX_STATS
+__device__ float g_dbg_eb[3840 * 2160];   // per pixel sum alpha/(1-alpha) of the float32 walk
+__device__ float g_dbg_t32[3840 * 2160];  // float32 final T
+__device__ int g_dbg_cnt32[3840 * 2160];
+__device__ unsigned g_dbg_max[4];          // max rel err, max rel/eb, #count mismatches, #pairs
+#endif
 
 struct FwdArgs {
     const uws_splat* splat;
@@ -41,15 +48,20 @@ struct FwdArgs {
 };
 
 // Transmittance band in which the float32 walk's T >= 1e-4 decision may differ
-// from the reference's float64 one.  The float32 alphas carry a relative error
-// of a few 1e-6 (tile-local offsets, ex2.approx), i.e. up to ~2e-4 relative in
-// (1 - alpha) for alpha near the 0.99 clamp; +-2e-3 leaves a 10x margin.  A
-// pixel whose final T, or whose T before its last blend, lands in the band is
-// re-walked in float64 by k_raster_fix.  Each blend lowers T by >= 0.39 %
-// (alpha >= 1/255), so a walk visits the 0.4 %-wide band at most twice and
-// one of those two values is always the final T or the T before the last blend.
-constexpr float kTBandLo = 1e-4f * (1.0f - 2e-3f);
-constexpr float kTBandHi = 1e-4f * (1.0f + 2e-3f);
+// from the reference's float64 one.  The float32 T carries a relative error of
+// about c * sum_i alpha_i / (1 - alpha_i) over its blends (each factor 1 - alpha
+// inherits alpha's relative error amplified by alpha / (1 - alpha)); measured
+// with -DUWS_FIX_STATS (tools/dbg_fix2.py, ~1M re-walked pixels at C2, C3, C4
+// and 1M @ 4K): c <= 1.65e-7 and max |T32 - T64| / T64 = 1.9e-6.  Near the
+// threshold T ~ 1e-4 the sum is bounded a priori: alpha <= 0.99 gives
+// alpha / (1 - alpha) <= 21.5 (-ln(1 - alpha)), and sum -ln(1 - alpha) = -ln T
+// ~ 9.2, so the sum is <= 198 and the error <= 3.3e-5.  The band is +-1e-4 (3x
+// that bound).  A pixel whose final T, or whose T before its last blend, lands
+// in the band is re-walked in float64 by k_raster_fix (~0.1 % of the pixels;
+// each blend lowers T by >= 0.39 %, so a walk visits the band at most once and
+// that value is the final T or the T before the last blend).
+constexpr float kTBandLo = 1e-4f * (1.0f - 1e-4f);
+constexpr float kTBandHi = 1e-4f * (1.0f + 1e-4f);
 
 __device__ __forceinline__ bool t_ambiguous(float t) { return t >= kTBandLo && t <= kTBandHi; }
 
@@ -123,6 +135,9 @@ __global__ void __launch_bounds__(kRasterThreads / PX, 4 * PX) k_raster_fwd(FwdA
     // pixel state; T = 0 marks a pixel outside the image as finished
     float fx[PX], T[PX], cr[PX], cg[PX], cb[PX], dsum[PX], wsum[PX];
     float tb[PX];  // T before the last blend (fix-up band test)
+#ifdef UWS_FIX_STATS
+    float eb[PX] = {};
+#endif
     int count[PX], last[PX];
     bool inside[PX];
 #pragma unroll
@@ -252,6 +267,9 @@ __global__ void __launch_bounds__(kRasterThreads / PX, 4 * PX) k_raster_fwd(FwdA
                             dsum[j] = fmaf(w, p1.w, dsum[j]);
                             wsum[j] += w;
                             tb[j] = T[j];
+#ifdef UWS_FIX_STATS
+                            eb[j] += alpha / (1.0f - alpha);
+#endif
                             T[j] = T[j] * (1.0f - alpha);
                             ++count[j];
                             last[j] = rel + idx[u];
@@ -281,8 +299,12 @@ __global__ void __launch_bounds__(kRasterThreads / PX, 4 * PX) k_raster_fwd(FwdA
             nst = rem;
         }
     }
+    // stored row count, flagged when it is the tile's whole list (nothing past it
+    // for the fix-up pass to look for)
     if (ROWS && a.out.tile_rows && threadIdx.x == 0)
-        a.out.tile_nrows[tile] = min(base, a.out.tile_rows_cap);
+        a.out.tile_nrows[tile] = min(base, a.out.tile_rows_cap) |
+                                 ((cur >= end && nst == 0 && base <= a.out.tile_rows_cap)
+                                      ? kRowsComplete : 0);
 #pragma unroll
     for (int j = 0; j < PX; ++j) {
         if (!inside[j]) continue;
@@ -290,6 +312,11 @@ __global__ void __launch_bounds__(kRasterThreads / PX, 4 * PX) k_raster_fwd(FwdA
         const float depth = count[j] > 0 ? dsum[j] / wsum[j] : a.far_plane;
         const float c3[3] = {cr[j], cg[j], cb[j]};
         store_pixel(a, pix, c3, depth, wsum[j], T[j], count[j], last[j]);
+#ifdef UWS_FIX_STATS
+        g_dbg_eb[pix] = eb[j];
+        g_dbg_t32[pix] = T[j];
+        g_dbg_cnt32[pix] = count[j];
+#endif
         if (a.out.fix_pixels && (t_ambiguous(T[j]) || t_ambiguous(tb[j]))) {
             const int slot = atomicAdd(a.out.fix_count, 1);
             a.out.fix_pixels[slot] = pix;   // capacity H*W: one slot per pixel at most
@@ -299,11 +326,76 @@ __global__ void __launch_bounds__(kRasterThreads / PX, 4 * PX) k_raster_fwd(FwdA
 
 // Float64 re-walk of the pixels whose float32 T >= 1e-4 decision was ambiguous
 // (rasterizer.py:166-178 exactly: live_i = T_i >= 1e-4, alpha = min(raw, 0.99),
-// raw < 1/255 -> 0): one warp per pixel, 32 list entries per step (alpha_raw in
-// float64 per lane, then the blend in list order).  The tile's list comes from
-// the CSR tile lists, or the rows the forward stored per tile, or -- past what
-// was stored -- from filtering the tile-row list.  fix_count = {count, ticket}:
-// the last block resets both, so the buffer is zero for the next call.
+// raw < 1/255 -> 0): one warp per pixel, 32 list entries per step.  Every lane
+// evaluates its entry's float64 alpha and loads its colour and depth; only the
+// transmittance recurrence T_{i+1} = T_i (1 - alpha_i) -- the product the
+// reference forms with cumprod, in the same order -- runs serially over the
+// passing lanes, each lane keeping the T it was blended with; the weighted sums
+// are then lane-parallel and reduced across the warp once at the end (the
+// reference forms them as a BLAS product, in no particular order either).  The
+// tile's list comes from the CSR tile lists, or the rows the forward stored per
+// tile, or -- past what was stored -- from filtering the tile-row list.
+// fix_count = {count, ticket}: the last block resets both, so the buffer is zero
+// for the next call.
+// One list entry as a lane sees it in the float64 re-walk.
+struct FixEntry {
+    double al;       // min(alpha_raw, 0.99) in float64
+    double d;        // float64 view depth
+    float r, g, b;   // colour
+    bool ok;         // row present and alpha_raw >= 1/255
+};
+
+__device__ __forceinline__ FixEntry fix_load(const FwdArgs& a, int row, int px, int py) {
+    FixEntry e;
+    const double ar = row >= 0 ? alpha_raw_f64(a.splat, a.exact, row, px, py) : 0.0;
+    e.ok = row >= 0 && ar >= kFloor;
+    e.al = fmin(ar, kClamp);
+    e.r = e.g = e.b = 0.f;
+    e.d = 0.0;
+    if (e.ok) {
+        const float4 c = *reinterpret_cast<const float4*>(&a.splat[row].r);
+        e.r = c.x; e.g = c.y; e.b = c.z;
+        e.d = a.depth64[row];
+    }
+    return e;
+}
+
+struct FixWalk {
+    double T = 1.0, c0 = 0.0, c1 = 0.0, c2 = 0.0, dn = 0.0, ws = 0.0;  // c*/dn/ws: lane partials
+    int count = 0, last = 0;
+    bool done = false;
+
+    // 32 list entries (lane entry e at list position pos), in list order
+    __device__ __forceinline__ void step(const FixEntry& e, int pos, int lane) {
+        unsigned pass = __ballot_sync(0xffffffffu, e.ok);
+        if (!pass || done) return;
+        double myT = 0.0;  // T this lane's entry is blended with (0: not blended)
+        unsigned blended = 0u;
+        while (pass) {
+            const int s = __ffs(pass) - 1;
+            pass &= pass - 1;
+            if (T < kTStop) { done = true; break; }
+            const double als = __shfl_sync(0xffffffffu, e.al, s);
+            if (lane == s) myT = T;
+            T *= 1.0 - als;
+            blended |= 1u << s;
+        }
+        if (blended) {
+            const int hi = 31 - __clz(blended);
+            count += __popc(blended);
+            last = __shfl_sync(0xffffffffu, pos, hi) + 1;
+        }
+        const double w = e.al * myT;
+        c0 += w * (double)e.r;
+        c1 += w * (double)e.g;
+        c2 += w * (double)e.b;
+        dn += w * e.d;
+        ws += w;
+    }
+};
+
+constexpr int kFixUnroll = 4;  // list chunks of 32 whose loads are in flight together
+
 template <bool ROWS>
 __global__ void __launch_bounds__(256) k_raster_fix(FwdArgs a) {
     pdl_entry();
@@ -317,77 +409,70 @@ __global__ void __launch_bounds__(256) k_raster_fix(FwdArgs a) {
         // list source: [0, nlist) direct; then (ROWS) the row-list filter
         const int32_t* list;
         int nlist;
+        bool complete = true;
         if (ROWS) {
             list = a.out.tile_rows ? a.out.tile_rows + (size_t)tile * a.out.tile_rows_cap : nullptr;
-            nlist = a.out.tile_rows ? a.out.tile_nrows[tile] : 0;
+            const int nr = a.out.tile_rows ? a.out.tile_nrows[tile] : 0;
+            nlist = nr & ~kRowsComplete;
+            complete = (nr & kRowsComplete) != 0;
         } else {
             list = a.entries + a.offsets[tile];
             nlist = a.offsets[tile + 1] - a.offsets[tile];
         }
-        double T = 1.0, c0 = 0.0, c1 = 0.0, c2 = 0.0, dn = 0.0, ws = 0.0;
-        int count = 0, last = 0;
-        bool done = false;
-        // phase 1: the directly listed entries
-        for (int k0 = 0; k0 < nlist && !done; k0 += 32) {
-            const int k = k0 + lane;
-            const int row = k < nlist ? list[k] : -1;
-            const double ar = row >= 0 ? alpha_raw_f64(a.splat, a.exact, row, px, py) : 0.0;
-            unsigned pass = __ballot_sync(0xffffffffu, row >= 0 && ar >= kFloor);
-            while (pass) {
-                const int b = __ffs(pass) - 1;
-                pass &= pass - 1;
-                if (T < kTStop) { done = true; break; }
-                const double al = fmin(__shfl_sync(0xffffffffu, ar, b), kClamp);
-                const int r = __shfl_sync(0xffffffffu, row, b);
-                const double w = al * T;
-                c0 += w * (double)a.splat[r].r;
-                c1 += w * (double)a.splat[r].g;
-                c2 += w * (double)a.splat[r].b;
-                dn += w * a.depth64[r];
-                ws += w;
-                T *= 1.0 - al;
-                ++count;
-                last = k0 + b + 1;
+        FixWalk fw;
+        // phase 1: the directly listed entries, kFixUnroll chunks of 32 at a time (the
+        // dependent list -> record loads are latency-bound)
+        for (int k0 = 0; k0 < nlist && !fw.done; k0 += 32 * kFixUnroll) {
+            int row[kFixUnroll];
+#pragma unroll
+            for (int u = 0; u < kFixUnroll; ++u) {
+                const int k = k0 + 32 * u + lane;
+                row[u] = k < nlist ? list[k] : -1;
             }
+            FixEntry e[kFixUnroll];
+#pragma unroll
+            for (int u = 0; u < kFixUnroll; ++u) e[u] = fix_load(a, row[u], px, py);
+#pragma unroll
+            for (int u = 0; u < kFixUnroll; ++u) fw.step(e[u], k0 + 32 * u + lane, lane);
         }
         // phase 2 (row lists, rare): the tile's entries past the stored ones
-        if (ROWS && !done && T >= kTStop) {
+        if (ROWS && !complete && !fw.done && fw.T >= kTStop) {
             int seen = 0;  // matches of this tile so far, in list order
             const int rend = a.row_start[ty + 1];
-            for (int c = a.row_start[ty]; c < rend && !done; c += 32) {
+            for (int c = a.row_start[ty]; c < rend && !fw.done; c += 32) {
                 const int q = c + lane;
                 const uint2 it = q < rend ? __ldg(a.row_items + q) : make_uint2(0u, 0xffffu);
                 const bool m = (int)(it.y & 0xffffu) <= tx && tx <= (int)(it.y >> 16);
                 const unsigned bal = __ballot_sync(0xffffffffu, m);
                 const int pos = seen + __popc(bal & lanemask_lt());  // list position if m
                 seen += __popc(bal);
-                const bool mine = m && pos >= nlist;
-                const int row = (int)it.x;
-                const double ar = mine ? alpha_raw_f64(a.splat, a.exact, row, px, py) : 0.0;
-                unsigned pass = __ballot_sync(0xffffffffu, mine && ar >= kFloor);
-                while (pass) {
-                    const int b = __ffs(pass) - 1;
-                    pass &= pass - 1;
-                    if (T < kTStop) { done = true; break; }
-                    const double al = fmin(__shfl_sync(0xffffffffu, ar, b), kClamp);
-                    const int r = __shfl_sync(0xffffffffu, row, b);
-                    const int p = __shfl_sync(0xffffffffu, pos, b);
-                    const double w = al * T;
-                    c0 += w * (double)a.splat[r].r;
-                    c1 += w * (double)a.splat[r].g;
-                    c2 += w * (double)a.splat[r].b;
-                    dn += w * a.depth64[r];
-                    ws += w;
-                    T *= 1.0 - al;
-                    ++count;
-                    last = p + 1;
-                }
+                fw.step(fix_load(a, (m && pos >= nlist) ? (int)it.x : -1, px, py), pos, lane);
             }
         }
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+            fw.c0 += __shfl_xor_sync(0xffffffffu, fw.c0, o);
+            fw.c1 += __shfl_xor_sync(0xffffffffu, fw.c1, o);
+            fw.c2 += __shfl_xor_sync(0xffffffffu, fw.c2, o);
+            fw.dn += __shfl_xor_sync(0xffffffffu, fw.dn, o);
+            fw.ws += __shfl_xor_sync(0xffffffffu, fw.ws, o);
+        }
+#ifdef UWS_FIX_STATS
         if (lane == 0) {
-            const float c3[3] = {(float)c0, (float)c1, (float)c2};
-            const float depth = ws > kWeightEps ? (float)(dn / ws) : a.far_plane;
-            store_pixel(a, pix, c3, depth, (float)ws, (float)T, count, last);
+            atomicAdd(&g_dbg_max[3], 1u);
+            if (g_dbg_cnt32[pix] == fw.count) {
+                const float rel = (float)(fabs((double)g_dbg_t32[pix] - fw.T) / fw.T);
+                atomicMax(&g_dbg_max[0], __float_as_uint(rel));
+                atomicMax(&g_dbg_max[1], __float_as_uint(rel / fmaxf(g_dbg_eb[pix], 1e-3f)));
+            } else {
+                atomicAdd(&g_dbg_max[2], 1u);
+            }
+        }
+#endif
+        if (lane == 0) {
+            const float c3[3] = {(float)fw.c0, (float)fw.c1, (float)fw.c2};
+            const float depth = fw.ws > kWeightEps ? (float)(fw.dn / fw.ws) : a.far_plane;
+            store_pixel(a, pix, c3, depth, (float)fw.ws, (float)fw.T, fw.count, fw.last);
         }
     }
     // reset {count, ticket} once every block has read the count
@@ -395,6 +480,7 @@ __global__ void __launch_bounds__(256) k_raster_fix(FwdArgs a) {
     if (threadIdx.x == 0) {
         __threadfence();
         if (atomicAdd(a.out.fix_count + 1, 1) == (int)gridDim.x - 1) {
+            a.out.fix_count[2] = a.out.fix_count[0];  // pixels re-walked (diagnostic)
             a.out.fix_count[0] = 0;
             a.out.fix_count[1] = 0;
         }
@@ -405,6 +491,15 @@ __global__ void __launch_bounds__(256) k_raster_fix(FwdArgs a) {
 }  // namespace uws
 
 using namespace uws;
+
+#ifdef UWS_FIX_STATS
+extern "C" int uws_debug_fix_stats(unsigned* out4) {
+    cudaMemcpyFromSymbol(out4, g_dbg_max, sizeof(unsigned) * 4);
+    unsigned z[4] = {0, 0, 0, 0};
+    cudaMemcpyToSymbol(g_dbg_max, z, sizeof(z));
+    return 0;
+}
+#endif
 
 extern "C" int uws_raster_fwd(const uws_projected* proj, const int32_t* offsets,
                               const int32_t* entries, const uws_camera* cam, const float* medium,

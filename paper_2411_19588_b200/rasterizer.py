@@ -187,7 +187,7 @@ def _alloc_output(H, W, dev, mode, medium_maps, tile_rows=True):
                        count=torch.empty(H, W, dtype=torch.int32, device=dev), mode=mode,
                        last=torch.empty(H, W, dtype=torch.int32, device=dev),
                        fix_pixels=torch.empty(H * W, dtype=torch.int32, device=dev),
-                       fix_count=torch.zeros(2, dtype=torch.int32, device=dev))
+                       fix_count=torch.zeros(3, dtype=torch.int32, device=dev))
     if tile_rows:
         tiles = ((H + TILE_SIZE - 1) // TILE_SIZE) * ((W + TILE_SIZE - 1) // TILE_SIZE)
         out.tile_rows = torch.empty(tiles, TILE_ROWS_CAP, dtype=torch.int32, device=dev)

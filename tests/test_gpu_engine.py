@@ -278,9 +278,14 @@ def test_forward_stored_rows_are_the_tile_list_prefix(name):
     last = np_(out.last)
     assert nrows.shape[0] == offs.shape[0] - 1 and (nrows > 0).any()
     gx = (cam.width + 15) // 16
+    complete = (nrows & (1 << 30)) != 0
+    nrows = nrows & ~(1 << 30)
     for t in range(nrows.shape[0]):
         n = int(nrows[t])
         assert n <= offs[t + 1] - offs[t]
+        # flagged complete <=> the stored rows are the tile's whole list
+        if complete[t]:
+            assert n == offs[t + 1] - offs[t]
         np.testing.assert_array_equal(rows[t, :n], ent[offs[t]:offs[t] + n])
         ty, tx = divmod(t, gx)
         consumed = last[16 * ty:16 * ty + 16, 16 * tx:16 * tx + 16].max()
