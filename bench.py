@@ -1,20 +1,24 @@
 """Benchmark of the underwater-3DGS training step (BASELINE.json metric).
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl b200|reference]
+                    [--config c3|c4]
 
 Workload (BASELINE.json configs[2], the config the headline metric is quoted
 on): 1M Gaussians, 1920x1080, one full training step = render (underwater)
 + L1/D-SSIM loss + backward + Adam, synthetic scene from the survey generator
-(SURVEY §8d), random-init parameters, U(0,1) ground truth.  With N GPUs
-(torchrun, one process per GPU) every rank renders its own view of the
-replicated 1M-Gaussian cloud, gradients are summed with one NCCL all-reduce
-and every rank applies the same Adam step: weak scaling, value = all ranks'
-pixels / max-over-ranks step time.
+(SURVEY 8d), random-init parameters, U(0,1) ground truth.  With N GPUs every
+rank renders its own view of the replicated cloud, gradients are summed with
+one NCCL all-reduce and every rank applies the same Adam step: weak scaling,
+value = all ranks' pixels / max-over-ranks step time.  ``--gpus N`` outside
+torchrun launches the N ranks itself (torch.distributed.run on 127.0.0.1);
+under torchrun it must equal WORLD_SIZE.  ``--config c4`` is BASELINE.json
+configs[3]: 3M Gaussians and a 64-view batch sharded 64/N views per GPU
+(strong scaling).
 
-``--impl reference`` times the reference's CPU algorithm (the float64 numpy
-oracle port in oracle/, the reference itself being pure Python that cannot be
-shipped to the GPU box) on the host cores, on a bounded per-step sample of the
-same workload, extrapolated to a full step.
+``--impl reference`` times the reference's own CPU implementation (the
+unmodified ``uwsplat`` installed in baseline/_ref; the float64 numpy port in
+oracle/ when that is absent) on the host cores, on a bounded per-step sample
+of the same workload, extrapolated to a full step.
 """
 
 from __future__ import annotations
@@ -156,6 +160,91 @@ class ClockSampler:
 
 
 # ----------------------------------------------------------------------------
+# workloads and the N-GPU launcher
+# ----------------------------------------------------------------------------
+CONFIGS = {
+    # name: (Gaussians, views per step (None = one per rank), scaling)
+    "c3": (N_GAUSS, None, "weak"),
+    "c4": (3_000_000, 64, "strong"),
+}
+
+
+def c4_eye(k, nviews=64):
+    """SURVEY 8d C4 camera ring: eye_k = (3 cos t, 2 sin t, -1), t = 2 pi k / 64."""
+    th = 2 * np.pi * k / nviews
+    return (3.0 * np.cos(th), 2.0 * np.sin(th), -1.0)
+
+
+def workload_config(world, name, n_gauss, views_per_step):
+    if name.upper() == "C4":
+        wl = (f"C4: {n_gauss // 10**6}M Gaussians 1920x1080, {views_per_step}-view batch "
+              f"sharded {views_per_step // world} views per GPU, gradient all-reduce + one Adam "
+              "step per batch")
+    else:
+        wl = ("C3: 1M Gaussians 1920x1080 underwater training step (render+loss+backward+Adam) "
+              "per GPU, view-sharded")
+    return {"workload": wl, "gaussians": n_gauss, "width": W, "height": H,
+            "views_per_step": views_per_step,
+            "parallelism": f"view-sharded dp{world} + NCCL all-reduce",
+            "l2": "working set > L2 (params + Adam state >= 168 MB, tile-row lists, 25 MB "
+                  "ground truth per view); no flush"}
+
+
+def free_port():
+    import socket
+    with socket.socket() as so:
+        so.bind(("127.0.0.1", 0))
+        return so.getsockname()[1]
+
+
+def launch_ranks(args):
+    """--gpus N > 1 outside torchrun: re-launch this script with N ranks (one per GPU)
+    through torch.distributed.run on 127.0.0.1 and return its exit code; None when this
+    process is already the (single or torchrun-launched) rank."""
+    world_env = os.environ.get("WORLD_SIZE")
+    if world_env is not None:
+        if int(world_env) != args.gpus:
+            raise SystemExit(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={world_env}")
+        return None
+    if args.gpus <= 1:
+        return None
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+           f"--nproc-per-node={args.gpus}", "--master-addr", "127.0.0.1",
+           "--master-port", str(free_port()), os.path.abspath(__file__)] + sys.argv[1:]
+    return subprocess.call(cmd)
+
+
+def run_dry(args):
+    """--dry-run: the launcher, process group, barriers and max-over-ranks timing of
+    the GPU arm, on CPU with gloo and no kernels (tests the harness, not the GPU)."""
+    import torch
+    import torch.distributed as dist
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    if world > 1:
+        dist.init_process_group("gloo")
+    for _ in range(args.warmup):
+        np.sort(np.random.default_rng(rank).uniform(size=1 << 16))
+    if world > 1:
+        dist.barrier()
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        np.sort(np.random.default_rng(rank).uniform(size=1 << 16))
+    ms = (time.perf_counter() - t0) * 1e3
+    if world > 1:
+        t = torch.tensor([ms], dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+        dist.barrier()
+        dist.destroy_process_group()
+    if rank != 0:
+        return None
+    return {"metric": METRIC, "dry_run": True, "value": None, "unit": "Mpixels/s",
+            "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": round(ms / max(args.steps, 1), 4), "ranks_timed": world}
+
+
+# ----------------------------------------------------------------------------
 # GPU arm
 # ----------------------------------------------------------------------------
 class StageTimer:
@@ -197,6 +286,29 @@ class StageTimer:
         return out
 
 
+class Snapshot:
+    """Device copy of everything a training step mutates, so every timed phase (and
+    the workload statistics) starts from the same scene."""
+
+    def __init__(self, state):
+        self.state = state
+        self.tensors = [t.clone() for t in self._live()]
+        self.steps = {k: v.step for k, v in state.adam.items()}
+        self.iteration = state.iteration
+
+    def _live(self):
+        s = self.state
+        return [s.cloud.flat, s.medium.flat, s.exp_avg, s.exp_avg_sq, s.medium_exp_avg,
+                s.medium_exp_avg_sq, s.grad_accum, s.obs_count]
+
+    def restore(self):
+        for dst, src in zip(self._live(), self.tensors):
+            dst.copy_(src)
+        for k, v in self.state.adam.items():
+            v.step = self.steps[k]
+        self.state.iteration = self.iteration
+
+
 def run_gpu(args):
     import torch
     import torch.distributed as dist
@@ -207,6 +319,9 @@ def run_gpu(args):
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     if world > 1:
+        # communicator set-up in the log: one "nranks N" line per rank
+        os.environ.setdefault("NCCL_DEBUG", "INFO")
+        os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
         dist.init_process_group("nccl", device_id=dev)
 
     import paper_2411_19588_b200 as uw
@@ -216,27 +331,56 @@ def run_gpu(args):
     timer.wrap(_lib)
     lib = _lib.load()
 
-    host = synthetic_cloud(N_GAUSS)
+    n_gauss, views_total, scaling = CONFIGS[args.config]
+    if views_total is None:        # C3: one view per rank, every rank its own camera
+        eyes = [view_eye(rank)]
+        views_total = world
+    else:                          # C4: the 64-view ring, round-robin over the ranks
+        if views_total % world:
+            raise SystemExit(f"{views_total} views do not shard over {world} GPUs")
+        eyes = [c4_eye(k, views_total) for k in range(rank, views_total, world)]
+    host = synthetic_cloud(n_gauss)
     cloud = uw.GaussianCloud(**host)
     medium = uw.MediumParams(**MEDIUM)
     state = uw.TrainState(cloud, medium, iteration=1)
     cfg = uw.OptimConfig()
-    trainer = uw.ViewShardedTrainer(state, cfg, W, H)
-    cam = uw.Camera.look_at(view_eye(rank), (0, 0, 12), width=W, height=H, fx=1.2 * W, fy=1.2 * W)
-    gt_host = torch.from_numpy(gt_image(rank)).pin_memory()
-    gt_dev = gt_host.to(dev)
+    trainer = uw.ViewShardedTrainer(state, cfg, W, H, views_per_rank=len(eyes))
+    cams = [uw.Camera.look_at(e, (0, 0, 12), width=W, height=H, fx=1.2 * W, fy=1.2 * W)
+            for e in eyes]
+    cam = cams[0]
+    seeds = [rank] if args.config == "c3" else list(range(rank, views_total, world))
+    gt_host = [torch.from_numpy(gt_image(sd)).pin_memory() for sd in seeds]
+    gt_dev = [g.to(dev) for g in gt_host]
+    snap = Snapshot(state)
+
+    # all-reduce time: CUDA events around the gradient all-reduce (stage-timer pass)
+    eng = trainer.engine
+    ar_events = []
+    orig_ar = eng._all_reduce_gradients
+
+    def timed_all_reduce():
+        if not timer.enabled:
+            return orig_ar()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        r = orig_ar()
+        e1.record()
+        ar_events.append((e0, e1))
+        return r
+
+    eng._all_reduce_gradients = timed_all_reduce
 
     # Steps are pipelined (StepEngine.step_async): step i is launched before the
     # host reads step i-1's result record (loss, finite/overflow flags, list sizes),
     # so the GPU never waits for the host; the last record is read by flush().
     def step_resident():
-        trainer.step_async([(cam, gt_dev)], sharded=True)
+        trainer.step_async(list(zip(cams, gt_dev)), sharded=True)
         state.iteration += 1
 
     def step_e2e():
         # ground truth from pinned host memory every step: the engine copies it on
         # its copy stream while the previous step's kernels run
-        trainer.step_async([(cam, gt_host)], sharded=True)
+        trainer.step_async(list(zip(cams, gt_host)), sharded=True)
         state.iteration += 1
 
     def barrier():
@@ -268,18 +412,26 @@ def run_gpu(args):
 
     for _ in range(args.warmup):
         step_resident()
+    trainer.flush()
+    snap.restore()
     clocks = ClockSampler(local)
     with clocks:
         ms, launches = timed(step_resident, args.steps)
     # per-stage breakdown from a separate run with CUDA events around every C-ABI
     # call (kept out of the timed region above)
+    snap.restore()
     timed(step_resident, args.steps, stage_timer=True)
     stages = timer.totals()
     gaps = timer.gaps()
+    allreduce_ms = (sum(a.elapsed_time(b) for a, b in ar_events) / args.steps) if ar_events else 0.0
+    snap.restore()
     for _ in range(max(2, args.warmup // 2)):   # both pipeline slots warm
         step_e2e()
+    trainer.flush()
+    snap.restore()
     ms_e2e, _ = timed(step_e2e, args.steps)
     trainer.flush()
+    snap.restore()
 
     # render FPS (BASELINE.json's second metric): the forward alone -- preprocess,
     # depth sort, tile-row lists, compositing with the medium epilogue -- per frame
@@ -287,7 +439,7 @@ def run_gpu(args):
     # read once the next frame is queued), at C3 and at C5's 1M Gaussians @ 3840x2160
     render_fps = {}
     for name, (rw, rh) in ((("C3 1M 1920x1080", (W, H)), ("C5 1M 3840x2160", (3840, 2160)))
-                           if not args.no_render_fps else ()):
+                           if not (args.no_render_fps or args.config != "c3") else ()):
         eng = trainer.engine if (rw, rh) == (W, H) else uw.StepEngine(state, rw, rh, cfg)
         rcam = uw.Camera.look_at(view_eye(rank), (0, 0, 12), width=rw, height=rh,
                                  fx=1.2 * rw, fy=1.2 * rw)
@@ -311,8 +463,9 @@ def run_gpu(args):
     # dark-pixel estimate from the C3 ground truth and the engine's render depth,
     # including the host read of the 96-byte result record (untimed for the step)
     refresh_ms = None
-    if not args.no_render_fps:
+    if not args.no_render_fps and args.config == "c3":
         depth_raw = trainer.engine.out.depth
+        gt_dev = gt_dev[0]
         for _ in range(2):
             uw.estimate_backscatter(gt_dev, depth_raw, depth_is_raw=True)
         barrier()
@@ -325,13 +478,16 @@ def run_gpu(args):
         refresh_ms = round(t0.elapsed_time(t1) / 5, 4)
     torch.cuda.empty_cache()
 
-    px_step = W * H * world
+    px_step = W * H * views_total
     value = px_step * args.steps / (ms / 1e3) / 1e6
     e2e = px_step * args.steps / (ms_e2e / 1e3) / 1e6
 
-    # workload statistics for the roofline (untimed)
+    # workload statistics for the roofline (untimed), on the scene every timed
+    # phase started from (the snapshot), view 0 of this rank
+    snap.restore()
     out = uw.render(cloud, cam, medium, "underwater")
     k_vis = len(out.proj)
+    s_items = int(out.rows.items.shape[0])
     e_ent = int(out.bins.entries.numel())
     last = out.last.view(-1).long()
     term = (out.final_transmittance.view(-1) < 1e-4)
@@ -342,8 +498,11 @@ def run_gpu(args):
     tid = ys * gx + xs
     m_tile = (offs[1:] - offs[:-1])[tid]
     p_pix = int(torch.where(term, last, m_tile).sum().item())
+    # per launch: per-view stages run views-per-rank times a step, Adam once
     per_step = {k: v / args.steps for k, v in stages.items()}
-    canon = {k: k.replace("_rows", "") for k in per_step}  # row-list variants: same work
+    per_launch = {k: v / len(timer.events[k]) for k, v in stages.items()}
+    canon = {k: ("uws_raster_fwd" if k == "uws_raster_fwd_rows" else
+                 "uws_raster_bwd" if k == "uws_raster_bwd_rows" else k) for k in per_step}
     total_stage = sum(per_step.values())
     fwd_flops = 30.0 * p_pix
     bwd_flops = 60.0 * p_pix
@@ -358,32 +517,33 @@ def run_gpu(args):
     rf_ms = per_step.get("uws_raster_fwd", float("nan"))
     dominant = max(per_step, key=per_step.get) if per_step else None
     stage_share = {k: round(v / total_stage, 4) for k, v in per_step.items()} if total_stage else {}
+    # algorithmic HBM bytes per launch
     hbm_bytes = {
-        "uws_preprocess_fwd": 56 * N_GAUSS + 48 * k_vis,
+        "uws_preprocess_fwd": 56 * n_gauss + 48 * k_vis,
         "uws_bin_count": 24 * k_vis,
         "uws_bin_emit": 20 * e_ent,
-        "uws_bin_rows": 24 * k_vis,
+        "uws_bin_rows": 12 * k_vis + 8 * s_items,
         "uws_loss_fwd_bwd": 36 * W * H,
-        "uws_preprocess_bwd": 36 * k_vis + 112 * N_GAUSS,
-        "uws_adam_step": 392 * N_GAUSS,
+        "uws_preprocess_bwd": 36 * k_vis + 112 * n_gauss,
+        "uws_adam_step": 392 * n_gauss,
     }
     stage_roofline = {}
-    for k, v in per_step.items():
+    for k, v in per_launch.items():
         if canon[k] in hbm_bytes and v > 0:
             gbs = hbm_bytes[canon[k]] / (v / 1e3) / 1e9
             stage_roofline[k] = {"bound": "hbm", "achieved_gbs": round(gbs, 1),
                                  "frac": round(gbs / hbm_peak, 4), "ms": round(v, 4)}
-    for k in per_step:
+    for k in per_launch:
         fl = {"uws_raster_fwd": fwd_flops, "uws_raster_bwd": bwd_flops}.get(canon[k])
-        if fl is not None and per_step[k] > 0:
-            tf = fl / (per_step[k] / 1e3) / 1e12
+        if fl is not None and per_launch[k] > 0:
+            tf = fl / (per_launch[k] / 1e3) / 1e12
             stage_roofline[k] = {"bound": "fp32", "achieved_tflops": round(tf, 3),
-                                 "frac": round(tf / fp32_peak, 4), "ms": round(per_step[k], 4)}
+                                 "frac": round(tf / fp32_peak, 4), "ms": round(per_launch[k], 4)}
     dom = stage_roofline.get(dominant, {})
     traffic = kernel_traffic(canon.get(dominant))
     if canon.get(dominant) in ("uws_raster_fwd", "uws_raster_bwd"):
         fl = bwd_flops if canon[dominant] == "uws_raster_bwd" else fwd_flops
-        achieved = fl / (per_step[dominant] / 1e3) / 1e12
+        achieved = fl / (per_launch[dominant] / 1e3) / 1e12
         roofline = {"bound": "fp32", "kernel": dominant, "achieved": round(achieved, 3),
                     "peak": round(fp32_peak, 1), "unit": "TFLOP/s",
                     "frac": round(achieved / fp32_peak, 4), "traffic": traffic,
@@ -393,7 +553,7 @@ def run_gpu(args):
                     "work": f"{fl / 1e9:.2f} GFLOP per launch (SURVEY 8d: "
                             f"{'60' if canon[dominant].endswith('bwd') else '30'} flop x P_pix={p_pix})"}
     elif canon.get(dominant) in hbm_bytes:
-        gbs = hbm_bytes[canon[dominant]] / (per_step[dominant] / 1e3) / 1e9
+        gbs = hbm_bytes[canon[dominant]] / (per_launch[dominant] / 1e3) / 1e9
         roofline = {"bound": "hbm", "kernel": dominant, "achieved": round(gbs, 1),
                     "peak": hbm_peak, "unit": "GB/s", "frac": round(gbs / hbm_peak, 4),
                     "traffic": traffic}
@@ -402,19 +562,18 @@ def run_gpu(args):
                     "unit": "GB/s", "frac": None, "traffic": None}
 
     result = {
-        "metric": METRIC, "value": round(value, 3), "unit": "Mpixels/s", "n_gpus": world,
+        "metric": METRIC if args.config == "c3" else
+        "fwd+bwd Mpixels/s at 3M Gaussians 1080p, 64-view batch",
+        "value": round(value, 3), "unit": "Mpixels/s", "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms / args.steps, 4),
-        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
-        "data": "synthetic (survey generator, random-init 1M Gaussians, U(0,1) ground truth)",
-        "config": {"workload": "C3: 1M Gaussians 1920x1080 underwater training step "
-                               "(render+loss+backward+Adam) per GPU, view-sharded",
-                   "gaussians": N_GAUSS, "width": W, "height": H, "views_per_step": world,
-                   "parallelism": f"view-sharded dp{world} + NCCL all-reduce",
-                   "l2": "working set > L2 (params+Adam 168 MB, tile lists ~"
-                         f"{e_ent * 8 / 1e6:.0f} MB); no flush"},
+        "higher_is_better": True, "scaling": scaling, "vs_baseline": None, "dtype": "f32",
+        "data": f"synthetic (survey generator, random-init {n_gauss // 10**6}M Gaussians, "
+                "U(0,1) ground truth)",
+        "config": workload_config(world, args.config.upper(), n_gauss, views_total),
         "e2e": {"value": round(e2e, 3), "unit": "Mpixels/s",
-                "h2d_bytes_per_step": H * W * 3 * 4,
-                "d2h_bytes_per_step": 4 + 8 + 7 * 8},
+                "h2d_bytes_per_step": H * W * 3 * 4 * len(cams),
+                "d2h_bytes_per_step": 8 * (10 * len(cams) + 2)},
+        "allreduce_ms_per_step": round(allreduce_ms, 4),
         "gpu_launches": int(launches),
         "render_fps": render_fps,
         "guidance_refresh_ms": refresh_ms,
@@ -423,10 +582,12 @@ def run_gpu(args):
         "gaps_after_stage_ms": {k: round(v / args.steps, 4) for k, v in gaps.items()},
         "stage_share": stage_share,
         "stage_roofline": stage_roofline,
-        "workload_stats": {"K": k_vis, "E": e_ent, "P_pix": p_pix},
+        "workload_stats": {"K": k_vis, "E": e_ent, "S_row_items": s_items, "P_pix": p_pix,
+                           "scene": "view 0 of rank 0 at the start of every timed phase"},
+        "launches_per_step": {k: len(v) // args.steps for k, v in timer.events.items()},
         "clocks": clocks.summary(),
     }
-    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+    if rank == 0 and world == 1 and args.config == "c3" and not args.no_cpu_baseline:
         result["cpu_baseline"] = cpu_baseline(args.cpu_tiles, report_only=True)
     if world > 1:
         dist.barrier()
@@ -435,105 +596,202 @@ def run_gpu(args):
 
 
 # ----------------------------------------------------------------------------
-# CPU reference arm (oracle port of the reference algorithm)
+# CPU reference arm: the reference's own code (baseline/_ref) when installed,
+# else the float64 numpy port in oracle/
 # ----------------------------------------------------------------------------
-def cpu_step_sample(cloud, cam, medium, gt, tiles_sample, workers, state):
-    """One sampled reference step; returns (extrapolated full-step seconds, details)."""
-    from concurrent.futures import ThreadPoolExecutor
-    from types import SimpleNamespace
+REF_DIR = os.path.join(ROOT, "baseline", "_ref")
 
-    from oracle import uwsplat_oracle as O
 
-    t0 = time.perf_counter()
-    proj = O.project(cloud, cam)
-    t_proj = time.perf_counter() - t0
-    gx, gy = O.grid_dims(cam.width, cam.height)
-    # binning (rasterizer.py:50-85): the entry emission runs on the full frame;
-    # the (tile, depth, source) lexsort runs on the sampled tiles' entries and
-    # is extrapolated linearly in E (n log n in reality: favours the CPU)
-    t0 = time.perf_counter()
-    rect = O.tile_rect(proj.mean2d, proj.radius, (gx, gy))
-    wx = rect[:, 2] - rect[:, 0] + 1
-    cnt = np.maximum(wx, 0) * np.maximum(rect[:, 3] - rect[:, 1] + 1, 0)
-    e_total = int(cnt.sum())
-    owner = np.repeat(np.arange(len(cnt)), cnt)
-    k = np.arange(e_total) - (np.cumsum(cnt) - cnt)[owner]
-    tid = (rect[owner, 1] + k // wx[owner]) * gx + (rect[owner, 0] + k % wx[owner])
-    t_emit = time.perf_counter() - t0
-    sel = np.isin(tid, tiles_sample)
-    owner, tid = owner[sel], tid[sel]
-    t0 = time.perf_counter()
-    perm = np.lexsort((proj.source_index[owner], proj.depth[owner], tid))
-    owner, tid = owner[perm], tid[perm]
-    offsets = np.zeros(gx * gy + 1, np.int64)
-    offsets[1:] = np.cumsum(np.bincount(tid, minlength=gx * gy))
-    entries = owner
-    t_sort = time.perf_counter() - t0
-    e_sample = int(entries.size)
-    t_bin = t_emit + t_sort * e_total / max(e_sample, 1)
-    # per-tile forward + backward on the sample (tile-parallel like the reference)
-    dL = np.zeros((cam.height, cam.width, 3))
+def import_reference():
+    """The UNMODIFIED reference package from baseline/_ref (None when not installed)."""
+    if not os.path.isdir(os.path.join(REF_DIR, "uwsplat")):
+        return None
+    if REF_DIR not in sys.path:
+        sys.path.insert(0, REF_DIR)
+    try:
+        import uwsplat  # noqa: F401
+        from uwsplat import backward, losses, optim, projection, rasterizer, scene  # noqa: F401
+    except Exception:  # noqa: BLE001
+        return None
+    return sys.modules["uwsplat"]
 
-    def fwd(t):
-        ty, tx = divmod(int(t), gx)
-        _, px, py = O._tile_pixels(tx, ty, cam.width, cam.height)
-        rows = entries[offsets[t]:offsets[t + 1]]
-        return O.blend(px, py, proj.mean2d[rows], proj.conic[rows], proj.color[rows],
-                       proj.opacity[rows], proj.depth[rows], float(cam.far))
 
-    def bwd(t):
-        ty, tx = divmod(int(t), gx)
-        (x0, x1, y0, y1), px, py = O._tile_pixels(tx, ty, cam.width, cam.height)
-        rows = entries[offsets[t]:offsets[t + 1]]
-        G = np.full(((y1 - y0) * (x1 - x0), 3), 1e-7)
-        return O.tile_grads(px, py, proj.mean2d[rows], proj.conic[rows], proj.color[rows],
-                            proj.opacity[rows], G)
+class CpuStepSampler:
+    """One bounded sample of the C3 training step on the host cores, through the
+    reference's own functions (``kind="reference"``: project_cloud, bin_and_sort,
+    _composite_block, total_loss, backward_medium, _backward_block,
+    _project_backward, apply_gradients from baseline/_ref) or the oracle port
+    (``kind="port"``).  Full frame: projection, loss, medium backward, projection
+    backward, Adam.  Sampled: the per-tile compositing forward and backward run
+    on ``n_tiles`` seeded tiles (tile-parallel on every core, as the
+    reference's ``workers``) and are scaled by the full frame's tile-list length;
+    the (tile, depth, source) lexsort of bin_and_sort over all E entries is
+    timed once per run and added to every step."""
 
-    with ThreadPoolExecutor(max_workers=workers) as pool:
+    def __init__(self, n_tiles, cores):
+        self.cores = cores
+        self.n_tiles = n_tiles
+        host = synthetic_cloud(N_GAUSS)
+        self.gt = gt_image(0).astype(np.float64)
+        gx, gy = (W + 15) // 16, (H + 15) // 16
+        self.grid = (gx, gy)
+        self.tiles = np.sort(np.random.default_rng(7).choice(gx * gy, n_tiles, replace=False))
+        rng = np.random.default_rng(1)
+        # full-frame stand-ins for the render outputs the loss / medium backward read
+        self.img = rng.uniform(0, 1, (H, W, 3))
+        self.depth = rng.uniform(4, 20, (H, W))
+        self.R = import_reference()
+        self.kind = "reference" if self.R is not None else "port"
+        if self.R is not None:
+            R = self.R
+            self.cloud = R.GaussianCloud(**host)
+            self.cam = R.Camera.look_at(view_eye(0), (0, 0, 12), width=W, height=H,
+                                        fx=1.2 * W, fy=1.2 * W)
+            self.medium = R.MediumParams(**{k: np.asarray(v, np.float32) for k, v in MEDIUM.items()})
+            # Adam runs on a copy: the rendered cloud (and so the tile lists) stays fixed
+            self.state = R.TrainState(self.cloud.copy(), self.medium.copy(), iteration=1)
+            self.cfg = R.OptimConfig()
+            proj = R.project_cloud(self.cloud, self.cam)
+            t0 = time.perf_counter()
+            self.bins = R.bin_and_sort(proj, W, H)
+            self.t_bin = time.perf_counter() - t0
+            self.e_total = int(self.bins.entries.size)
+            lens = np.diff(self.bins.offsets)
+        else:
+            from types import SimpleNamespace
+            from oracle import uwsplat_oracle as O
+            from paper_2411_19588_b200.scene import Camera
+            self.O = O
+            self.cloud = SimpleNamespace(**host)
+            self.cam = Camera.look_at(view_eye(0), (0, 0, 12), width=W, height=H,
+                                      fx=1.2 * W, fy=1.2 * W)
+            self.medium = SimpleNamespace(**{k: np.asarray(v, np.float32) for k, v in MEDIUM.items()})
+            self.adam_state = {}
+            proj = O.project(self.cloud, self.cam)
+            rect = O.tile_rect(proj.mean2d, proj.radius, self.grid)
+            wx = rect[:, 2] - rect[:, 0] + 1
+            cnt = np.maximum(wx, 0) * np.maximum(rect[:, 3] - rect[:, 1] + 1, 0)
+            owner = np.repeat(np.arange(len(cnt)), cnt)
+            k = np.arange(int(cnt.sum())) - (np.cumsum(cnt) - cnt)[owner]
+            tid = (rect[owner, 1] + k // wx[owner]) * gx + (rect[owner, 0] + k % wx[owner])
+            t0 = time.perf_counter()
+            perm = np.lexsort((proj.source_index[owner], proj.depth[owner], tid))
+            self.t_bin = time.perf_counter() - t0
+            owner, tid = owner[perm], tid[perm]
+            offsets = np.zeros(gx * gy + 1, np.int64)
+            offsets[1:] = np.cumsum(np.bincount(tid, minlength=gx * gy))
+            self.bins = SimpleNamespace(offsets=offsets, entries=owner)
+            self.e_total = int(owner.size)
+            lens = np.diff(offsets)
+        self.e_sample = max(int(lens[self.tiles].sum()), 1)
+        self.scale = self.e_total / self.e_sample
+
+    def _tile_box(self, t):
+        ty, tx = divmod(int(t), self.grid[0])
+        return tx * 16, min(tx * 16 + 16, W), ty * 16, min(ty * 16 + 16, H)
+
+    def step(self):
+        """Seconds of one full step (sampled tile work extrapolated) and its breakdown."""
+        from concurrent.futures import ThreadPoolExecutor
+        ref = self.R is not None
+        t = {}
         t0 = time.perf_counter()
-        list(pool.map(fwd, tiles_sample))
-        t_fwd = time.perf_counter() - t0
+        if ref:
+            proj = self.R.project_cloud(self.cloud, self.cam)
+        else:
+            proj = self.O.project(self.cloud, self.cam)
+        t["project"] = time.perf_counter() - t0
+        bins = self.bins
+        far = float(self.cam.far)
+        if ref:
+            from uwsplat.rasterizer import _composite_block, _pixel_centers
+            from uwsplat.backward import _backward_block, _project_backward
+
+        def rows_of(tid):
+            return bins.entries[bins.offsets[tid]:bins.offsets[tid + 1]]
+
+        def fwd(tid):
+            x0, x1, y0, y1 = self._tile_box(tid)
+            r = rows_of(tid)
+            if ref:
+                px, py = _pixel_centers(x0, x1, y0, y1)
+                return _composite_block(px, py, proj.mean2d[r], proj.conic[r], proj.color[r],
+                                        proj.opacity[r], proj.depth[r], far)
+            _, px, py = self.O._tile_pixels(x0 // 16, y0 // 16, W, H)
+            return self.O.blend(px, py, proj.mean2d[r], proj.conic[r], proj.color[r],
+                                proj.opacity[r], proj.depth[r], far)
+
+        G_img = np.full((H, W, 3), 1e-7)
+
+        def bwd(tid):
+            x0, x1, y0, y1 = self._tile_box(tid)
+            r = rows_of(tid)
+            G = G_img[y0:y1, x0:x1].reshape(-1, 3)
+            if ref:
+                px, py = _pixel_centers(x0, x1, y0, y1)
+                return r, _backward_block(px, py, proj.mean2d[r], proj.conic[r], proj.color[r],
+                                          proj.opacity[r], G)
+            _, px, py = self.O._tile_pixels(x0 // 16, y0 // 16, W, H)
+            return r, self.O.tile_grads(px, py, proj.mean2d[r], proj.conic[r], proj.color[r],
+                                        proj.opacity[r], G)
+
+        with ThreadPoolExecutor(max_workers=self.cores) as pool:
+            t0 = time.perf_counter()
+            list(pool.map(fwd, self.tiles))
+            t["fwd_sample"] = time.perf_counter() - t0
+            t0 = time.perf_counter()
+            res = list(pool.map(bwd, self.tiles))
+            t["bwd_sample"] = time.perf_counter() - t0
         t0 = time.perf_counter()
-        list(pool.map(bwd, tiles_sample))
-        t_bwd = time.perf_counter() - t0
-    # full-image loss (the reference evaluates it on the whole frame)
-    img = np.random.default_rng(1).uniform(0, 1, gt.shape)
-    t0 = time.perf_counter()
-    O.total_loss(img, gt, medium, 0.3, 0.1)
-    t_loss = time.perf_counter() - t0
-    # projection backward over all visible rows + Adam over all parameters
-    K = len(proj.depth)
-    rng = np.random.default_rng(2)
-    t0 = time.perf_counter()
-    g = O.world_grads(proj, cam, rng.normal(size=(K, 2)) * 1e-6, rng.normal(size=(K, 3)) * 1e-6,
-                      rng.normal(size=(K, 3)) * 1e-6, rng.normal(size=K) * 1e-6,
-                      len(cloud.positions))
-    t_world = time.perf_counter() - t0
-    t0 = time.perf_counter()
-    for f in ("positions", "log_scales", "rotations", "sh_coeffs", "opacity_logits"):
-        p = getattr(cloud, f)
-        z = state.setdefault(f, (np.zeros_like(p), np.zeros_like(p)))
-        O.adam(p, g["d_" + f], z[0], z[1], 1, 1e-3)
-    t_adam = time.perf_counter() - t0
-    lens = offsets[1:] - offsets[:-1]
-    # scale the sampled per-tile work by the full frame's tile-list length
-    e_in_sample = max(int(lens[np.asarray(tiles_sample)].sum()), 1)
-    scale_tiles = e_total / e_in_sample
-    full = t_proj + t_bin + (t_fwd + t_bwd) * scale_tiles + t_loss + t_world + t_adam
-    return full, dict(project=t_proj, bin_emit=t_emit, bin_sort_sample=t_sort, fwd_sample=t_fwd,
-                      bwd_sample=t_bwd, loss=t_loss, world=t_world, adam=t_adam,
-                      e_total=e_total, e_sample=e_sample, scale=scale_tiles)
+        if ref:
+            _, dL = self.R.total_loss(self.img, self.gt, self.medium, 0.3, 0.1)
+        else:
+            self.O.total_loss(self.img, self.gt, self.medium, 0.3, 0.1)
+        t["loss"] = time.perf_counter() - t0
+        K = len(proj.depth)
+        t0 = time.perf_counter()
+        if ref:
+            from types import SimpleNamespace
+            out = SimpleNamespace(depth=self.depth, color_clean=self.img)
+            self.R.backward_medium(out, dL, self.medium, 0.1)
+            d_color, d_logit = np.zeros((K, 3)), np.zeros(K)
+            d_mean2d, d_conic = np.zeros((K, 2)), np.zeros((K, 3))
+            for r, (dc, dl, dm, dk) in res:      # fixed tile order (backward.py:334-341)
+                np.add.at(d_color, r, dc)
+                np.add.at(d_logit, r, dl)
+                np.add.at(d_mean2d, r, dm)
+                np.add.at(d_conic, r, dk)
+            buf = self.R.GradientBuffer(len(self.cloud))
+            _project_backward(proj, self.cam, d_mean2d, d_conic, d_color, d_logit, buf)
+        else:
+            rng = np.random.default_rng(2)
+            g = self.O.world_grads(proj, self.cam, rng.normal(size=(K, 2)) * 1e-6,
+                                   rng.normal(size=(K, 3)) * 1e-6, rng.normal(size=(K, 3)) * 1e-6,
+                                   rng.normal(size=K) * 1e-6, len(self.cloud.positions))
+        t["backward_world"] = time.perf_counter() - t0
+        t0 = time.perf_counter()
+        if ref:
+            self.R.optim.apply_gradients(self.state, buf, self.cfg)
+        else:
+            for f in ("positions", "log_scales", "rotations", "sh_coeffs", "opacity_logits"):
+                p = getattr(self.cloud, f).copy()
+                z = self.adam_state.setdefault(f, (np.zeros_like(p), np.zeros_like(p)))
+                self.O.adam(p, g["d_" + f], z[0], z[1], 1, 1e-3)
+        t["adam"] = time.perf_counter() - t0
+        full = (t["project"] + self.t_bin + (t["fwd_sample"] + t["bwd_sample"]) * self.scale
+                + t["loss"] + t["backward_world"] + t["adam"])
+        t["bin_sort_once"] = self.t_bin
+        return full, t
 
-
-def cpu_setup():
-    from types import SimpleNamespace
-    host = synthetic_cloud(N_GAUSS)
-    cloud = SimpleNamespace(**host)
-    from paper_2411_19588_b200.scene import Camera
-    cam = Camera.look_at(view_eye(0), (0, 0, 12), width=W, height=H, fx=1.2 * W, fy=1.2 * W)
-    medium = SimpleNamespace(**{k: np.asarray(v, np.float32) for k, v in MEDIUM.items()})
-    gt = gt_image(0).astype(np.float64)
-    return cloud, cam, medium, gt
+    def describe(self):
+        gx, gy = self.grid
+        code = ("the reference's own functions from baseline/_ref (uwsplat 0.1.0, float64 numpy)"
+                if self.kind == "reference" else "float64 numpy port of the reference (oracle/)")
+        return (f"{code}; per step: full projection, loss, medium + projection backward and Adam; "
+                f"per-tile compositing forward/backward on {self.n_tiles} of {gx * gy} seeded tiles "
+                f"({self.cores} threads), scaled by tile-list length (x{self.scale:.0f}); the "
+                f"bin_and_sort lexsort over all {self.e_total} entries timed once "
+                f"({self.t_bin:.1f} s) and added to every step")
 
 
 def cpu_cores():
@@ -545,23 +803,16 @@ def cpu_cores():
 
 def cpu_baseline(n_tiles, report_only=False, steps=1):
     cores = cpu_cores()
-    cloud, cam, medium, gt = cpu_setup()
-    gx, gy = (W + 15) // 16, (H + 15) // 16
-    tiles = np.sort(np.random.default_rng(7).choice(gx * gy, n_tiles, replace=False))
-    state = {}
-    times = []
+    smp = CpuStepSampler(n_tiles, cores)
+    times, det = [], {}
     for _ in range(steps):
-        full, det = cpu_step_sample(cloud, cam, medium, gt, tiles, cores, state)
+        full, det = smp.step()
         times.append(full)
     full = float(np.median(times))
     return {"value": round(W * H / full / 1e6, 6), "unit": "Mpixels/s", "cores": cores,
-            "kind": "port",
-            "sample": (f"float64 numpy oracle of the reference algorithm; full projection, "
-                       f"loss, projection-backward and Adam; binning + per-tile forward/backward "
-                       f"on {n_tiles} of {gx * gy} seeded tiles (tile-parallel, {cores} threads), "
-                       f"extrapolated by tile-list length (x{det['scale']:.0f})"),
+            "kind": smp.kind, "sample": smp.describe(),
             "extrapolated_step_s": round(full, 2),
-            "breakdown_s": {k: round(v, 3) for k, v in det.items() if isinstance(v, float)}}
+            "breakdown_s": {k: round(v, 3) for k, v in det.items()}}
 
 
 def run_reference(args):
@@ -570,50 +821,56 @@ def run_reference(args):
     if rank != 0:
         return None
     cores = cpu_cores()
-    os.environ.setdefault("OMP_NUM_THREADS", str(cores))
-    cloud, cam, medium, gt = cpu_setup()
-    gx, gy = (W + 15) // 16, (H + 15) // 16
-    tiles = np.sort(np.random.default_rng(7).choice(gx * gy, args.cpu_tiles, replace=False))
-    state = {}
+    for v in ("OMP_NUM_THREADS", "OPENBLAS_NUM_THREADS"):
+        os.environ.setdefault(v, str(cores))
+    smp = CpuStepSampler(args.cpu_tiles, cores)
     for _ in range(args.warmup):
-        cpu_step_sample(cloud, cam, medium, gt, tiles, cores, state)
-    times = []
+        smp.step()
+    times, det = [], {}
     for _ in range(args.steps):
-        full, det = cpu_step_sample(cloud, cam, medium, gt, tiles, cores, state)
+        full, det = smp.step()
         times.append(full)
     per_step = float(np.mean(times))
-    value = W * H / per_step / 1e6
+    value = W * H / per_step / 1e6      # one view per step on the host, whatever N is
     return {
         "impl": "reference", "metric": METRIC, "value": round(value, 6), "unit": "Mpixels/s",
         "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": round(per_step * 1e3, 1), "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": "f64",
         "data": "synthetic (survey generator, random-init 1M Gaussians, U(0,1) ground truth)",
-        "config": {"workload": "C3: 1M Gaussians 1920x1080 underwater training step "
-                               "(render+loss+backward+Adam), reference CPU algorithm",
-                   "gaussians": N_GAUSS, "width": W, "height": H},
+        "config": workload_config(world, "C3", N_GAUSS, world),
         "cpu_baseline": {"value": round(value, 6), "unit": "Mpixels/s", "cores": cores,
-                         "kind": "port",
-                         "sample": f"per step: full projection/loss/projection-backward/Adam, "
-                                   f"binning+compositing fwd/bwd on {args.cpu_tiles} of "
-                                   f"{gx * gy} tiles, extrapolated (x{det['scale']:.0f})"},
+                         "kind": smp.kind, "sample": smp.describe(),
+                         "step_time": "extrapolated from the sample (see sample)"},
         "e2e": {"value": round(value, 6), "unit": "Mpixels/s", "h2d_bytes_per_step": 0,
                 "d2h_bytes_per_step": 0},
+        "breakdown_s": {k: round(v, 3) for k, v in det.items()},
     }
 
 
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--config", choices=tuple(CONFIGS), default="c3",
+                    help="c3: 1M Gaussians, one 1080p view per GPU (weak scaling, the headline); "
+                         "c4: 3M Gaussians, 64-view batch sharded over the GPUs (strong)")
+    ap.add_argument("--dry-run", action="store_true",
+                    help="exercise the launcher / process group / timing on CPU (gloo), no GPU")
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", choices=("b200", "reference"), default="b200")
-    ap.add_argument("--cpu-tiles", type=int, default=12)
+    ap.add_argument("--cpu-tiles", type=int, default=100)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-render-fps", action="store_true",
                     help="skip the render-FPS frames (e.g. for a step-only ncu launch list)")
     args = ap.parse_args()
-    res = run_reference(args) if args.impl == "reference" else run_gpu(args)
+    rc = launch_ranks(args)
+    if rc is not None:
+        sys.exit(rc)
+    if args.dry_run:
+        res = run_dry(args)
+    else:
+        res = run_reference(args) if args.impl == "reference" else run_gpu(args)
     if res is not None:
         print(json.dumps(res), flush=True)
 
