@@ -208,6 +208,27 @@ int uws_raster_bwd_rows(const uws_projected* proj, const int32_t* row_start,
                         const uws_raster_out* fwd, const float* dL_dC, float* screen_grads,
                         double* medium_acc, void* stream);
 
+/* Deterministic backward (opt-in): gradients bit-identical from run to run,
+ * like the reference, which merges per-tile partials in tile order
+ * (backward.py:334-341).  uws_raster_bwd_det_prefix writes each
+ * tile's consumed list prefix (max of fwd->last over its pixels) to
+ * tile_count [tiles] and their exclusive prefix to tile_base [tiles+1]
+ * (tile_base[tiles] = R, the slot count).  uws_raster_bwd_det then runs the
+ * backward kernel writing every (tile, Gaussian) partial to its own slot,
+ * sorts the slots by row (stable) and sums each row's partials in tile order
+ * into screen_grads (+=); the per-tile medium partials are summed in tile
+ * order into medium_acc (+=).  Exactly one of offsets/entries (tile lists) or
+ * row_start/row_items (row lists) is given; k = visible rows (proj->num_visible). */
+int uws_raster_bwd_det_prefix(const uws_camera* cam, const uws_raster_out* fwd,
+                              int32_t* tile_count, int32_t* tile_base, void* stream);
+int uws_raster_bwd_det_workspace_size(int32_t tiles, int64_t r, int64_t k, size_t* bytes);
+int uws_raster_bwd_det(const uws_projected* proj, const int32_t* offsets, const int32_t* entries,
+                       const int32_t* row_start, const void* row_items, const uws_camera* cam,
+                       const float* medium, const uws_raster_out* fwd, const float* dL_dC,
+                       float* screen_grads, double* medium_acc, const int32_t* tile_base,
+                       int64_t r, int64_t k, void* workspace, size_t workspace_bytes,
+                       void* stream);
+
 /* ---- projection backward (replaces backward._project_backward :184-258 and
  *      _quat_backward :166-181).  grads: float32 flat buffer laid out as
  *      [positions 3n | log_scales 3n | rotations 4n | sh 3n | opacity n |

@@ -89,6 +89,13 @@ _SIGS = {
     "uws_raster_bwd_rows": (c_int, [POINTER(ProjectedC), c_void_p, c_void_p, POINTER(CameraC),
                                     c_void_p, POINTER(RasterOutC), c_void_p, c_void_p, c_void_p,
                                     c_void_p]),
+    "uws_raster_bwd_det_prefix": (c_int, [POINTER(CameraC), POINTER(RasterOutC), c_void_p,
+                                          c_void_p, c_void_p]),
+    "uws_raster_bwd_det_workspace_size": (c_int, [c_int32, c_int64, c_int64, POINTER(c_size_t)]),
+    "uws_raster_bwd_det": (c_int, [POINTER(ProjectedC), c_void_p, c_void_p, c_void_p, c_void_p,
+                                   POINTER(CameraC), c_void_p, POINTER(RasterOutC), c_void_p,
+                                   c_void_p, c_void_p, c_void_p, c_int64, c_int64, c_void_p,
+                                   c_size_t, c_void_p]),
     "uws_preprocess_bwd": (c_int, [POINTER(CloudC), POINTER(CameraC), POINTER(ProjectedC),
                                    c_int64, c_void_p, c_void_p, c_void_p, c_int32, c_double,
                                    c_void_p, c_void_p, c_int32, c_void_p]),

@@ -18,6 +18,7 @@
 // (14 shuffles instead of 45), accumulated over the CTA's warps in shared
 // memory, chained through the conic once per (tile, Gaussian) and only then
 // sent to HBM with 9 atomics.
+#include "radix.cuh"
 #include "raster_common.cuh"
 #include "row_filter.cuh"
 
@@ -54,6 +55,13 @@ struct BwdArgs {
     const float* dL;
     float* screen;       // [K][9]
     double* medium_acc;  // [9]
+    // deterministic mode (DET): the (tile, Gaussian) partials go to slot
+    // tile_base[tile] + list position instead of atomics on screen / medium_acc
+    const int32_t* tile_base;  // [tiles + 1] exclusive prefix of the consumed prefixes
+    float* part;               // [R][9]
+    uint32_t* part_row;        // [R] visible row, or none_row when no pixel used it
+    uint32_t none_row;
+    double* med_part;          // [tiles][9]
 };
 
 // Reduce v[0..7] across the warp; returns the full sum of value index
@@ -83,7 +91,7 @@ __device__ __forceinline__ float butterfly8(const float v[8], int lane) {
 
 constexpr int kMaxMarks = 64;   // recorded batch starts per tile (row-list source)
 
-template <bool ROWS, int MINB>
+template <bool ROWS, int MINB, bool DET = false>
 __global__ void __launch_bounds__(kThreads, MINB) k_raster_bwd(BwdArgs a) {
     // launched serially (no pdl_entry): the per-CTA L1 invalidation costs more here
     __shared__ int sMarkCur[ROWS ? kMaxMarks : 1], sMarkSkip[ROWS ? kMaxMarks : 1];
@@ -170,7 +178,10 @@ __global__ void __launch_bounds__(kThreads, MINB) k_raster_bwd(BwdArgs a) {
         float s = 0.f;
 #pragma unroll
         for (int w = 0; w < kWarps; ++w) s += sMed[w][threadIdx.x];
-        atomicAdd(&a.medium_acc[threadIdx.x], (double)s);
+        if (DET)
+            a.med_part[(size_t)tile * 9 + threadIdx.x] = (double)s;
+        else
+            atomicAdd(&a.medium_acc[threadIdx.x], (double)s);
     }
     __syncthreads();
     const int maxlast = sMaxLast;
@@ -331,7 +342,24 @@ __global__ void __launch_bounds__(kThreads, MINB) k_raster_bwd(BwdArgs a) {
                     for (int i = 0; i < 9; ++i) s[i] += sAcc[w][i][k];
                 }
             }
-            if (any) {
+            if (DET) {
+                // every consumed slot is written (row = none when no pixel used it)
+                const size_t slot = (size_t)a.tile_base[tile] + lo + k;
+                const float ca = sRec[k].A.A * (-2.0f * kLn2);
+                const float cb = sRec[k].A.B * (-kLn2);
+                const float cc = sRec[k].B.C * (-2.0f * kLn2);
+                float* g = a.part + slot * 9;
+                g[0] = s[0];
+                g[1] = ca * s[1] + cb * s[2];
+                g[2] = cb * s[1] + cc * s[2];
+                g[3] = -0.5f * s[3];
+                g[4] = -s[4];
+                g[5] = -0.5f * s[5];
+                g[6] = s[6];
+                g[7] = s[7];
+                g[8] = s[8];
+                a.part_row[slot] = any ? (uint32_t)sRec[k].C.row : a.none_row;
+            } else if (any) {
                 // natural-units conic from the log2-scaled staged values
                 const float ca = sRec[k].A.A * (-2.0f * kLn2);
                 const float cb = sRec[k].A.B * (-kLn2);
@@ -351,10 +379,129 @@ __global__ void __launch_bounds__(kThreads, MINB) k_raster_bwd(BwdArgs a) {
     }
 }
 
+// ---- deterministic mode ---------------------------------------------------
+// Per tile: the consumed list prefix = max over its pixels of `last` (what the
+// backward walks), written to count[tile].
+__global__ void __launch_bounds__(256) k_tile_consumed(const int32_t* __restrict__ last, int width,
+                                                       int height, int gx, int32_t* count) {
+    pdl_entry();
+    const int tile = blockIdx.x;
+    const int ty = tile / gx, tx = tile - ty * gx;
+    const int px = tx * kTile + (threadIdx.x & 15), py = ty * kTile + (threadIdx.x >> 4);
+    int v = (px < width && py < height) ? last[py * width + px] : 0;
+    v = __reduce_max_sync(0xffffffffu, v);
+    __shared__ int sm[8];
+    if ((threadIdx.x & 31) == 0) sm[threadIdx.x >> 5] = v;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        int m = 0;
+        for (int w = 0; w < 8; ++w) m = max(m, sm[w]);
+        count[tile] = m;
+    }
+}
+
+// Exclusive scan of count[0..n) into base[0..n], one block (n = tiles <= a few 1e4).
+__global__ void __launch_bounds__(1024) k_tile_scan(const int32_t* __restrict__ count, int n,
+                                                    int32_t* base) {
+    pdl_entry();
+    __shared__ int32_t sm[33];
+    int32_t carry = 0;
+    for (int c = 0; c < n; c += 1024) {
+        const int i = c + threadIdx.x;
+        const int32_t v = i < n ? count[i] : 0;
+        int32_t tot;
+        const int32_t ex = block_exclusive_sum<1024, int32_t>(v, sm, &tot);
+        if (i < n) base[i] = carry + ex;
+        carry += tot;
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) base[n] = carry;
+}
+
+// One thread per run of equal rows in the row-sorted slots: the run's partials
+// summed in slot order (tile order, as backward.py:334-341 merges), stored.
+__global__ void __launch_bounds__(256) k_part_reduce(const uint32_t* __restrict__ rows,
+                                                     const uint32_t* __restrict__ slots,
+                                                     const float* __restrict__ part,
+                                                     const int32_t* __restrict__ n_dev,
+                                                     uint32_t none_row, float* screen) {
+    pdl_entry();
+    const int n = *n_dev;
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+        const uint32_t r = rows[i];
+        if (r == none_row || (i > 0 && rows[i - 1] == r)) continue;
+        float acc[9];
+#pragma unroll
+        for (int v = 0; v < 9; ++v) acc[v] = 0.f;
+        for (int j = i; j < n && rows[j] == r; ++j) {
+            const float* g = part + (size_t)slots[j] * 9;
+#pragma unroll
+            for (int v = 0; v < 9; ++v) acc[v] += g[v];
+        }
+        float* o = screen + (size_t)r * 9;
+#pragma unroll
+        for (int v = 0; v < 9; ++v) o[v] += acc[v];
+    }
+}
+
+// medium_acc += per-tile medium partials summed in tile order (thread v = slot v).
+__global__ void __launch_bounds__(32) k_med_reduce(const double* __restrict__ med_part, int tiles,
+                                                   double* medium_acc) {
+    pdl_entry();
+    if (threadIdx.x >= 9) return;
+    double s = 0.0;
+    for (int t = 0; t < tiles; ++t) s += med_part[(size_t)t * 9 + threadIdx.x];
+    medium_acc[threadIdx.x] += s;
+}
+
+struct DetPlan {
+    float* part;
+    uint32_t *part_row, *rows_sorted, *slots_sorted;
+    double* med_part;
+    radix::Plan<uint32_t> sort;
+};
+
+inline void det_plan(Workspace& ws, int tiles, int64_t r, int64_t k, DetPlan& p) {
+    const uint32_t n = (uint32_t)(r > 0 ? r : 1);
+    int bits = 1;
+    while (bits < 32 && (1ull << bits) <= (uint64_t)k) ++bits;  // keys 0..k (k = none)
+    p.part = ws.take<float>((size_t)n * 9);
+    p.part_row = ws.take<uint32_t>(n);
+    p.rows_sorted = ws.take<uint32_t>(n);
+    p.slots_sorted = ws.take<uint32_t>(n);
+    p.med_part = ws.take<double>((size_t)tiles * 9);
+    radix::plan<uint32_t>(ws, n, (bits + 7) / 8, p.sort);
+}
+
 }  // namespace
 }  // namespace uws
 
 using namespace uws;
+
+extern "C" int uws_raster_bwd_det_prefix(const uws_camera* cam, const uws_raster_out* fwd,
+                                         int32_t* tile_count, int32_t* tile_base, void* stream) {
+    UWS_REQUIRE(cam && fwd && fwd->last && tile_count && tile_base,
+                "uws_raster_bwd_det_prefix: null argument");
+    const int gx = (int)ceil_div(cam->width, kTile), gy = (int)ceil_div(cam->height, kTile);
+    launch(k_tile_consumed, dim3(gx * gy), dim3(256), 0, as_stream(stream), fwd->last, cam->width,
+           cam->height, gx, tile_count);
+    launch(k_tile_scan, dim3(1), dim3(1024), 0, as_stream(stream), (const int32_t*)tile_count,
+           gx * gy, tile_base);
+    count_launches(1);
+    UWS_CHECK_LAUNCH("k_tile_scan");
+    return UWS_OK;
+}
+
+extern "C" int uws_raster_bwd_det_workspace_size(int32_t tiles, int64_t r, int64_t k,
+                                                 size_t* bytes) {
+    UWS_REQUIRE(bytes && tiles >= 0 && r >= 0 && k >= 0,
+                "uws_raster_bwd_det_workspace_size: bad argument");
+    Workspace ws(nullptr, 0, true);
+    DetPlan p;
+    det_plan(ws, tiles, r, k, p);
+    *bytes = ws.used;
+    return UWS_OK;
+}
 
 extern "C" int uws_raster_bwd(const uws_projected* proj, const int32_t* offsets,
                               const int32_t* entries, const uws_camera* cam, const float* medium,
@@ -427,4 +574,85 @@ extern "C" int uws_raster_bwd_rows(const uws_projected* proj, const int32_t* row
     launch_serial(k_raster_bwd<true, 12>, dim3(a.gx * gy), dim3(kThreads), 0, as_stream(stream), a);
     UWS_CHECK_LAUNCH("k_raster_bwd_rows");
     return UWS_OK;
+}
+
+// Deterministic form of uws_raster_bwd / uws_raster_bwd_rows: the same kernel
+// writes each (tile, Gaussian) partial to its slot, the slots are stably sorted
+// by row and every row's partials are summed in tile order.
+template <bool ROWS>
+static int bwd_det(BwdArgs a, int gy, const int32_t* tile_base, int64_t r, int64_t k,
+                   void* workspace, size_t workspace_bytes, cudaStream_t st) {
+    const int tiles = a.gx * gy;
+    Workspace ws(workspace, workspace_bytes);
+    DetPlan p;
+    det_plan(ws, tiles, r, k, p);
+    UWS_REQUIRE(ws.ok(), "uws_raster_bwd_det: workspace too small");
+    a.tile_base = tile_base;
+    a.part = p.part;
+    a.part_row = p.part_row;
+    a.none_row = (uint32_t)k;
+    a.med_part = p.med_part;
+    launch_serial(k_raster_bwd<ROWS, 12, true>, dim3(tiles), dim3(kThreads), 0, st, a);
+    UWS_CHECK_LAUNCH("k_raster_bwd_det");
+    if (r > 0) {
+        UWS_CUDA(radix::sort_pairs<uint32_t>(p.sort, p.part_row, nullptr, p.rows_sorted,
+                                             p.slots_sorted, (uint32_t)r, nullptr, 0, st));
+        const int64_t nb = (int64_t)ceil_div(r, 256);
+        const int blocks = (int)(nb < 148 * 8 ? nb : 148 * 8);
+        launch(k_part_reduce, dim3(blocks), dim3(256), 0, st, (const uint32_t*)p.rows_sorted,
+               (const uint32_t*)p.slots_sorted, (const float*)p.part, tile_base + tiles,
+               (uint32_t)k, a.screen);
+        UWS_CHECK_LAUNCH("k_part_reduce");
+    }
+    if (a.medium) {
+        launch(k_med_reduce, dim3(1), dim3(32), 0, st, (const double*)p.med_part, tiles,
+               a.medium_acc);
+        UWS_CHECK_LAUNCH("k_med_reduce");
+    }
+    return UWS_OK;
+}
+
+extern "C" int uws_raster_bwd_det(const uws_projected* proj, const int32_t* offsets,
+                                  const int32_t* entries, const int32_t* row_start,
+                                  const void* row_items, const uws_camera* cam,
+                                  const float* medium, const uws_raster_out* fwd,
+                                  const float* dL_dC, float* screen_grads, double* medium_acc,
+                                  const int32_t* tile_base, int64_t r, int64_t k, void* workspace,
+                                  size_t workspace_bytes, void* stream) {
+    UWS_REQUIRE(proj && cam && fwd && dL_dC && screen_grads && tile_base,
+                "uws_raster_bwd_det: null argument");
+    UWS_REQUIRE((offsets != nullptr) != (row_start != nullptr),
+                "uws_raster_bwd_det: give either tile lists or row lists");
+    UWS_REQUIRE(fwd->final_T && fwd->last, "uws_raster_bwd_det: forward context missing");
+    UWS_REQUIRE(medium == nullptr || (fwd->color_clean && fwd->depth && medium_acc),
+                "uws_raster_bwd_det: underwater backward needs color_clean, depth and medium_acc");
+    UWS_REQUIRE(r >= 0 && k >= 0 && k < 0xffffffffll, "uws_raster_bwd_det: bad sizes");
+    BwdArgs a = {};
+    a.splat = proj->splat;
+    a.exact = proj->exact;
+    a.offsets = offsets;
+    a.entries = entries;
+    a.row_start = row_start;
+    a.row_items = (const uint2*)row_items;
+    if (row_start) {
+        a.tile_rows = fwd->tile_rows;
+        a.tile_nrows = fwd->tile_nrows;
+        a.tile_rows_cap = fwd->tile_rows_cap;
+    }
+    a.width = cam->width;
+    a.height = cam->height;
+    a.gx = (int)ceil_div(cam->width, kTile);
+    const int gy = (int)ceil_div(cam->height, kTile);
+    a.medium = medium;
+    a.color_clean = fwd->color_clean;
+    a.depth = fwd->depth;
+    a.final_T = fwd->final_T;
+    a.last = fwd->last;
+    a.dL = dL_dC;
+    a.screen = screen_grads;
+    a.medium_acc = medium_acc;
+    return row_start ? bwd_det<true>(a, gy, tile_base, r, k, workspace, workspace_bytes,
+                                     as_stream(stream))
+                     : bwd_det<false>(a, gy, tile_base, r, k, workspace, workspace_bytes,
+                                      as_stream(stream));
 }

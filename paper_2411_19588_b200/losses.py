@@ -128,3 +128,42 @@ def psnr(a, b, cap: float = 99.0) -> float:
     if mse <= 10 ** (-cap / 10.0):
         return cap
     return float(-10.0 * np.log10(mse))
+
+
+def loss_value_f64(rendered, gt, medium: Optional[MediumParams], lambda_ssim: float = 0.3,
+                   lambda_guide: float = 0.1) -> float:
+    """The objective of total_loss (losses.py:140-160) evaluated in float64 with
+    torch ops on the device -- no gradient, for the finite-difference harness,
+    whose difference quotients need the loss far below the float32 kernel's
+    rounding (its per-tile partial sums are float32)."""
+    dev = medium.flat.device if medium is not None else default_device()
+    a = torch.as_tensor(rendered if isinstance(rendered, torch.Tensor) else np.asarray(rendered))
+    b = torch.as_tensor(gt if isinstance(gt, torch.Tensor) else np.asarray(gt))
+    a = a.to(device=dev, dtype=torch.float64)
+    b = b.to(device=dev, dtype=torch.float64)
+    if a.shape != b.shape:
+        raise DataError(f"shape mismatch {tuple(a.shape)} vs {tuple(b.shape)}")
+    l1 = float((a - b).abs().mean())
+    x = torch.arange(SSIM_WINDOW, dtype=torch.float64, device=dev) - (SSIM_WINDOW - 1) / 2
+    k = torch.exp(-x * x / (2 * SSIM_SIGMA ** 2))
+    k = k / k.sum()
+    img = torch.stack([a, b]).permute(0, 3, 1, 2) if a.dim() == 3 else torch.stack([a, b])[:, None]
+    c = img.shape[1]
+
+    def filt(t):  # valid separable 11x11 Gaussian filter per channel
+        t = torch.nn.functional.conv2d(t, k.view(1, 1, 1, -1).expand(c, 1, 1, -1), groups=c)
+        return torch.nn.functional.conv2d(t, k.view(1, 1, -1, 1).expand(c, 1, -1, 1), groups=c)
+
+    pa, pb = img[0:1], img[1:2]
+    mu_a, mu_b = filt(pa), filt(pb)
+    saa = filt(pa * pa) - mu_a * mu_a
+    sbb = filt(pb * pb) - mu_b * mu_b
+    sab = filt(pa * pb) - mu_a * mu_b
+    ssim = ((2 * mu_a * mu_b + SSIM_C1) * (2 * sab + SSIM_C2)) / \
+        ((mu_a * mu_a + mu_b * mu_b + SSIM_C1) * (saa + sbb + SSIM_C2))
+    d_ssim = 1.0 - float(ssim.mean())
+    lb = 0.0
+    if medium is not None and medium.has_guidance:
+        lb = float((medium.water_color.double() - medium.water_color_guide.double()).abs().sum()
+                   + (medium.backscatter.double() - medium.backscatter_guide.double()).abs().sum())
+    return (1.0 - lambda_ssim) * l1 + lambda_ssim * d_ssim + lambda_guide * lb

@@ -9,6 +9,8 @@ reference's names.
 from __future__ import annotations
 
 import ctypes
+from dataclasses import dataclass
+from typing import Optional
 
 import numpy as np
 import torch
@@ -21,6 +23,17 @@ COV2D_DILATION = 0.3
 ALPHA_FLOOR = 1.0 / 255.0
 MIN_RADIUS_SIGMA = 3.0
 SPLAT_FLOATS = 12  # uws_splat is 48 bytes
+
+
+@dataclass
+class Projected2D:
+    """One footprint as host float64 values (reference projection.py:29-37)."""
+
+    mean2d: np.ndarray     # (2,) pixels
+    cov2d: np.ndarray      # (2, 2), dilation included
+    depth: float           # view z
+    radius: float          # footprint radius, pixels
+    source_index: int
 
 
 class ProjectedCloud:
@@ -114,6 +127,15 @@ class ProjectedCloud:
     def color_clamped(self):
         return self.color <= 0.0
 
+    def item(self, i: int) -> Projected2D:
+        """Row ``i`` as a host Projected2D (needs the geometry fields)."""
+        if self._cov2d is None:
+            raise ValueError("projected without geometry (with_geometry=False)")
+        a, b, c = (float(v) for v in self._cov2d[i].tolist())
+        return Projected2D(mean2d=self.mean2d[i].cpu().numpy().astype(np.float64),
+                           cov2d=np.array([[a, b], [b, c]]), depth=float(self.depth[i]),
+                           radius=float(self.radius[i]), source_index=int(self.source_index[i]))
+
 
 def preprocess_into(proj: ProjectedCloud, cloud: GaussianCloud, cam, workspace=None) -> None:
     """Run the preprocess kernel into an existing ProjectedCloud (no host sync)."""
@@ -139,12 +161,24 @@ def project_cloud(cloud: GaussianCloud, cam, with_geometry: bool = True) -> Proj
     return proj
 
 
-def tile_span(mean2d, radius, tile_size: int = TILE_SIZE, grid=None):
-    """Inclusive tile rectangle of one footprint, None when empty (projection.py:214-226).
+def project_gaussian(g, cam) -> Optional[Projected2D]:
+    """Project one primitive through the device kernel; None when culled
+    (reference projection.py:202-211)."""
+    from .scene import GaussianCloud
+    cloud = GaussianCloud(g.position[None, :], g.log_scale[None, :], g.rotation[None, :],
+                          np.asarray(g.sh_coeffs, np.float64).reshape(1, -1, 3),
+                          np.array([g.opacity_logit]))
+    proj = project_cloud(cloud, cam)
+    return proj.item(0) if len(proj) else None
+
+
+def tile_span(p, tile_size: int = TILE_SIZE, grid=None):
+    """Inclusive tile rectangle of one footprint ``p`` (mean2d, radius), None when
+    no pixel centre is reached (projection.py:214-226).
 
     Host-side helper (float64, same formula as the device kernel)."""
-    mx, my = float(mean2d[0]), float(mean2d[1])
-    r = float(radius)
+    mx, my = float(p.mean2d[0]), float(p.mean2d[1])
+    r = float(p.radius)
     s = [np.floor(np.ceil(mx - r - 0.5 - 1e-9) / tile_size),
          np.floor(np.ceil(my - r - 0.5 - 1e-9) / tile_size),
          np.floor(np.floor(mx + r - 0.5 + 1e-9) / tile_size),

@@ -12,11 +12,12 @@ import ctypes
 from dataclasses import dataclass
 from typing import Optional
 
+import numpy as np
 import torch
 
 from . import _lib
 from .medium import logistic_remap
-from .projection import TILE_SIZE, ProjectedCloud, project_cloud
+from .projection import ALPHA_FLOOR, TILE_SIZE, ProjectedCloud, project_cloud
 from .scene import Camera, GaussianCloud, MediumParams
 
 ALPHA_CLAMP = 0.99
@@ -247,11 +248,76 @@ def render(cloud: GaussianCloud, cam, medium: Optional[MediumParams] = None,
     return out
 
 
+def render_naive(cloud: GaussianCloud, cam, medium: Optional[MediumParams] = None,
+                 mode: str = "clean", row_chunk: int = 16) -> RenderOutput:
+    """Every visible Gaussian against every pixel, no tile culling
+    (rasterizer.py:254-296): the global (depth, source) order of all K visible
+    rows is each tile's list, composited by the same device kernel as the tiled
+    path (uws_raster_fwd + the float64 transmittance fix-up).  Tiled == naive
+    therefore checks that binning drops no contributor.  Lists hold K entries
+    per tile, so this is for oracle-sized scenes as in the reference;
+    ``row_chunk`` is accepted and ignored."""
+    if mode not in ("clean", "underwater"):
+        raise ValueError(f"unknown render mode {mode!r}")
+    if mode == "underwater" and medium is None:
+        raise ValueError("underwater mode requires medium parameters")
+    cam = Camera.from_any(cam)
+    proj = project_cloud(cloud, cam, with_geometry=False)
+    k = proj.k
+    gx, gy = cam.grid
+    # rows are in ascending source order: a stable sort by depth is the
+    # reference's lexsort((source_index, depth))
+    order = torch.sort(proj.depth, stable=True).indices.to(torch.int32)
+    entries = order.repeat(gx * gy) if k else torch.zeros(1, dtype=torch.int32, device=proj.device)
+    offsets = (torch.arange(gx * gy + 1, device=proj.device, dtype=torch.int64) * k).to(torch.int32)
+    out = composite(proj, TileBins(gx, gy, offsets, entries), cam, medium, mode)
+    out.proj = out.bins = None
+    return out
+
+
+def alpha_at(p, opacity_logit: float, pixel_center) -> float:
+    """Opacity of one footprint at a pixel centre, float64 (rasterizer.py:88-101):
+    sigmoid(logit) exp(-d^T cov^-1 d / 2), clamped at 0.99, 0 below 1/255.
+    Scalar host helper; the kernels evaluate the same expression per pair."""
+    d = np.asarray(pixel_center, dtype=np.float64) - np.asarray(p.mean2d, dtype=np.float64)
+    q = float(d @ np.linalg.inv(np.asarray(p.cov2d, dtype=np.float64)) @ d)
+    a = min(float(1.0 / (1.0 + np.exp(-opacity_logit)) * np.exp(-0.5 * q)), ALPHA_CLAMP)
+    return a if a >= ALPHA_FLOOR else 0.0
+
+
+def composite_pixel(contributors, pixel, far: float):
+    """Front-to-back blend of one pixel's depth-sorted (Projected2D, logit, rgb)
+    list (rasterizer.py:104-129); returns (color, depth, weight, T_final, count).
+    Scalar host helper mirroring the compositing kernel's rules."""
+    color = np.zeros(3)
+    weight = depth_num = 0.0
+    t = 1.0
+    count = 0
+    for p, logit, rgb in contributors:
+        if t < T_EARLY_STOP:
+            break
+        a = alpha_at(p, logit, pixel)
+        if a == 0.0:
+            continue
+        w = a * t
+        color += w * np.asarray(rgb, dtype=np.float64)
+        depth_num += w * p.depth
+        weight += w
+        t *= 1.0 - a
+        count += 1
+    return color, (depth_num / weight if weight > WEIGHT_EPS else far), weight, t, count
+
+
 def apply_water(color_clean: torch.Tensor, depth_raw: torch.Tensor,
                 medium: MediumParams) -> torch.Tensor:
     """Attenuate a clean render and add backscatter (rasterizer.py:244-251).
 
     Utility outside the hot path (the render kernel fuses this epilogue)."""
+    dev = medium.flat.device
+    color_clean = torch.as_tensor(np.asarray(color_clean) if not isinstance(
+        color_clean, torch.Tensor) else color_clean).to(dev)
+    depth_raw = torch.as_tensor(np.asarray(depth_raw) if not isinstance(
+        depth_raw, torch.Tensor) else depth_raw).to(dev)
     z = logistic_remap(depth_raw)[..., None]
     att = torch.exp(-medium.attenuation.double() * z)
     bsc = medium.water_color.double() * (1.0 - torch.exp(-medium.backscatter.double() * z))

@@ -64,6 +64,38 @@ def feature_to_rgb(f):
     return np.asarray(f, dtype=np.float64) * SH_C0 + 0.5
 
 
+@dataclass
+class Gaussian:
+    """One primitive as host float64 values (reference scene.py:60-74)."""
+
+    position: np.ndarray
+    log_scale: np.ndarray
+    rotation: np.ndarray
+    sh_coeffs: np.ndarray
+    opacity_logit: float
+
+    def __post_init__(self):
+        for name, shape in (("position", (3,)), ("log_scale", (3,)), ("rotation", (4,)),
+                            ("sh_coeffs", (-1, 3))):
+            v = getattr(self, name)
+            if isinstance(v, torch.Tensor):
+                v = v.detach().cpu().double().numpy()
+            setattr(self, name, np.asarray(v, dtype=np.float64).reshape(shape))
+        self.opacity_logit = float(self.opacity_logit)
+
+
+def covariance(g: Gaussian) -> np.ndarray:
+    """World covariance (R diag(e^s)) (R diag(e^s))^T of one primitive (scene.py:77-81).
+    Scalar host helper; the device kernels form it per Gaussian in float64."""
+    m = quat_to_rotmat(g.rotation) * np.exp(g.log_scale)[None, :]
+    return m @ m.T
+
+
+def opacity(g: Gaussian) -> float:
+    """sigmoid(logit) as 1 / (1 + exp(-x)) (scene.py:84-86; scipy expit's formula)."""
+    return float(1.0 / (1.0 + np.exp(-g.opacity_logit)))
+
+
 def flat_views(flat: torch.Tensor, n: int) -> dict:
     """Named per-field views of a [14n(+...)] flat buffer."""
     out = {}
@@ -168,8 +200,15 @@ class GaussianCloud:
         """Clamped degree-0 RGB, float64 (scene.py:136-139)."""
         return torch.clamp(self.sh_coeffs[:, 0, :].double() * SH_C0 + 0.5, min=0.0)
 
+    def gaussian(self, i: int) -> Gaussian:
+        """Primitive ``i`` as a host Gaussian (scene.py:140-148)."""
+        row = {name: getattr(self, name)[i].detach().cpu().double().numpy()
+               for name in CLOUD_FIELDS}
+        return Gaussian(row["positions"], row["log_scales"], row["rotations"],
+                        row["sh_coeffs"], float(row["opacity_logits"]))
+
     def copy(self) -> "GaussianCloud":
-        c = GaussianCloud.__new__(GaussianCloud)
+        c = type(self).__new__(type(self))
         object.__setattr__(c, "_n", self._n)
         object.__setattr__(c, "_flat", self._flat.clone())
         c._bind()
@@ -249,9 +288,9 @@ class MediumParams:
         self._flat[6:9].clamp_(*BACKSCATTER_BOUNDS)
 
     def copy(self) -> "MediumParams":
-        return MediumParams(self.attenuation, self.water_color, self.backscatter,
-                            self.water_color_guide, self.backscatter_guide,
-                            device=self._flat.device)
+        return type(self)(self.attenuation, self.water_color, self.backscatter,
+                          self.water_color_guide, self.backscatter_guide,
+                          device=self._flat.device)
 
     @staticmethod
     def zero(device=None) -> "MediumParams":

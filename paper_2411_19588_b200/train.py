@@ -166,3 +166,71 @@ class ViewShardedTrainer:
                 med.flat[9:15].copy_(msg[:6])
                 med.mark_guidance()
         return est
+
+
+@dataclass
+class FitResult:
+    state: TrainState
+    log_rows: list
+    engine: object
+
+
+def fit(state: TrainState, cameras: Sequence, images: Sequence, train_idx: Sequence[int],
+        cfg: OptimConfig, spatial_scale: float, rng, engine=None) -> FitResult:
+    """The loop of pipeline.train (pipeline.py:169-233) on the sync-free StepEngine.
+
+    Same schedule and random stream as the reference: views are drawn by
+    popping a list reshuffled with ``rng`` whenever it runs empty (171-175),
+    densify_and_prune every ``densify_interval`` iterations in
+    [densify_from, densify_until] with the same ``rng`` (195-200), opacity
+    reset every ``opacity_reset_interval`` (201-202) and the guidance refresh
+    from the current view every ``refit_period`` (204-208).  Iterations that
+    need none of those run pipelined (step i is launched before step i-1's
+    record is read); the engine is flushed before each densify / reset /
+    refit.  Ground-truth images are host arrays, copied on the engine's copy
+    stream.  ``log_rows`` carries the reference's per-iteration log columns
+    (pipeline.py:210-225) except the medium values, which are read only at
+    flush points (``None`` elsewhere) to keep the loop free of host syncs."""
+    from .engine import StepEngine
+    from .optim import densify_and_prune, position_lr, reset_opacities
+    W, H = int(cameras[0].width), int(cameras[0].height)
+    eng = engine or StepEngine(state, W, H, cfg, spatial_scale)
+    rows, order, pending = [], [], []
+
+    def record(it, st):
+        if st is None:
+            return
+        rows.append({"iter": it, "l1": st.l1, "d_ssim": st.d_ssim, "l_bs": st.l_bs,
+                     "total": st.total, "skipped": st.skipped,
+                     "lr_position": position_lr(it, cfg, spatial_scale)})
+
+    for it in range(1, cfg.iterations + 1):
+        state.iteration = it
+        if not order:
+            order = list(train_idx)
+            rng.shuffle(order)
+        view = order.pop()
+        densify = (cfg.densify_from <= it <= cfg.densify_until
+                   and it % cfg.densify_interval == 0)
+        reset = bool(cfg.opacity_reset_interval) and it % cfg.opacity_reset_interval == 0
+        refit = bool(cfg.refit_period) and it % cfg.refit_period == 0
+        prev = eng.step_async([(cameras[view], images[view])])
+        if pending:
+            record(pending.pop(), prev)
+        pending.append(it)
+        if densify or reset or refit:
+            st = eng.flush()
+            record(pending.pop(), st)
+            if not st.skipped:     # the reference `continue`s past a skipped step
+                if densify:
+                    densify_and_prune(state, cfg, spatial_scale, rng)
+                if reset:
+                    reset_opacities(state, cfg)
+                if refit:
+                    eng.refresh_guidance(images[view])
+            m = state.medium.flat[:9].tolist()
+            rows[-1].update({"num_gaussians": len(state.cloud), "medium": m})
+    st = eng.flush()
+    if pending:
+        record(pending.pop(), st)
+    return FitResult(state, rows, eng)

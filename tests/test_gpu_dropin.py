@@ -1,0 +1,294 @@
+"""The reference's own callers, unchanged, on the device path.
+
+The unmodified reference package (installed in baseline/_ref, which travels
+with the repo to the GPU box) is imported and ``dropin.install`` rebinds its
+hot-path names to this package; then the reference's ``dataset``,
+``pipeline`` (train / evaluate / render_novel), ``fixtures`` and ``cli`` code
+runs as written.  Results are compared with what the reference itself produced
+on the CPU (tests/golden/e2e_canonical.npz, written by make_e2e.py), including
+SPEC acceptance 5: 2000 training iterations on the canonical fixture.
+"""
+
+import io
+import os
+import sys
+from contextlib import redirect_stdout
+
+import numpy as np
+import pytest
+import torch
+
+from golden_util import GOLDEN
+
+pytestmark = pytest.mark.gpu
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+REF = os.path.join(ROOT, "baseline", "_ref")
+
+
+@pytest.fixture(scope="module")
+def R():
+    if not os.path.isdir(os.path.join(REF, "uwsplat")):
+        pytest.skip("reference not installed in baseline/_ref")
+    sys.path.insert(0, REF)
+    import uwsplat
+    import uwsplat.cli  # noqa: F401
+    from paper_2411_19588_b200 import dropin
+    dropin.install(uwsplat)
+    yield uwsplat
+    dropin.uninstall()
+
+
+@pytest.fixture(scope="module")
+def golden():
+    return np.load(os.path.join(GOLDEN, "e2e_canonical.npz"))
+
+
+@pytest.fixture(scope="module")
+def dataset_dir(R, tmp_path_factory):
+    d = str(tmp_path_factory.mktemp("canonical"))
+    R.dataset.generate_synthetic(R.dataset.canonical_spec(), d)   # renders on the device
+    return d
+
+
+def test_generate_synthetic_matches_reference(R, golden, dataset_dir):
+    """dataset.generate_synthetic (dataset.py:392-431) through the drop-in render:
+    the observed images and remapped depths equal the reference's."""
+    ds = R.dataset.load_dataset(dataset_dir)
+    img = np.stack([np.asarray(a, np.float32) for a in ds.images])
+    dep = np.stack([np.asarray(a, np.float32) for a in ds.depths])
+    assert img.shape == golden["images"].shape
+    assert np.abs(img - golden["images"]).max() <= 1e-4
+    assert np.abs(dep - golden["depths"]).max() <= 1e-5
+
+
+def _load(R, golden):
+    """The reference's canonical dataset (its own images and cameras)."""
+    cams = []
+    for R_, t_, intr in zip(golden["cam_R"], golden["cam_t"], golden["cam_intr"]):
+        w, h, fx, fy, cx, cy, near, far = intr
+        cams.append(R.scene.Camera(width=int(w), height=int(h), fx=fx, fy=fy, cx=cx, cy=cy,
+                                   R=R_, t=t_, near=near, far=far))
+    from types import SimpleNamespace
+    return SimpleNamespace(images=[np.asarray(a, np.float64) for a in golden["images"]],
+                           depths=list(golden["depths"]), cameras=cams)
+
+
+def _col(golden, name):
+    return list(golden["log_cols"]).index(name)
+
+
+def test_train_loop_tracks_reference(R, golden):
+    """pipeline.train (pipeline.py:157-235) unchanged on the device: the same
+    initial cloud, view order and updates, so the per-iteration loss follows the
+    reference's float64 run (float32 device arithmetic)."""
+    ds = _load(R, golden)
+    n = 499   # up to the first guidance refresh (see test_engine_fit_tracks_reference)
+    res = R.pipeline.train(ds, R.OptimConfig(iterations=n), seed=0)
+    got = np.array([r["total"] for r in res.log_rows])
+    ref = golden["log"][:n, _col(golden, "total")]
+    assert len(got) == n
+    rel = np.abs(got - ref) / np.abs(ref)
+    assert rel[0] < 1e-5, rel[0]          # iteration 1: same cloud, same view
+    assert rel[:100].max() < 1e-3, rel[:100].max()
+    assert rel.max() < 2e-2, (rel.max(), int(rel.argmax()) + 1)
+    med = np.array([[r[c] for c in ("water_color_r", "water_color_g", "water_color_b",
+                                    "backscatter_r", "backscatter_g", "backscatter_b")]
+                    for r in res.log_rows])
+    ref_med = golden["log"][:n, [_col(golden, c) for c in (
+        "water_color_r", "water_color_g", "water_color_b", "backscatter_r", "backscatter_g",
+        "backscatter_b")]]
+    assert np.abs(med[:100] - ref_med[:100]).max() < 1e-4
+    assert np.abs(med - ref_med).max() < 2e-2
+
+
+def test_evaluate_render_novel_and_checkpoint_cli(R, dataset_dir, tmp_path):
+    """cli train -> eval -> render on the drop-in (cli.py:96-166): the checkpoint
+    the device path writes is read back, evaluated and rendered by the reference's
+    own command code."""
+    C = R.cli
+    out = str(tmp_path / "run")
+    buf = io.StringIO()
+    with redirect_stdout(buf):
+        assert C.main(["train", "--data", dataset_dir, "--out", out, "--iterations", "60",
+                       "--checkpoint-interval", "0"]) == 0
+        assert C.main(["eval", "--checkpoint", os.path.join(out, "checkpoint.bin"),
+                       "--data", dataset_dir, "--out", str(tmp_path / "eval.csv")]) == 0
+        assert C.main(["render", "--checkpoint", os.path.join(out, "checkpoint.bin"),
+                       "--data", dataset_dir, "--out", str(tmp_path / "novel")]) == 0
+    text = buf.getvalue()
+    assert "finished 60 iterations" in text and "rendered 24 poses" in text
+    rows = open(tmp_path / "eval.csv").read().splitlines()
+    assert rows[0] == "view,psnr,ssim" and rows[-1].startswith("mean,")
+    assert np.isfinite(float(rows[-1].split(",")[1]))
+    for mode in ("clean", "underwater"):
+        assert os.path.exists(tmp_path / "novel" / f"pose_000_{mode}.png")
+        assert os.path.exists(tmp_path / "novel" / f"pose_023_{mode}_depth.pfm")
+
+
+def test_cli_bench_tiled_equals_naive(R):
+    """cli bench (cli.py:208-227): the device render against render_naive (every
+    visible Gaussian composited at every pixel) -- SPEC acceptance 2's tiled == naive."""
+    buf = io.StringIO()
+    with redirect_stdout(buf):
+        assert R.cli.main(["bench", "--gaussians", "500", "--size", "256", "--repeats", "2"]) == 0
+    line = [ln for ln in buf.getvalue().splitlines() if "max |difference|" in ln][0]
+    diff = float(line.split("max |difference|")[1].strip(" )"))
+    assert diff <= 1e-6, line
+
+
+def test_tiled_equals_naive_random_scenes(R):
+    """SPEC acceptance 2: tiled == naive within 1e-6 on 20 random scenes
+    (<= 500 Gaussians, 64x64), both modes, through the reference's fixtures."""
+    F = R.fixtures
+    rng = np.random.default_rng(5)
+    for k in range(20):
+        cloud = F.random_cloud(int(rng.integers(20, 500)), rng, spread=float(rng.uniform(1, 5)))
+        cam = F.front_camera(width=64, height=64, focal=float(rng.uniform(40, 90)))
+        med = R.MediumParams((0.5, 0.4, 0.3), (0.25, 0.35, 0.45), (0.9, 1.1, 1.3))
+        for mode in ("clean", "underwater"):
+            a = R.rasterizer.render(cloud, cam, med, mode)
+            b = R.rasterizer.render_naive(cloud, cam, med, mode)
+            assert float(np.abs(a.color - b.color).max()) <= 1e-6, (k, mode)
+            assert np.array_equal(np.asarray(a.count), np.asarray(b.count)), (k, mode)
+
+
+def test_cli_check_grad_device_finite_differences(R):
+    """cli check-grad (cli.py:198-205) on the drop-in: the device gradients of the
+    canonical 50-Gaussian scene against central differences of the device forward
+    (float32, 1e-3 steps): the median relative error is small and the entries
+    that exceed 1e-2 are few (float32 forward noise on tiny gradients)."""
+    F = R.fixtures
+    cloud, cam, medium, gt = F.gradient_check_scene()
+    rep = R.backward.finite_diff_check(cloud, cam, medium, gt)
+    rel = np.array([r.rel_err for r in rep.rows])
+    assert len(rep.rows) == 50 * 14 + 9
+    assert np.median(rel) < 1e-3, np.median(rel)
+    # float32 render noise in the loss ~1e-10 (measured: tools/fd_report.py), so a
+    # difference quotient with step h carries ~1e-10 / h of noise
+    ok = [abs(r.analytic - r.fd) <= 1e-2 * abs(r.fd) + 5e-10 / r.step for r in rep.rows]
+    assert np.mean(ok) > 0.97, rep.table()
+    for r in rep.rows:
+        if r.param in ("attenuation", "water_color", "backscatter"):
+            assert r.rel_err < 1e-2, r
+
+
+def _acceptance(golden, psnr, medium):
+    """SPEC acceptance 5's checks: train-view PSNR >= 25 dB, B_inf
+    within 0.07 and B_b within 0.3 of truth."""
+    truth = dict(zip(golden["truth_keys"], golden["truth_vals"]))
+    water = np.array([truth[f"water_color_{c}"] for c in "rgb"])
+    bsc = np.array([truth[f"backscatter_{c}"] for c in "rgb"])
+    return (bool(psnr >= truth["psnr_min"]),
+            bool(np.abs(medium[3:6] - water).max() <= truth["train_water_tol"]),
+            bool(np.abs(medium[6:9] - bsc).max() <= truth["train_backscatter_tol"]))
+
+
+def _check_against_reference_runs(golden, psnr, medium, n):
+    """The canonical 2000-iteration run is chaotic (make_e2e_envelope.py): the
+    reference's own float64 runs from initial clouds perturbed at 1e-7 end between
+    16.2 and 20.1 dB train PSNR with 593-975 Gaussians, their learned water colour
+    is bimodal (B_inf red 0.16 or 0.58), and every one misses SPEC's thresholds.
+    A float32 device run cannot follow one of them past the first densification,
+    so it is judged against that spread: PSNR within the reference runs' range
+    +-2 dB, the Gaussian count within 0.5x-1.5x of it, the medium inside its
+    boxes, and SPEC's PSNR verdict the same as every reference run's."""
+    ps = np.append(golden["env_psnr"], golden["train_psnr"].mean())
+    ns = np.append(golden["env_n"], golden["final_n"])
+    assert ps.min() - 2.0 <= psnr <= ps.max() + 2.0, (psnr, ps)
+    assert 0.5 * ns.min() <= n <= 1.5 * ns.max(), (n, ns)
+    assert np.isfinite(medium).all() and (medium[:3] >= 0).all(), medium
+    assert ((medium[3:6] >= 0) & (medium[3:6] <= 1) & (medium[6:9] >= 0)
+            & (medium[6:9] <= 5)).all(), medium
+    ref_psnr_verdicts = {bool(p >= dict(zip(golden["truth_keys"], golden["truth_vals"]))[
+        "psnr_min"]) for p in ps}
+    assert ref_psnr_verdicts == {_acceptance(golden, psnr, medium)[0]}, (psnr, ref_psnr_verdicts)
+
+
+def test_end_to_end_training_acceptance(R, golden):
+    """SPEC acceptance 5 on the device: the reference's train()
+    for 2000 iterations on the canonical fixture -- densification from 1500,
+    guidance refresh every 500 -- evaluated on the train views, against the
+    reference's own runs of the same loop (see _check_against_reference_runs)."""
+    ds = _load(R, golden)
+    res = R.pipeline.train(ds, R.OptimConfig(iterations=2000), seed=0)
+    train_idx, _ = R.pipeline.split_dataset(len(ds.images))
+    ev = R.pipeline.evaluate(res.state, ds, indices=train_idx)
+    m = res.state.medium
+    medium = np.concatenate([np.asarray(m.attenuation, np.float64),
+                             np.asarray(m.water_color, np.float64),
+                             np.asarray(m.backscatter, np.float64)])
+    assert len(res.log_rows) == 2000
+    _check_against_reference_runs(golden, ev["mean_psnr"], medium, len(res.state.cloud))
+
+
+def test_engine_fit_acceptance(R, golden):
+    """SPEC acceptance 5 through the sync-free StepEngine loop (train.fit):
+    the same initial cloud (the reference's init_cloud on the same seed), view
+    order, densification, opacity-reset and guidance-refresh schedule as
+    pipeline.train, 2000 iterations; judged as above."""
+    import paper_2411_19588_b200 as uw
+    from paper_2411_19588_b200.train import fit
+    ds = _load(R, golden)
+    train_idx, _ = R.pipeline.split_dataset(len(ds.images))
+    cams = ds.cameras
+    extent = R.pipeline.scene_extent(cams)
+    rng = np.random.default_rng(0)
+    init = R.pipeline.init_cloud([cams[i] for i in train_idx], 1000, rng)   # device cloud
+    state = uw.TrainState(init, uw.MediumParams(np.full(3, 0.05), np.full(3, 0.3),
+                                                np.full(3, 0.05)))
+    imgs = [np.asarray(a, np.float32) for a in ds.images]
+    res = fit(state, cams, imgs, train_idx, uw.OptimConfig(iterations=2000), extent, rng)
+    assert len(res.log_rows) == 2000 and not any(r["skipped"] for r in res.log_rows)
+    psnr = np.mean([uw.psnr(np.clip(np.asarray(uw.render(state.cloud, cams[i], state.medium,
+                                                         "underwater").color.cpu()), 0, 1),
+                            ds.images[i]) for i in train_idx])
+    medium = np.asarray(state.medium.flat[:9].double().cpu())
+    _check_against_reference_runs(golden, psnr, medium, len(state.cloud))
+
+
+def test_seeded_training_runs_identical(R, golden):
+    """SPEC acceptance 8: two seeded training runs produce identical
+    logs -- pipeline.train on the drop-in with the deterministic backward."""
+    from paper_2411_19588_b200 import backward
+    ds = _load(R, golden)
+    backward.set_deterministic(True)
+    try:
+        logs = [[tuple(r.values()) for r in
+                 R.pipeline.train(ds, R.OptimConfig(iterations=600), seed=0).log_rows]
+                for _ in range(2)]
+    finally:
+        backward.set_deterministic(False)
+    assert logs[0] == logs[1]
+
+
+def test_engine_fit_tracks_reference(R, golden):
+    """train.fit (the StepEngine loop) follows the reference's float64 run over
+    the 499 iterations before the first guidance refresh as closely as
+    pipeline.train on the drop-in does: same initial cloud, view order and
+    updates.  (The refresh itself is discontinuous in its input: a last-ulp
+    change of one render depth can move a pixel across a depth-cluster edge and
+    change the dark-pixel set, so runs are compared up to it; the estimator's
+    parity is tested on fixed inputs in test_backscatter / test_gpu_golden.)"""
+    import paper_2411_19588_b200 as uw
+    from paper_2411_19588_b200.train import fit
+    ds = _load(R, golden)
+    train_idx, _ = R.pipeline.split_dataset(len(ds.images))
+    cams = ds.cameras
+    extent = R.pipeline.scene_extent(cams)
+    rng = np.random.default_rng(0)
+    init = R.pipeline.init_cloud([cams[i] for i in train_idx], 1000, rng)
+    state = uw.TrainState(init, uw.MediumParams(np.full(3, 0.05), np.full(3, 0.3),
+                                                np.full(3, 0.05)))
+    imgs = [np.asarray(a, np.float32) for a in ds.images]
+    res = fit(state, cams, imgs, train_idx, uw.OptimConfig(iterations=499), extent, rng)
+    got = np.array([r["total"] for r in res.log_rows])
+    ref = golden["log"][:499, _col(golden, "total")]
+    rel = np.abs(got - ref) / np.abs(ref)
+    assert rel[0] < 1e-5, rel[0]
+    assert rel[:100].max() < 1e-3, rel[:100].max()
+    assert rel.max() < 2e-2, (rel.max(), int(rel.argmax()) + 1)
+    ref_m = golden["log"][498, [_col(golden, f"{p}_{c}") for p in ("attenuation", "water_color",
+                                                                      "backscatter") for c in "rgb"]]
+    m = state.medium.flat[:9].double().cpu().numpy()
+    assert np.abs(m - ref_m).max() < 2e-2, (m, ref_m)
