@@ -129,7 +129,7 @@ __global__ void __launch_bounds__(kThreads, MINB) k_raster_bwd(BwdArgs a) {
     float med[9];
 #pragma unroll
     for (int v = 0; v < 9; ++v) med[v] = 0.f;
-    int maxl = 0;
+    int maxl = 0, minl = 0x7fffffff;  // longest / shortest consumed prefix of the thread's pixels
 #pragma unroll
     for (int p = 0; p < kPix; ++p) {
         const int ly = ly0 + 2 * p;
@@ -140,11 +140,13 @@ __global__ void __launch_bounds__(kThreads, MINB) k_raster_bwd(BwdArgs a) {
         mylast[p] = 0;
         G[p][0] = G[p][1] = G[p][2] = 0.f;
         const int px = ox + lx, py = oy + ly;
+        if (!(px < a.width && py < a.height)) minl = 0;
         if (px < a.width && py < a.height) {
             const int pix = py * a.width + px;
             T[p] = a.final_T[pix];
             mylast[p] = a.last[pix];
             maxl = max(maxl, mylast[p]);
+            minl = min(minl, mylast[p]);
             if (a.medium) {
                 const float d = a.depth[pix];
                 const float z = 2.0f / (1.0f + __expf(-(float)kLogisticRate * d)) - 1.0f;
@@ -275,25 +277,8 @@ __global__ void __launch_bounds__(kThreads, MINB) k_raster_bwd(BwdArgs a) {
                 dx = fx - A.mx;
                 const float tA = A.A * dx;
                 const float skipv = B.hi - kSkipDelta;
-#pragma unroll
-                for (int p = 0; p < kPix; ++p) {
-                    if (jrel >= mylast[p]) continue;
-                    const float dy = fy[p] - A.my;
-                    const float power = dx * fmaf(A.B, dy, tA) + B.C * dy * dy;
-                    if (power < skipv) continue;
-                    const float araw = B.op * ex2_ftz(power);
-                    bool unclamped = araw < kClampLo;
-                    if (power < B.hi || fabsf(araw - kClampMid) < kClampHalf) {
-                        // near a gate (rare): the full decision from alpha_raw, with
-                        // both gates re-decided from the float64 record in the guard bands
-                        if (araw < kFloorLo) continue;
-                        if (araw < kFloorHi || fabsf(araw - kClampMid) < kClampHalf) {
-                            const double e = alpha_raw_f64_cold(a.splat, a.exact, C.row, ox + lx,
-                                                                oy + ly0 + 2 * p);
-                            if (!(e >= kFloor)) continue;
-                            unclamped = e < kClamp;
-                        }
-                    }
+                // one pair's contribution: alpha = min(araw, 0.99), d power masked by the clamp
+                auto pair = [&](int p, float dy, float araw, bool unclamped) {
                     hit = true;
                     const float alpha = fminf(araw, kClampF);
                     const float inv_om = rcp_ftz(1.0f - alpha);
@@ -311,6 +296,47 @@ __global__ void __launch_bounds__(kThreads, MINB) k_raster_bwd(BwdArgs a) {
                     wg0 = fmaf(w, G[p][0], wg0);
                     wg1 = fmaf(w, G[p][1], wg1);
                     wg2 = fmaf(w, G[p][2], wg2);
+                };
+                if (jrel < minl && B.op < kClampLo) {
+                    // every pixel of the thread still consumes this entry and alpha_raw
+                    // <= opacity stays below the clamp band: only the floor gate remains
+#pragma unroll
+                    for (int p = 0; p < kPix; ++p) {
+                        const float dy = fy[p] - A.my;
+                        const float power = dx * fmaf(A.B, dy, tA) + B.C * dy * dy;
+                        if (power < skipv) continue;
+                        const float araw = B.op * ex2_ftz(power);
+                        if (power < B.hi) {
+                            if (araw < kFloorLo) continue;
+                            if (araw < kFloorHi &&
+                                !(alpha_raw_f64_cold(a.splat, a.exact, C.row, ox + lx,
+                                                     oy + ly0 + 2 * p) >= kFloor))
+                                continue;
+                        }
+                        pair(p, dy, araw, true);
+                    }
+                } else {
+#pragma unroll
+                    for (int p = 0; p < kPix; ++p) {
+                        if (jrel >= mylast[p]) continue;
+                        const float dy = fy[p] - A.my;
+                        const float power = dx * fmaf(A.B, dy, tA) + B.C * dy * dy;
+                        if (power < skipv) continue;
+                        const float araw = B.op * ex2_ftz(power);
+                        bool unclamped = araw < kClampLo;
+                        if (power < B.hi || fabsf(araw - kClampMid) < kClampHalf) {
+                            // near a gate (rare): the full decision from alpha_raw, with
+                            // both gates re-decided from the float64 record in the guard bands
+                            if (araw < kFloorLo) continue;
+                            if (araw < kFloorHi || fabsf(araw - kClampMid) < kClampHalf) {
+                                const double e = alpha_raw_f64_cold(a.splat, a.exact, C.row,
+                                                                    ox + lx, oy + ly0 + 2 * p);
+                                if (!(e >= kFloor)) continue;
+                                unclamped = e < kClamp;
+                            }
+                        }
+                        pair(p, dy, araw, unclamped);
+                    }
                 }
             }
             const float sdpx = sdp * dx;

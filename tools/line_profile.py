@@ -1,6 +1,8 @@
 """Warp-stall samples and executed instructions per CUDA source line for one kernel.
 
-    python tools/line_profile.py report.ncu-rep build/obj/<unit>.o <kernel-regex> <mangled-substring> [n]
+    python tools/line_profile.py report.ncu-rep|source.csv build/obj/<unit>.o <kernel-regex> <mangled-substring> [n]
+
+(a .csv argument is an `ncu -i rep --page source --csv -k <kernel>` export)
 
 Maps the ncu SASS page (absolute addresses) onto `nvdisasm -g` line info of the
 same object's cubin (function-relative offsets)."""
@@ -25,8 +27,11 @@ for l in body.splitlines():
     m = re.search(r"/\*([0-9a-f]{4,})\*/", l)
     if m and line:
         off2line[int(m.group(1), 16)] = line
-raw = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv", "--print-source", "sass", "-k",
-                      "regex:" + kre], capture_output=True, text=True).stdout
+if rep.endswith(".csv"):
+    raw = open(rep).read()
+else:
+    raw = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv", "--print-source", "sass",
+                          "-k", "regex:" + kre], capture_output=True, text=True).stdout
 rows = list(csv.reader(io.StringIO(raw)))
 hdr = rows[1]
 idx = {h: i for i, h in enumerate(hdr)}
