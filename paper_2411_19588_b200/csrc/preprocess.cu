@@ -21,9 +21,15 @@
 namespace uws {
 namespace {
 
+#ifndef UWS_PRE_IPT
+#define UWS_PRE_IPT 2
+#endif
+#ifndef UWS_PRE_MINB
+#define UWS_PRE_MINB 8
+#endif
 constexpr int kThreads = 128;
-constexpr int kIpt = 2;
-constexpr int kMinBlocks = 8;
+constexpr int kIpt = UWS_PRE_IPT;
+constexpr int kMinBlocks = UWS_PRE_MINB;
 
 struct Proj {
     double mx, my, depth, a, b, c, radius, k0, k1, k2, s;
