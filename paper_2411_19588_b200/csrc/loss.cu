@@ -63,6 +63,13 @@ __device__ __forceinline__ void cp_async4(float* sdst, const float* gsrc, bool o
                  "r"(ok ? 4 : 0)
                  : "memory");
 }
+// 16-byte asynchronous global -> shared copy; ok = false writes zeros
+__device__ __forceinline__ void cp_async16(float* sdst, const float* gsrc, bool ok) {
+    const unsigned s = (unsigned)__cvta_generic_to_shared(sdst);
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(s), "l"(gsrc),
+                 "r"(ok ? 16 : 0)
+                 : "memory");
+}
 __device__ __forceinline__ void cp_async_commit() {
     asm volatile("cp.async.commit_group;" ::: "memory");
 }
@@ -71,7 +78,17 @@ __device__ __forceinline__ void cp_async_wait() {
     asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
 }
 
-constexpr size_t kGradSmem = (size_t)(2 * 3 * kP * (kP + 1) + 3 * kP * (kT + 1)) * sizeof(float);
+// Derivative-map planes are stored with kMapPad zero columns on the left (window x at
+// column x + kMapPad) and zero columns up to the row pitch on the right, so the grad
+// pass stages each block's 42-column window as 11 aligned 16-byte chunks per row
+// (x0 - 2R + kMapPad = x0: 16-byte aligned since x0 is a multiple of 32).
+constexpr int kMapPad = 2 * kR;
+constexpr int kMP = 44;              // staged window row: 42 columns rounded up to 16 bytes
+constexpr size_t kGradSmem = (size_t)(2 * 3 * kP * kMP + 3 * kP * (kT + 1)) * sizeof(float);
+
+__host__ __device__ constexpr int map_pitch(int w) {  // floats per map row
+    return kT * ((w + kT - 1) / kT) + 12;
+}
 
 __device__ __forceinline__ float block_sum_f(float v, float* sred) {
     v = warp_sum(v);
@@ -103,7 +120,23 @@ __global__ void __launch_bounds__(kThreads, 3) k_ssim_moments(const float* __res
     __shared__ float sred[kThreads / 32];
     const int x0 = blockIdx.x * kT, y0 = blockIdx.y * kT;  // valid-window origin == image pixel
     const int VW = W - 2 * kR, VH = H - 2 * kR;
-    const size_t plane = (size_t)VH * VW;
+    const int MPW = map_pitch(W);
+    const size_t plane = (size_t)VH * MPW;
+    // zero pad columns of this block's map rows: the left pad [0, kMapPad) in the first
+    // column of blocks, everything right of the valid windows [VW + kMapPad, MPW) in the last
+    {
+        const int left = blockIdx.x == 0 ? kMapPad : 0;
+        const int rfirst = VW + kMapPad;
+        const int right = blockIdx.x == gridDim.x - 1 ? MPW - rfirst : 0;
+        const int per_row = left + right;
+        for (int i = threadIdx.x; i < kT * 3 * C * per_row; i += kThreads) {
+            const int k = i % per_row, rest = i / per_row;
+            const int r = rest % kT, m = rest / kT;
+            const int col = k < left ? k : rfirst + (k - left);
+            const int oy = y0 + r;
+            if (oy < VH) maps[(size_t)m * plane + (size_t)oy * MPW + col] = 0.f;
+        }
+    }
     // stage rows of kP*C contiguous floats (coalesced): one warp per row, every
     // copy asynchronous so all of the patch's loads are in flight at once
     {
@@ -206,7 +239,7 @@ __global__ void __launch_bounds__(kThreads, 3) k_ssim_moments(const float* __res
                 const float inv = r1 * r2;
                 const float S = A1 * A2 * inv;
                 ssum += S;
-                const size_t o = (size_t)oy * VW + ox;
+                const size_t o = (size_t)oy * MPW + ox + kMapPad;
                 maps[(0 * C + ch) * plane + o] = 2.0f * u2 * (A2 - A1) * inv - 2.0f * u1 * S * (r1 - r2);
                 maps[(1 * C + ch) * plane + o] = -S * r2;
                 maps[(2 * C + ch) * plane + o] = 2.0f * A1 * inv;
@@ -233,33 +266,43 @@ __global__ void __launch_bounds__(kThreads, 3) k_ssim_grad(const float* __restri
     // double-buffered derivative-map windows [2][3][kP][kP+1] (cp.async: the next
     // channel's window streams in while this channel is filtered), then hs
     extern __shared__ float smem[];
-    typedef float Win[3][kP][kP + 1];
+    typedef float Win[3][kP][kMP];
     Win* sbuf = reinterpret_cast<Win*>(smem);
-    float (*hs)[kP][kT + 1] = reinterpret_cast<float (*)[kP][kT + 1]>(smem + 2 * 3 * kP * (kP + 1));
+    float (*hs)[kP][kT + 1] = reinterpret_cast<float (*)[kP][kT + 1]>(smem + 2 * 3 * kP * kMP);
     __shared__ float sred[kThreads / 32];
     const int C = CT > 0 ? CT : C_;
     const int x0 = blockIdx.x * kT, y0 = blockIdx.y * kT;
-    const int VW = W - 2 * kR, VH = H - 2 * kR;
-    const size_t plane = (size_t)VH * VW;
+    const int VH = H - 2 * kR;
+    const int MPW = map_pitch(W);
+    const size_t plane = (size_t)VH * MPW;
     // adj[y][x] = sum_{u,v} w_u w_v M[y+u-2R][x+v-2R], M zero outside the valid grid
-    auto issue = [&](int ch) {  // one warp per window row (kP = 42 columns: 2 per lane)
+    // (zero pad columns in the planes, zero fill for rows outside)
+    // chunk i = threadIdx.x + 256 k of [3 maps][kP rows][kMP/4 chunks]: its (map, row, chunk)
+    // advance by (0, 23, 3) per step (256 = 23 * 11 + 3), with carries -- no divisions
+    constexpr int kCh = kMP / 4;
+    static_assert(kThreads == 23 * kCh + 3, "chunk stepping");
+    const int c4_0 = threadIdx.x % kCh, r_0 = (threadIdx.x / kCh) % kP;
+    auto issue = [&](int ch) {  // 3 maps x 42 rows x 11 aligned 16-byte chunks
         Win& dst = sbuf[ch & 1];
-        const int lane = threadIdx.x & 31;
-        const float* m0 = maps + (size_t)(0 * C + ch) * plane;
-        const float* m1 = maps + (size_t)(1 * C + ch) * plane;
-        const float* m2 = maps + (size_t)(2 * C + ch) * plane;
-        for (int r = threadIdx.x >> 5; r < kP; r += kThreads / 32) {
-            const int my = y0 + r - 2 * kR;
-            const bool rok = my >= 0 && my < VH;
+        const float* mp = maps + (size_t)ch * plane + x0;
+        int c4 = c4_0, r = r_0, m = 0;
 #pragma unroll
-            for (int c = lane; c < 64; c += 32) {
-                if (c >= kP) break;
-                const int mx = x0 + c - 2 * kR;
-                const bool ok = rok && mx >= 0 && mx < VW;
-                const size_t o = ok ? (size_t)my * VW + mx : 0;
-                cp_async4(&dst[0][r][c], m0 + o, ok);
-                cp_async4(&dst[1][r][c], m1 + o, ok);
-                cp_async4(&dst[2][r][c], m2 + o, ok);
+        for (int k = 0; k < (3 * kP * kCh + kThreads - 1) / kThreads; ++k) {
+            if (m < 3) {
+                const int my = y0 + r - 2 * kR;
+                const bool ok = my >= 0 && my < VH;
+                const float* src = mp + (size_t)m * C * plane + (size_t)(ok ? my : 0) * MPW + 4 * c4;
+                cp_async16(&dst[m][r][4 * c4], src, ok);
+            }
+            c4 += 3;
+            r += 23;
+            if (c4 >= kCh) {
+                c4 -= kCh;
+                ++r;
+            }
+            if (r >= kP) {
+                r -= kP;
+                ++m;
             }
         }
         cp_async_commit();
@@ -274,7 +317,7 @@ __global__ void __launch_bounds__(kThreads, 3) k_ssim_grad(const float* __restri
             cp_async_wait<0>();
         }
         __syncthreads();
-        float (*sm)[kP][kP + 1] = sbuf[ch & 1];
+        float (*sm)[kP][kMP] = sbuf[ch & 1];
         for (int it = threadIdx.x; it < kP * (kT / kHR); it += kThreads) {
             const int r = it >> 2, c0 = (it & 3) * kHR;
             float2 g01[kHR];
@@ -416,14 +459,14 @@ int ensure_taps() {
 }
 
 struct LossPlan {
-    float* maps;  // [3 maps][C][VH][VW]
+    float* maps;  // [3 maps][C][VH][map_pitch(W)] (zero-padded rows)
     double *part_s, *part_l1;
     int n_s, n_l1;
 };
 
 void plan_loss(Workspace& ws, int h, int w, int c, LossPlan& p) {
     int vh = h - 2 * kR > 0 ? h - 2 * kR : 1, vw = w - 2 * kR > 0 ? w - 2 * kR : 1;
-    p.maps = ws.take<float>((size_t)vh * vw * c * 3);
+    p.maps = ws.take<float>((size_t)vh * map_pitch(w) * c * 3);
     p.n_s = (int)(ceil_div(vw, kT) * ceil_div(vh, kT));
     p.n_l1 = (int)(ceil_div(w, kT) * ceil_div(h, kT));
     p.part_s = ws.take<double>(p.n_s);
