@@ -650,7 +650,7 @@ def backward(out, dL_dC, n_source, medium=None, lambda_guide=0.0, tiles=None, sc
 
 
 # ---------------------------------------------------------------------------
-# optimizer (optim.py:55-120, scene.py:132-134, 207-211)
+# optimizer (optim.py:55-120, scene.py:132-134, 174-178)
 # ---------------------------------------------------------------------------
 def position_lr(iteration, lr_init=0.00016, lr_final=0.0000016, delay_mult=0.01,
                 max_steps=30000, spatial_scale=1.0):

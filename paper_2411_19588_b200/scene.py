@@ -66,7 +66,7 @@ def feature_to_rgb(f):
 
 @dataclass
 class Gaussian:
-    """One primitive as host float64 values (reference scene.py:60-74)."""
+    """One primitive as host float64 values (reference scene.py:61-75)."""
 
     position: np.ndarray
     log_scale: np.ndarray
@@ -85,14 +85,14 @@ class Gaussian:
 
 
 def covariance(g: Gaussian) -> np.ndarray:
-    """World covariance (R diag(e^s)) (R diag(e^s))^T of one primitive (scene.py:77-81).
+    """World covariance (R diag(e^s)) (R diag(e^s))^T of one primitive (scene.py:78-82).
     Scalar host helper; the device kernels form it per Gaussian in float64."""
     m = quat_to_rotmat(g.rotation) * np.exp(g.log_scale)[None, :]
     return m @ m.T
 
 
 def opacity(g: Gaussian) -> float:
-    """sigmoid(logit) as 1 / (1 + exp(-x)) (scene.py:84-86; scipy expit's formula)."""
+    """sigmoid(logit) as 1 / (1 + exp(-x)) (scene.py:85-87; scipy expit's formula)."""
     return float(1.0 / (1.0 + np.exp(-g.opacity_logit)))
 
 
@@ -201,7 +201,7 @@ class GaussianCloud:
         return torch.clamp(self.sh_coeffs[:, 0, :].double() * SH_C0 + 0.5, min=0.0)
 
     def gaussian(self, i: int) -> Gaussian:
-        """Primitive ``i`` as a host Gaussian (scene.py:140-148)."""
+        """Primitive ``i`` as a host Gaussian (scene.py:122-130)."""
         row = {name: getattr(self, name)[i].detach().cpu().double().numpy()
                for name in CLOUD_FIELDS}
         return Gaussian(row["positions"], row["log_scales"], row["rotations"],
