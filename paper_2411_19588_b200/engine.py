@@ -107,6 +107,10 @@ class StepEngine:
         # parity tests: leave the step's summed gradients in ``grads`` after Adam
         # (Adam normally consumes and zeroes them)
         self.keep_gradients = False
+        # run-to-run bit-identical gradients (backward.py:334-341's fixed tile-order merge):
+        # the deterministic backward, at the cost of one host read per view (slot count)
+        self.deterministic = False
+        self._det_ws = None
         self.copy_stream = torch.cuda.Stream(device=dev)
 
     def _alloc(self, n: int):
@@ -232,10 +236,13 @@ class StepEngine:
         total_loss_device(out.color, gt, medium, self.cfg.lambda_ssim, self.cfg.lambda_guide,
                           result=rec[_ST_LOSS:_ST_LOSS + 6], grad=self.dL, workspace=self.loss_ws,
                           nonfinite=self.grads.nonfinite)
-        _lib.call("uws_raster_bwd_rows", ctypes.byref(pc), _lib.ptr(self.row_start),
-                  _lib.ptr(self.row_items), ctypes.byref(cc), _lib.ptr(medium.flat),
-                  ctypes.byref(oc), _lib.ptr(self.dL), _lib.ptr(self.screen),
-                  _lib.ptr(self.med_acc), st)
+        if self.deterministic:
+            self._raster_bwd_det(pc, cc, oc, medium, st)
+        else:
+            _lib.call("uws_raster_bwd_rows", ctypes.byref(pc), _lib.ptr(self.row_start),
+                      _lib.ptr(self.row_items), ctypes.byref(cc), _lib.ptr(medium.flat),
+                      ctypes.byref(oc), _lib.ptr(self.dL), _lib.ptr(self.screen),
+                      _lib.ptr(self.med_acc), st)
         cl = cloud.c_struct()
         guided = 1 if medium.has_guidance else 0
         _lib.call("uws_preprocess_bwd", ctypes.byref(cl), ctypes.byref(cc), ctypes.byref(pc),
@@ -243,6 +250,29 @@ class StepEngine:
                   guided, float(self.cfg.lambda_guide), _lib.ptr(self.grads.flat),
                   _lib.ptr(self.grads.nonfinite), 1 if view > 0 else 0, st)
         # (the first view stores: Adam leaves the parameter gradients zeroed)
+
+    def _raster_bwd_det(self, pc, cc, oc, medium, st):
+        """Deterministic K8 on the row lists (uws_raster_bwd_det): slot partials summed
+        per Gaussian in tile order.  Reads the slot count (one sync per view)."""
+        tiles = self.gx * self.gy
+        if self._det_ws is None:
+            self._det_ws = (torch.empty(tiles, dtype=torch.int32, device=self.dev),
+                            torch.empty(tiles + 1, dtype=torch.int32, device=self.dev),
+                            torch.empty(1, dtype=torch.uint8, device=self.dev))
+        count, base, ws = self._det_ws
+        _lib.call("uws_raster_bwd_det_prefix", ctypes.byref(cc), ctypes.byref(oc),
+                  _lib.ptr(count), _lib.ptr(base), st)
+        r = int(base[tiles].item())
+        k = self.proj.k
+        nb = _lib.size_out()
+        _lib.call("uws_raster_bwd_det_workspace_size", tiles, r, k, ctypes.byref(nb))
+        if ws.numel() < nb.value:
+            ws = torch.empty(int(nb.value * 1.25) + 1, dtype=torch.uint8, device=self.dev)
+            self._det_ws = (count, base, ws)
+        _lib.call("uws_raster_bwd_det", ctypes.byref(pc), 0, 0, _lib.ptr(self.row_start),
+                  _lib.ptr(self.row_items), ctypes.byref(cc), _lib.ptr(medium.flat),
+                  ctypes.byref(oc), _lib.ptr(self.dL), _lib.ptr(self.screen),
+                  _lib.ptr(self.med_acc), _lib.ptr(base), r, k, _lib.ptr(ws), ws.numel(), st)
 
     def last_render(self) -> RenderOutput:
         """Forward buffers of the most recent view (valid until the next step).
