@@ -22,6 +22,17 @@ def num(d, k):
         return float("nan")
 
 
+# pipe utilisation and shared-memory throughput (north_star: SM/LSU and shared-memory
+# throughput for rasterization)
+PIPES = (("fma_cycles", "sm__pipe_fma_cycles_active.avg.pct_of_peak_sustained_active"),
+         ("fma_inst", "sm__inst_executed_pipe_fma.avg.pct_of_peak_sustained_active"),
+         ("alu", "sm__inst_executed_pipe_alu.avg.pct_of_peak_sustained_active"),
+         ("lsu", "sm__inst_executed_pipe_lsu.avg.pct_of_peak_sustained_active"),
+         ("xu", "sm__inst_executed_pipe_xu.avg.pct_of_peak_sustained_active"),
+         ("fp64", "sm__pipe_fp64_cycles_active.avg.pct_of_peak_sustained_active"))
+SMEM = "l1tex__data_pipe_lsu_wavefronts_mem_shared.sum.pct_of_peak_sustained_elapsed"
+CONFL = "l1tex__data_bank_conflicts_pipe_lsu_mem_shared.sum"
+
 lines, traffic, seen = [], {}, set()
 for d in rows[2:]:
     name = d[idx["Kernel Name"]].split("(")[0].replace("uws::<unnamed>::", "").replace("void ", "")
@@ -40,7 +51,10 @@ for d in rows[2:]:
         f"{num(d, 'sm__warps_active.avg.pct_of_peak_sustained_active'):5.1f}%  regs "
         f"{d[idx['launch__registers_per_thread']]:>3}\n      stalls: " +
         ", ".join(f"{h.replace('smsp__average_warps_issue_stalled_', '').replace('_per_issue_active.ratio', '')}"
-                  f"={v:.2f}" for v, h in st))
+                  f"={v:.2f}" for v, h in st) +
+        "\n      pipes (% of peak, active): " + ", ".join(
+            f"{lbl}={num(d, m):.1f}" for lbl, m in PIPES) +
+        f"; smem wavefronts {num(d, SMEM):.1f}% (bank conflicts {num(d, CONFL):.0f})")
 with open(out_txt, "w") as f:
     f.write(f"ncu --set full --clock-control none (single launches, cold cache, serialised); {rep}\n")
     f.write("\n".join(lines) + "\n")
