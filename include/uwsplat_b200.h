@@ -75,6 +75,9 @@ typedef struct uws_projected {
     double* cov2d;           /* optional [K][3] packed a,b,c (NULL to skip) */
     double* radius;          /* optional [K] footprint radius (NULL to skip) */
     int32_t* num_visible;    /* [1] K, written by uws_preprocess_fwd */
+    uint32_t* depth_range;   /* optional [2] {~min, max} of the visible depths' high 32 bits,
+                                written by uws_preprocess_fwd for uws_bin_count (NULL: the
+                                binning finds them itself) */
 } uws_projected;
 
 /* Per-pixel forward outputs (RenderOutput, rasterizer.py:132-145).  All

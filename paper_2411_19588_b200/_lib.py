@@ -35,7 +35,7 @@ class CloudC(ctypes.Structure):
 class ProjectedC(ctypes.Structure):
     _fields_ = [("source_index", c_void_p), ("splat", c_void_p), ("exact", c_void_p),
                 ("depth", c_void_p), ("rect", c_void_p), ("cov2d", c_void_p),
-                ("radius", c_void_p), ("num_visible", c_void_p)]
+                ("radius", c_void_p), ("num_visible", c_void_p), ("depth_range", c_void_p)]
 
 
 class RasterOutC(ctypes.Structure):

@@ -568,7 +568,6 @@ __global__ void __launch_bounds__(kThreads) k_cell_scatter(const uint2* __restri
 // workspace plans
 // ---------------------------------------------------------------------------
 struct CountPlan {
-    uint32_t* keys_hi;            // high words of the depth bits
     uint32_t* sorted_rows;        // rows in (depth, row) order
     uint32_t* tmp;                // scratch rows (long-bucket counting sort)
     depth_bucket::Meta* meta;     // -- zeroed per call: meta, scan status, bucket counts --
@@ -590,7 +589,6 @@ static_assert(depth_bucket::kBuckets % (kThreads * kScanIpt) == 0, "bucket scan 
 void plan_count(Workspace& ws, uint32_t k, int nbands, CountPlan& p) {
     const uint32_t kk = k > 0 ? k : 1;
     p.nblk_r = (uint32_t)ceil_div(kk, kBlockItems);
-    p.keys_hi = ws.take<uint32_t>(kk);
     p.sorted_rows = ws.take<uint32_t>(kk);
     p.tmp = ws.take<uint32_t>(kk);
     p.meta = ws.take<depth_bucket::Meta>(1);
@@ -681,16 +679,20 @@ extern "C" int uws_bin_count(const uws_projected* proj, int64_t k_cap, const uws
     namespace db = depth_bucket;
     const unsigned kb = (unsigned)ceil_div(kc, 256);
     UWS_CUDA(zero_async(p.meta, (char*)(p.bcount + db::kBuckets) - (char*)p.meta, st));
-    launch(db::k_hi_minmax, dim3(kb), dim3(256), 0, st, dbits, k_dev, kc, p.keys_hi, p.meta);
-    UWS_CHECK_LAUNCH("k_hi_minmax");
-    launch(db::k_bucket_count, dim3(kb), dim3(256), 0, st, (const uint32_t*)p.keys_hi, k_dev, kc,
-           (const db::Meta*)p.meta, p.bcount);
+    // the visible depths' high-word range: from the preprocess kernel when it wrote it
+    const uint32_t* range = proj->depth_range;
+    if (!range) {
+        launch(db::k_hi_minmax, dim3(kb), dim3(256), 0, st, dbits, k_dev, kc, p.meta);
+        UWS_CHECK_LAUNCH("k_hi_minmax");
+        range = &p.meta->neg_min;
+    }
+    launch(db::k_bucket_count, dim3(kb), dim3(256), 0, st, dbits, k_dev, kc, range, p.bcount);
     UWS_CHECK_LAUNCH("k_bucket_count");
     launch(k_scan_u32, dim3(kBucketScanTiles), dim3(kThreads), 0, st, (const uint32_t*)p.bcount,
            p.bstart, db::kBuckets, (uint32_t*)nullptr, p.bstat, p.bticket);
     UWS_CHECK_LAUNCH("k_scan_u32");
-    launch(db::k_bucket_scatter, dim3(kb), dim3(256), 0, st, (const uint32_t*)p.keys_hi, k_dev, kc,
-           (const db::Meta*)p.meta, p.bstart, p.sorted_rows);
+    launch(db::k_bucket_scatter, dim3(kb), dim3(256), 0, st, dbits, k_dev, kc, range, p.bstart,
+           p.sorted_rows);
     UWS_CHECK_LAUNCH("k_bucket_scatter");
     launch(db::k_bucket_fix, dim3(db::kBuckets / 256), dim3(256), 0, st, (const uint32_t*)p.bstart,
            dbits, p.sorted_rows, p.meta, p.wlist, p.clist);

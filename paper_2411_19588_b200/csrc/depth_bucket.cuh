@@ -35,8 +35,10 @@ struct Meta {
     uint32_t neg_min, max, n_warp, n_cta;
 };
 
-__device__ __forceinline__ uint32_t bucket_shift(const Meta* m) {
-    const uint32_t span = m->max - ~m->neg_min;
+// range = {~min, max} of the keys' high words (Meta's first two fields, or the
+// preprocess kernel's uws_projected.depth_range)
+__device__ __forceinline__ uint32_t bucket_shift(const uint32_t* range) {
+    const uint32_t span = range[1] - ~range[0];
     const int bits = span ? 32 - __clz(span) : 0;
     return bits > kLogBuckets ? (uint32_t)(bits - kLogBuckets) : 0u;
 }
@@ -48,17 +50,14 @@ __device__ __forceinline__ bool key_less(uint64_t ka, uint32_t ra, uint64_t kb, 
 // high words of the keys and their min / max
 __global__ void __launch_bounds__(256) k_hi_minmax(const uint64_t* __restrict__ depth_bits,
                                                    const uint32_t* __restrict__ n_dev,
-                                                   uint32_t n_cap, uint32_t* __restrict__ keys,
-                                                   Meta* meta) {
+                                                   uint32_t n_cap, Meta* meta) {
     pdl_entry();
     __shared__ uint32_t s_lo[8], s_hi[8];
     const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
     const uint32_t n = min(*n_dev, n_cap);
     uint32_t lo = 0xffffffffu, hi = 0u;
     if (i < n) {
-        const uint32_t k = (uint32_t)(depth_bits[i] >> 32);
-        keys[i] = k;
-        lo = hi = k;
+        lo = hi = (uint32_t)(depth_bits[i] >> 32);
     }
     lo = __reduce_min_sync(0xffffffffu, lo);
     hi = __reduce_max_sync(0xffffffffu, hi);
@@ -78,30 +77,34 @@ __global__ void __launch_bounds__(256) k_hi_minmax(const uint64_t* __restrict__ 
     }
 }
 
-__global__ void __launch_bounds__(256) k_bucket_count(const uint32_t* __restrict__ keys,
+__device__ __forceinline__ uint32_t key_hi(const uint64_t* depth_bits, uint32_t i) {
+    return (uint32_t)(depth_bits[i] >> 32);
+}
+
+__global__ void __launch_bounds__(256) k_bucket_count(const uint64_t* __restrict__ depth_bits,
                                                       const uint32_t* __restrict__ n_dev,
-                                                      uint32_t n_cap, const Meta* __restrict__ meta,
+                                                      uint32_t n_cap, const uint32_t* __restrict__ range,
                                                       uint32_t* __restrict__ count) {
     pdl_entry();
     const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
     const uint32_t n = min(*n_dev, n_cap);
     if (i >= n) return;
-    const uint32_t kmin = ~meta->neg_min, sh = bucket_shift(meta);
-    atomicAdd(&count[(keys[i] - kmin) >> sh], 1u);
+    const uint32_t kmin = ~range[0], sh = bucket_shift(range);
+    atomicAdd(&count[min((key_hi(depth_bits, i) - kmin) >> sh, kBuckets - 1)], 1u);
 }
 
 // start[] = exclusive bucket starts on entry, bucket ends on exit
-__global__ void __launch_bounds__(256) k_bucket_scatter(const uint32_t* __restrict__ keys,
+__global__ void __launch_bounds__(256) k_bucket_scatter(const uint64_t* __restrict__ depth_bits,
                                                         const uint32_t* __restrict__ n_dev,
-                                                        uint32_t n_cap, const Meta* __restrict__ meta,
+                                                        uint32_t n_cap, const uint32_t* __restrict__ range,
                                                         uint32_t* __restrict__ start,
                                                         uint32_t* __restrict__ rows) {
     pdl_entry();
     const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
     const uint32_t n = min(*n_dev, n_cap);
     if (i >= n) return;
-    const uint32_t kmin = ~meta->neg_min, sh = bucket_shift(meta);
-    rows[atomicAdd(&start[(keys[i] - kmin) >> sh], 1u)] = i;
+    const uint32_t kmin = ~range[0], sh = bucket_shift(range);
+    rows[atomicAdd(&start[min((key_hi(depth_bits, i) - kmin) >> sh, kBuckets - 1)], 1u)] = i;
 }
 
 // One thread per bucket: short buckets sorted in registers, longer ones listed.
@@ -119,6 +122,14 @@ __global__ void __launch_bounds__(256) k_bucket_fix(const uint32_t* __restrict__
     if (len > (uint32_t)kThreadRun) {
         if (len <= 32u) warp_list[atomicAdd(&meta->n_warp, 1u)] = b;
         else cta_list[atomicAdd(&meta->n_cta, 1u)] = b;
+        return;
+    }
+    if (len == 2) {  // the common non-trivial case (~1-3 rows per bucket): one exchange
+        const uint32_t r0 = rows[lo], r1 = rows[lo + 1];
+        if (key_less(depth_bits[r1], r1, depth_bits[r0], r0)) {
+            rows[lo] = r1;
+            rows[lo + 1] = r0;
+        }
         return;
     }
     uint32_t r[kThreadRun];

@@ -155,9 +155,35 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) k_preprocess(uws_cloud c
     }
     __syncthreads();
     unsigned long long row = s_base + ex;
+    uint32_t dlo = 0xffffffffu, dhi = 0u;  // high words of the visible depths (binning's range)
 #pragma unroll
     for (int q = 0; q < kIpt; ++q)
-        if (vis[q]) emit_row(out, row++, i0 + q, p[q]);
+        if (vis[q]) {
+            emit_row(out, row++, i0 + q, p[q]);
+            const uint32_t h = (uint32_t)(__double_as_longlong(p[q].depth) >> 32);
+            dlo = min(dlo, h);
+            dhi = max(dhi, h);
+        }
+    if (out.depth_range) {
+        dlo = __reduce_min_sync(0xffffffffu, dlo);
+        dhi = __reduce_max_sync(0xffffffffu, dhi);
+        if ((threadIdx.x & 31) == 0) {
+            s_scan[threadIdx.x >> 5] = ((unsigned long long)dhi << 32) | (~dlo);
+        }
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            uint32_t nlo = 0u, hi = 0u;
+#pragma unroll
+            for (int w = 0; w < kThreads / 32; ++w) {
+                nlo = max(nlo, (uint32_t)s_scan[w]);
+                hi = max(hi, (uint32_t)(s_scan[w] >> 32));
+            }
+            if (nlo != 0u) {   // some visible row in the block
+                atomicMax(&out.depth_range[0], nlo);
+                atomicMax(&out.depth_range[1], hi);
+            }
+        }
+    }
     if (tile == (int)gridDim.x - 1 && threadIdx.x == kThreads - 1)
         *out.num_visible = (int32_t)(s_base + total);
 }
@@ -196,6 +222,7 @@ extern "C" int uws_preprocess_fwd(const uws_cloud* cloud, const uws_camera* cam,
     auto* ticket = ws.take<unsigned>(1);
     UWS_REQUIRE(ws.ok(), "uws_preprocess_fwd: workspace too small");
     UWS_CUDA(zero_async(status, (char*)(ticket + 1) - (char*)status, st));
+    if (out->depth_range) UWS_CUDA(zero_async(out->depth_range, 2 * sizeof(uint32_t), st));
     launch_serial(k_preprocess, dim3((unsigned)blocks), dim3(kThreads), 0, st, *cloud, *cam, *out, gx, gy, status, ticket);
     UWS_CHECK_LAUNCH("k_preprocess");
     return UWS_OK;

@@ -60,13 +60,15 @@ class ProjectedCloud:
         self._cov2d = torch.empty(cap, 3, dtype=torch.float64, device=device) if with_geometry else None
         self._radius = torch.empty(cap, dtype=torch.float64, device=device) if with_geometry else None
         self._num_visible = torch.zeros(1, dtype=torch.int32, device=device)
+        # {~min, max} of the visible depths' high words (preprocess -> binning)
+        self._depth_range = torch.zeros(2, dtype=torch.int32, device=device)
         self._k = 0 if n_source == 0 else None   # host copy of K, read lazily
 
     def c_struct(self) -> _lib.ProjectedC:
         return _lib.ProjectedC(_lib.ptr(self._source_index), _lib.ptr(self._splat),
                                _lib.ptr(self._exact), _lib.ptr(self._depth), _lib.ptr(self._rect),
                                _lib.ptr(self._cov2d), _lib.ptr(self._radius),
-                               _lib.ptr(self._num_visible))
+                               _lib.ptr(self._num_visible), _lib.ptr(self._depth_range))
 
     @property
     def k(self) -> int:
