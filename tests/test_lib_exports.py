@@ -59,7 +59,7 @@ def test_struct_layouts_match_header():
     # offsets the kernels rely on (uws_splat is 48 bytes, camera doubles 8-aligned)
     assert ctypes.sizeof(_lib.CameraC) == 8 + 4 * 8 + 9 * 8 + 3 * 8 + 2 * 8
     assert ctypes.sizeof(_lib.CloudC) == 6 * 8
-    assert ctypes.sizeof(_lib.ProjectedC) == 8 * 8
+    assert ctypes.sizeof(_lib.ProjectedC) == 9 * 8
     # 11 pointers, int32 cap + padding, 2 fix-up pointers
     assert ctypes.sizeof(_lib.RasterOutC) == 11 * 8 + 8 + 2 * 8
     assert ctypes.sizeof(_lib.AdamParamsC) == 45 * 8
