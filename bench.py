@@ -443,8 +443,9 @@ def run_gpu(args):
         eng = trainer.engine if (rw, rh) == (W, H) else uw.StepEngine(state, rw, rh, cfg)
         rcam = uw.Camera.look_at(view_eye(rank), (0, 0, 12), width=rw, height=rh,
                                  fx=1.2 * rw, fy=1.2 * rw)
-        for _ in range(3):
-            eng.render(rcam)
+        for _ in range(4):            # both frame sets of the stream allocated and warm
+            eng.render_async(rcam)
+        eng.render_flush()
         nfr = max(args.steps, 10)
         barrier()
         t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)

@@ -102,6 +102,8 @@ class StepEngine:
         self._async_done = [torch.cuda.Event(), torch.cuda.Event()]
         self._async_frames = 0
         self._async_pending = None
+        self._fs = None          # the frame stream's second buffer set (lazy)
+        self._latest = None      # buffer set of the most recent frame (None: the engine's)
         self._k = 0
         self._pending = None
         # parity tests: leave the step's summed gradients in ``grads`` after Adam
@@ -149,62 +151,107 @@ class StepEngine:
 
     # -- forward of one view (render path) ----------------------------------------
     def _forward(self, cam: Camera, stats: torch.Tensor, view: int, mode: str = "underwater",
-                 train: bool = True):
+                 train: bool = True, fs: "_FrameSet" = None):
+        """Preprocess, depth order + row lists, compositing of one view into the
+        engine's buffers, or into frame set ``fs`` (the frame stream's second set)."""
+        b = self if fs is None else fs
         st = _lib.stream_handle()
         cloud, medium = self.state.cloud, self.state.medium
         cc = cam.c_struct()
-        preprocess_into(self.proj, cloud, cam, self.pre_ws)
-        pc = self.proj.c_struct()
+        preprocess_into(b.proj, cloud, cam, b.pre_ws)
+        pc = b.proj.c_struct()
         rec = stats[view * _ST_SIZE:(view + 1) * _ST_SIZE]
         totals = rec[_ST_TOTALS:_ST_TOTALS + 2].view(torch.int64)
         ovf = rec[_ST_OVF:_ST_OVF + 1].view(torch.int32)[:1]
         _lib.call("uws_bin_count", ctypes.byref(pc), self.n, ctypes.byref(cc), _lib.ptr(totals),
-                  _lib.ptr(self.count_ws), self.count_ws.numel(), st)
-        _lib.call("uws_bin_rows", ctypes.byref(pc), self.n, self.s_cap, ctypes.byref(cc),
-                  _lib.ptr(totals), _lib.ptr(self.row_start), _lib.ptr(self.row_items),
+                  _lib.ptr(b.count_ws), b.count_ws.numel(), st)
+        _lib.call("uws_bin_rows", ctypes.byref(pc), self.n, b.s_cap, ctypes.byref(cc),
+                  _lib.ptr(totals), _lib.ptr(b.row_start), _lib.ptr(b.row_items),
                   _lib.ptr(ovf), _lib.ptr(self.grads.nonfinite) if train else 0,
-                  _lib.ptr(self.count_ws), self.count_ws.numel(), st)
-        out = self.out
+                  _lib.ptr(b.count_ws), b.count_ws.numel(), st)
+        out = b.out
         oc = out.c_struct()
         med = _lib.ptr(medium.flat) if mode == "underwater" else 0
-        _lib.call("uws_raster_fwd_rows", ctypes.byref(pc), _lib.ptr(self.row_start),
-                  _lib.ptr(self.row_items), ctypes.byref(cc), med, ctypes.byref(oc), st)
+        _lib.call("uws_raster_fwd_rows", ctypes.byref(pc), _lib.ptr(b.row_start),
+                  _lib.ptr(b.row_items), ctypes.byref(cc), med, ctypes.byref(oc), st)
         return cc, pc, oc, rec
 
     def render_async(self, cam, mode: str = "underwater") -> RenderOutput:
         """Queue one render-only frame without waiting for it (a frame stream).
 
-        The row-list overflow flag of the PREVIOUS queued frame is read after this
-        one is queued, so the host never idles the GPU between frames.  Every
-        frame writes the same output buffers: they hold a valid image only for
-        the most recent frame and only once ``render_flush()`` has returned (a
-        frame that overflowed its row lists is a medium-only image until then;
-        the flush grows the lists and renders the most recent frame again,
-        synchronously).  ``step_async`` and ``refresh_guidance`` flush a
-        pending frame first."""
+        Consecutive frames alternate between two buffer sets and two streams (the
+        engine's own buffers on the current stream, a second set on a side
+        stream), so frame i+1's preprocess and depth order -- latency-bound
+        kernels that leave most SMs idle -- run while frame i composites.  The
+        row-list overflow flag of the PREVIOUS queued frame is read after this one
+        is queued, so the host never idles the GPU between frames.  A frame's
+        buffers hold its image only once ``render_flush()`` has returned
+        (``last_render()`` then returns the most recent frame; a frame that
+        overflowed its row lists is re-rendered there, synchronously).  The
+        cloud must not change while frames are queued; ``step_async`` and
+        ``refresh_guidance`` flush a pending frame first."""
         cam = Camera.from_any(cam)
         if self._pending is None:
             self._sync_cloud()
         k = self._async_frames % 2
         self._async_frames += 1
-        stats = self._async_stats[k]
-        stats.zero_()
-        self._forward(cam, stats, 0, mode, train=False)
-        # the frame's overflow flag to pinned memory, behind the frame's kernels
-        self._async_flag[k].copy_(stats[_ST_OVF:_ST_OVF + 1].view(torch.int32), non_blocking=True)
-        self._async_done[k].record()
+        cur = torch.cuda.current_stream()
+        if k == 1:
+            fs = self._frame_set()
+            if self._async_pending is None:
+                # first side-stream frame of a stream: after everything queued so far
+                # (the parameters it reads)
+                fs.stream.wait_stream(cur)
+            stream_ctx = torch.cuda.stream(fs.stream)
+        else:
+            fs = None
+            stream_ctx = torch.cuda.stream(cur)
+        with stream_ctx:
+            stats = self._async_stats[k]
+            stats.zero_()
+            self._forward(cam, stats, 0, mode, train=False, fs=fs)
+            # the frame's overflow flag to pinned memory, behind the frame's kernels
+            self._async_flag[k].copy_(stats[_ST_OVF:_ST_OVF + 1].view(torch.int32),
+                                      non_blocking=True)
+            self._async_done[k].record()
+        (self.out if fs is None else fs.out).mode = mode
         prev, self._async_pending = self._async_pending, (cam, mode, k)
-        self.out.mode = mode
+        self._latest = fs
         if prev is not None and self._async_overflowed(prev[2]):
             self.render_flush()
-        return self.last_render()
+        return self._frame_output(fs)
 
     def render_flush(self) -> RenderOutput:
-        """Check the last queued frame (re-rendering it if its row lists overflowed)."""
+        """Wait for the queued frames; re-render the last one if its row lists overflowed.
+        Returns the most recent frame."""
         frame, self._async_pending = self._async_pending, None
+        if self._fs is not None:
+            torch.cuda.current_stream().wait_stream(self._fs.stream)
         if frame is not None and self._async_overflowed(frame[2]):
+            self._latest = None
             return self.render(frame[0], frame[1])
-        return self.last_render()
+        return self._frame_output(self._latest)
+
+    def _frame_set(self) -> "_FrameSet":
+        """The frame stream's second buffer set, (re)built for the engine's sizes."""
+        if self._fs is None or self._fs.n != self.n or self._fs.s_cap != self.s_cap:
+            if self._fs is not None:
+                self._fs.stream.synchronize()   # its buffers are freed below
+                stream = self._fs.stream
+            else:
+                stream = torch.cuda.Stream(device=self.dev)
+            self._fs = None
+            self._fs = _FrameSet(self, stream)
+        return self._fs
+
+    def _frame_output(self, fs) -> RenderOutput:
+        if fs is None:
+            return self.last_render()
+        out = fs.out
+        out.proj = fs.proj
+        out.bins = None
+        out.rows = RowLists(self.gx, self.gy, fs.row_start, fs.row_items)
+        return out
 
     def _async_overflowed(self, k: int) -> bool:
         self._async_done[k].synchronize()   # waits for that frame only
@@ -463,6 +510,21 @@ class StepEngine:
         Loss values in the returned stats are this rank's view averages."""
         self.step_async(views)
         return self.flush()
+
+
+class _FrameSet:
+    """A second set of forward buffers on a side stream (StepEngine.render_async)."""
+
+    def __init__(self, eng: StepEngine, stream):
+        dev = eng.dev
+        self.stream = stream
+        self.n, self.s_cap = eng.n, eng.s_cap
+        self.proj = ProjectedCloud(eng.n, dev, with_geometry=False)
+        self.pre_ws = torch.empty_like(eng.pre_ws)
+        self.count_ws = torch.empty_like(eng.count_ws)
+        self.row_start = torch.zeros_like(eng.row_start)
+        self.row_items = torch.empty_like(eng.row_items)
+        self.out = _alloc_output(eng.height, eng.width, dev, "underwater", False)
 
 
 class _Slot:

@@ -364,6 +364,17 @@ def test_render_async_stream_matches_render(capacity):
     out = eng.render_flush()
     for k, v in want.items():
         np.testing.assert_array_equal(np_(getattr(out, k)), v)
+    # an odd-length stream ends in the engine's own buffer set, an even one in the side
+    # set; a training step after the stream sees the right buffers either way
+    for c in (other, other, cam):
+        eng.render_async(c)
+    out = eng.render_flush()
+    for k, v in want.items():
+        np.testing.assert_array_equal(np_(getattr(out, k)), v)
+    gt = torch.as_tensor(g.gt, dtype=torch.float32).cuda()
+    eng.render_async(other)
+    st = eng.step([(cam, gt)])
+    assert not st.skipped and np.isfinite(st.total)
 
 
 def test_nonfinite_step_with_many_visible_gaussians_is_not_an_overflow():
