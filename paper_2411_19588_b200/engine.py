@@ -67,6 +67,8 @@ class EngineStats:
 class StepEngine:
     """Persistent-buffer, sync-free training step for one (cloud size, image size)."""
 
+    OVERLAP_VIEWS = True   # default of ``overlap_views``
+
     def __init__(self, state: TrainState, width: int, height: int, cfg: OptimConfig,
                  spatial_scale: float = 1.0, max_views: int = 1, entry_capacity: int = 0,
                  group=None):
@@ -103,6 +105,9 @@ class StepEngine:
         self._async_frames = 0
         self._async_pending = None
         self._fs = None          # the frame stream's second buffer set (lazy)
+        # steps over several views overlap consecutive views on two streams / buffer sets
+        self.overlap_views = self.OVERLAP_VIEWS
+        self._last_view_set = None  # buffer set holding the last step's last view
         self._latest = None      # buffer set of the most recent frame (None: the engine's)
         self._k = 0
         self._pending = None
@@ -232,8 +237,9 @@ class StepEngine:
             return self.render(frame[0], frame[1])
         return self._frame_output(self._latest)
 
-    def _frame_set(self) -> "_FrameSet":
-        """The frame stream's second buffer set, (re)built for the engine's sizes."""
+    def _frame_set(self, train: bool = False) -> "_FrameSet":
+        """The second buffer set (frame stream, overlapped views), (re)built for the
+        engine's sizes; ``train`` adds the loss / backward buffers."""
         if self._fs is None or self._fs.n != self.n or self._fs.s_cap != self.s_cap:
             if self._fs is not None:
                 self._fs.stream.synchronize()   # its buffers are freed below
@@ -242,6 +248,8 @@ class StepEngine:
                 stream = torch.cuda.Stream(device=self.dev)
             self._fs = None
             self._fs = _FrameSet(self, stream)
+        if train:
+            self._fs.add_training(self)
         return self._fs
 
     def _frame_output(self, fs) -> RenderOutput:
@@ -275,25 +283,33 @@ class StepEngine:
         return self.last_render()
 
     # -- one view: forward + loss + backward into self.grads -----------------------
-    def _view(self, cam: Camera, gt: torch.Tensor, stats: torch.Tensor, view: int):
+    def _view(self, cam: Camera, gt: torch.Tensor, stats: torch.Tensor, view: int,
+              fs: "_FrameSet" = None, after=None):
+        """Forward, loss and backward of one view into the engine's buffers (or
+        buffer set ``fs``); the projection backward -- the only stage writing the
+        shared gradient buffer -- first waits for event ``after`` (the previous
+        view's projection backward on the other stream)."""
+        b = self if fs is None else fs
         st = _lib.stream_handle()
         cloud, medium = self.state.cloud, self.state.medium
-        cc, pc, oc, rec = self._forward(cam, stats, view)
-        out = self.out
+        cc, pc, oc, rec = self._forward(cam, stats, view, fs=fs)
+        out = b.out
         total_loss_device(out.color, gt, medium, self.cfg.lambda_ssim, self.cfg.lambda_guide,
-                          result=rec[_ST_LOSS:_ST_LOSS + 6], grad=self.dL, workspace=self.loss_ws,
+                          result=rec[_ST_LOSS:_ST_LOSS + 6], grad=b.dL, workspace=b.loss_ws,
                           nonfinite=self.grads.nonfinite)
         if self.deterministic:
             self._raster_bwd_det(pc, cc, oc, medium, st)
         else:
-            _lib.call("uws_raster_bwd_rows", ctypes.byref(pc), _lib.ptr(self.row_start),
-                      _lib.ptr(self.row_items), ctypes.byref(cc), _lib.ptr(medium.flat),
-                      ctypes.byref(oc), _lib.ptr(self.dL), _lib.ptr(self.screen),
-                      _lib.ptr(self.med_acc), st)
+            _lib.call("uws_raster_bwd_rows", ctypes.byref(pc), _lib.ptr(b.row_start),
+                      _lib.ptr(b.row_items), ctypes.byref(cc), _lib.ptr(medium.flat),
+                      ctypes.byref(oc), _lib.ptr(b.dL), _lib.ptr(b.screen),
+                      _lib.ptr(b.med_acc), st)
+        if after is not None:
+            torch.cuda.current_stream().wait_event(after)
         cl = cloud.c_struct()
         guided = 1 if medium.has_guidance else 0
         _lib.call("uws_preprocess_bwd", ctypes.byref(cl), ctypes.byref(cc), ctypes.byref(pc),
-                  self.n, _lib.ptr(self.screen), _lib.ptr(self.med_acc), _lib.ptr(medium.flat),
+                  self.n, _lib.ptr(b.screen), _lib.ptr(b.med_acc), _lib.ptr(medium.flat),
                   guided, float(self.cfg.lambda_guide), _lib.ptr(self.grads.flat),
                   _lib.ptr(self.grads.nonfinite), 1 if view > 0 else 0, st)
         # (the first view stores: Adam leaves the parameter gradients zeroed)
@@ -359,8 +375,12 @@ class StepEngine:
     def _launch(self, slot: "_Slot"):
         cur = torch.cuda.current_stream()
         cur.wait_event(slot.copied)
-        for i, (cam, gt) in enumerate(slot.views):
-            self._view(cam, gt, slot.stats, i)
+        if len(slot.views) > 1 and self.overlap_views and not self.deterministic:
+            self._launch_views_overlapped(slot, cur)
+        else:
+            for i, (cam, gt) in enumerate(slot.views):
+                self._view(cam, gt, slot.stats, i)
+            self._last_view_set = None
         chunks = None
         if self.dist is not None and self.world > 1:
             chunks = self._all_reduce_gradients()
@@ -374,6 +394,24 @@ class StepEngine:
         slot.host.copy_(slot.stats, non_blocking=True)
         slot.done.record(cur)
         slot.free.record(cur)
+
+    def _launch_views_overlapped(self, slot: "_Slot", cur):
+        """Several views in one step: even views on the engine's buffers and the
+        current stream, odd views on the second buffer set and its stream, so a
+        view's preprocess / depth order / compositing overlap the previous view's
+        backward.  The projection backwards (the only writers of the gradient
+        buffer; view 0 stores, later views add) stay in view order through events."""
+        ts = self._frame_set(train=True)
+        ts.stream.wait_stream(cur)      # parameters (previous Adam) and ground-truth copies
+        prev = None
+        for i, (cam, gt) in enumerate(slot.views):
+            fs = ts if i % 2 else None
+            with torch.cuda.stream(ts.stream if i % 2 else cur):
+                self._view(cam, gt, slot.stats, i, fs=fs, after=prev)
+                prev = torch.cuda.Event()
+                prev.record()
+        cur.wait_stream(ts.stream)
+        self._last_view_set = ts if (len(slot.views) - 1) % 2 else None
 
     # gradient all-reduce: 1 = one NCCL all-reduce of the whole flat buffer, then
     # the single Adam launch (the default: the split form below has only been
@@ -502,7 +540,8 @@ class StepEngine:
                                "render_async frame has replaced it")
         if not isinstance(gt, torch.Tensor):
             gt = torch.from_numpy(np.ascontiguousarray(gt, dtype=np.float32))
-        return refresh_guidance(self.state.medium, gt, self.out.depth, **kw)
+        out = self.out if self._last_view_set is None else self._last_view_set.out
+        return refresh_guidance(self.state.medium, gt, out.depth, **kw)
 
     def step(self, views: Sequence) -> EngineStats:
         """One optimizer step over this rank's views, synchronously.
@@ -525,6 +564,14 @@ class _FrameSet:
         self.row_start = torch.zeros_like(eng.row_start)
         self.row_items = torch.empty_like(eng.row_items)
         self.out = _alloc_output(eng.height, eng.width, dev, "underwater", False)
+        self.dL = None
+
+    def add_training(self, eng: StepEngine):
+        if self.dL is None:
+            self.dL = torch.empty_like(eng.dL)
+            self.loss_ws = torch.empty_like(eng.loss_ws)
+            self.screen = torch.zeros_like(eng.screen)
+            self.med_acc = torch.zeros_like(eng.med_acc)
 
 
 class _Slot:

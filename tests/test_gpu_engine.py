@@ -243,6 +243,41 @@ def test_engine_two_views_per_step_equals_summed_api_gradients():
         np.testing.assert_array_equal(np_(getattr(sa.cloud, f)), v, err_msg=f)
 
 
+@pytest.mark.parametrize("nviews", [3, 4])
+def test_overlapped_views_equal_serial_views(nviews):
+    """Several views per step on two streams / buffer sets (overlap_views) == the same
+    views one after another on one stream: per-view losses and the summed gradients,
+    over two steps (the second after an Adam update), and the guidance refresh reads
+    the last view's depth from whichever set holds it."""
+    g = load("survey2k")
+    _, cam0 = _state(g)
+    cams = [cam0] + [uw.Camera.look_at((2.5 - 0.2 * k, -2.2 + 0.1 * k, -1.2), (0, 0, 12),
+                                       width=cam0.width, height=cam0.height, fx=cam0.fx,
+                                       fy=cam0.fy) for k in range(1, nviews)]
+    gt = torch.as_tensor(g.gt, dtype=torch.float32).cuda()
+    res = []
+    for overlap in (False, True):
+        s, _ = _state(g)
+        eng = uw.StepEngine(s, cams[0].width, cams[0].height, uw.OptimConfig(), max_views=nviews)
+        eng.overlap_views = overlap
+        eng.keep_gradients = True
+        stats = []
+        for _ in range(2):
+            st = eng.step([(c, gt) for c in cams])
+            assert not st.skipped
+            stats.append(st.total)
+        grads = np_(eng.grads.flat).copy()
+        depth = np_(eng.out.depth if eng._last_view_set is None
+                    else eng._last_view_set.out.depth).copy()
+        res.append((stats, grads, depth))
+    (sa, ga, da), (sb, gb, db) = res
+    np.testing.assert_allclose(sa, sb, rtol=1e-6)
+    np.testing.assert_array_equal(da, db)
+    n = (ga.size - 16) // 16
+    bad, worst = grad_tolerance_ok(gb[:14 * n], ga[:14 * n], rel=1e-4, abs_frac=1e-6)
+    assert bad == 0, worst
+
+
 @pytest.mark.parametrize("name", ["survey2k", "opaque3k"])
 def test_tile_list_backward_matches_row_list_backward(name):
     """backward_render through the materialised tile lists (composite) == through the
