@@ -7,7 +7,7 @@ cp $lib /tmp/base.so
 for v in base build/variants/*.so; do
   name=$(basename $v .so)
   if [ "$v" = base ]; then cp /tmp/base.so $lib; else cp $v $lib; fi
-  python bench.py --steps $steps --warmup 5 --no-cpu-baseline --no-render-fps > gpurun_out/ab_$name.log 2>&1
+  timeout 300 python bench.py --steps $steps --warmup 5 --no-cpu-baseline --no-render-fps > gpurun_out/ab_$name.log 2>&1
   python - "$name" <<'PY'
 import json, sys
 d = json.loads(open(f"gpurun_out/ab_{sys.argv[1]}.log").read().strip().splitlines()[-1])
