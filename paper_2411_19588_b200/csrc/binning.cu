@@ -334,23 +334,6 @@ __device__ __forceinline__ SegRange seg_range(uint32_t b, const uint32_t* blk_st
     return r;
 }
 
-// an item's cells inside the band: local rows [r0, r0+nr), columns [x0, x0+nx)
-struct Cells {
-    int r0, nr, x0, nx;
-};
-
-__device__ __forceinline__ Cells band_cells(short4 rc, int band) {
-    Cells c;
-    const int lo = band * kBand;
-    const int y0 = max((int)rc.y, lo), y1 = min((int)rc.w, lo + kBand - 1);
-    c.r0 = y0 - lo;
-    c.nr = y1 - y0 + 1;
-    c.x0 = rc.x;
-    c.nx = rect_nx(rc);
-    if (c.nr <= 0 || c.nx <= 0) c.nr = c.nx = 0;
-    return c;
-}
-
 __device__ __forceinline__ void seg_load(const uint2* seg, const short4* rect, SegRange sr,
                                          int warp, int lane, uint32_t (&rw)[kSegChunks],
                                          Cells (&cl)[kSegChunks]) {

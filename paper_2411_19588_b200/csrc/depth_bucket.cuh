@@ -23,7 +23,10 @@
 namespace uws {
 namespace depth_bucket {
 
-constexpr int kLogBuckets = 20;
+#ifndef UWS_LOG_BUCKETS
+#define UWS_LOG_BUCKETS 20
+#endif
+constexpr int kLogBuckets = UWS_LOG_BUCKETS;  // measured at C3: 2^19 and 2^21 are slower
 constexpr uint32_t kBuckets = 1u << kLogBuckets;
 constexpr int kThreadRun = 8;
 constexpr int kCtaThreads = 256;
@@ -206,7 +209,7 @@ __global__ void __launch_bounds__(kCtaThreads) k_bucket_cta(const uint32_t* __re
     __shared__ uint32_t s_base[256];
     __shared__ uint32_t s_wc[W][257];
     __shared__ uint32_t s_tmp[W + 1];
-    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int tid = threadIdx.x, warp = tid >> 5;
     const uint32_t nlist = meta->n_cta;
     for (uint32_t w = blockIdx.x; w < nlist; w += gridDim.x) {
         const uint32_t b = list[w];
