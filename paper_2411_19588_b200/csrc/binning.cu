@@ -334,6 +334,11 @@ __device__ __forceinline__ SegRange seg_range(uint32_t b, const uint32_t* blk_st
     return r;
 }
 
+// an item's cells inside the band: local rows [r0, r0+nr), columns [x0, x0+nx)
+struct Cells {
+    int r0, nr, x0, nx;
+};
+
 __device__ __forceinline__ void seg_load(const uint2* seg, const short4* rect, SegRange sr,
                                          int warp, int lane, uint32_t (&rw)[kSegChunks],
                                          Cells (&cl)[kSegChunks]) {

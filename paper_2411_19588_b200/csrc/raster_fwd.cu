@@ -78,7 +78,7 @@ __device__ __forceinline__ bool t_ambiguous(float t) { return t >= kTBandLo && t
 // exceeds 0.24 of that band, no count mismatch outside it) and ~10x fewer re-walks,
 // but measured slower overall: the forward gains 47 us (spills, extra MUFU) for the
 // ~20 us the smaller fix-up saves.
-__device__ __forceinline__ bool t_ambiguous_eb(float t, float eb) {
+[[maybe_unused]] __device__ __forceinline__ bool t_ambiguous_eb(float t, float eb) {
     const float d = fmaf(5e-7f, eb, 2e-6f) * 1e-4f;
     return fabsf(t - 1e-4f) <= d;
 }
