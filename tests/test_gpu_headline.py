@@ -5,8 +5,9 @@
 * C3 (1M, 1920x1080, the headline config): backward on seeded tiles (dL/dC
   zero elsewhere, so the other tiles contribute exactly nothing), with the
   oracle's OWN projection and tile lists; forward on seeded tiles.
-* C5 (1M @ 3840x2160): forward on seeded tiles against the oracle's own
-  binning of those tiles.
+* C5 (1M and 5M @ 3840x2160): forward on seeded tiles against the oracle's own
+  binning of those tiles (5M through the two-set frame stream).
+* C4's per-view size (3M @ 1080p): every parameter gradient on seeded tiles.
 * StepEngine (the benchmarked path): one step with the gradients kept --
   its render, dL/dC and summed gradient buffer against the oracle, then its
   Adam update bit-exact against the reference's adam_step applied to the
@@ -192,6 +193,47 @@ def test_c5_1m_4k_forward_sampled_tiles():
     api = uw.render(cloud, cam, m, "underwater")
     for f in ("color", "depth", "count", "final_transmittance"):
         assert torch.equal(getattr(api, f), getattr(out, f)), f
+
+
+def test_c5_5m_4k_frame_stream_sampled_tiles():
+    """5M Gaussians @ 3840x2160 (the largest C5 point) through the two-set frame
+    stream (the last frame lands in the side set): seeded tiles against the oracle,
+    and the whole frame equal to the API render."""
+    hc = host_cloud(5_000_000, seed=4)
+    cam = survey_camera(3840, 2160)
+    med = survey_medium()
+    cloud, m = _device(hc, med)
+    eng = uw.StepEngine(uw.TrainState(cloud, m), cam.width, cam.height, uw.OptimConfig())
+    for _ in range(2):
+        eng.render_async(cam)
+    out = eng.render_flush()
+    assert eng._latest is not None           # the side buffer set
+    tiles = _sample_tiles(cam, 12, seed=17)
+    ref = O.render(hc, cam, med, "underwater", tiles=tiles)
+    _check_images(out, ref, _tile_mask(cam, tiles))
+    api = uw.render(cloud, cam, m, "underwater")
+    for f in ("color", "depth", "count", "final_transmittance", "last"):
+        assert torch.equal(getattr(api, f), getattr(out, f)), f
+
+
+def test_c4_3m_backward_sampled_tiles():
+    """3M Gaussians at 1080p (C4's per-view size): every parameter gradient with
+    dL/dC restricted to seeded tiles, against the oracle."""
+    hc = host_cloud(3_000_000, seed=6)
+    cam = survey_camera(1920, 1080)
+    med = survey_medium()
+    cloud, m = _device(hc, med)
+    out = uw.render(cloud, cam, m, "underwater")
+    tiles = _sample_tiles(cam, 12, seed=8)
+    mask = _tile_mask(cam, tiles)
+    rng = np.random.default_rng(10)
+    dL = np.where(mask[..., None], rng.normal(size=(cam.height, cam.width, 3)), 0.0) / mask.sum()
+    buf = uw.backward_render(out, torch.as_tensor(dL, dtype=torch.float32).cuda(), cloud, m, 0.1)
+    ref = O.render(hc, cam, med, "underwater", tiles=tiles)
+    _check_images(out, ref, mask)
+    g = O.backward(ref, dL.astype(np.float32).astype(np.float64), len(hc.positions), med, 0.1,
+                   tiles=tiles)
+    _check_grads(buf, g)
 
 
 # ----------------------------------------------------------------------------
