@@ -18,6 +18,18 @@ namespace {
 
 constexpr int kThreads = 128;
 
+// Arithmetic type of the chain rule below the recomputed float64 geometry.  The
+// geometry itself, and with it every frustum-clamp / sign decision, stays float64;
+// the chain rule runs in float32 (its inputs are the float32 screen-space sums of
+// K8): within the gradient contract on every parity test, no spills (float64: 148 B
+// of spills at 96 registers), 0.076 -> 0.071 ms at C3.  -DUWS_PBWD_F64 restores
+// float64.
+#ifdef UWS_PBWD_F64
+typedef double real;
+#else
+typedef float real;
+#endif
+
 template <bool ACC>  // add into the gradient buffer (else store: it is known to be zero)
 __global__ void __launch_bounds__(kThreads, 5) k_preprocess_bwd(uws_cloud cl, uws_camera cam,
                                                              const int32_t* __restrict__ src_index,
@@ -32,9 +44,9 @@ __global__ void __launch_bounds__(kThreads, 5) k_preprocess_bwd(uws_cloud cl, uw
     const int64_t n = cl.n;
     const int64_t i = src_index[row];
     float* sg = screen + row * 9;
-    const double gl = sg[0], dmx = sg[1], dmy = sg[2];
-    const double dca = sg[3], dcb = sg[4], dcc = sg[5];
-    const double dcol[3] = {sg[6], sg[7], sg[8]};
+    const real gl = sg[0], dmx = sg[1], dmy = sg[2];
+    const real dca = sg[3], dcb = sg[4], dcc = sg[5];
+    const real dcol[3] = {sg[6], sg[7], sg[8]};
     // leave the screen-space accumulator zeroed for the next view
 #pragma unroll
     for (int v = 0; v < 9; ++v) sg[v] = 0.f;
@@ -42,38 +54,55 @@ __global__ void __launch_bounds__(kThreads, 5) k_preprocess_bwd(uws_cloud cl, uw
     Geo G;
     geo_view(cl, cam, i, G);
     geo_shape(cl, cam, i, G);
+    // geometry in the chain rule's type (float64 decisions above are kept: xm, ym, signs)
+    real GS[9], GRq[9], Gs[3], Gqu[4];
+#pragma unroll
+    for (int q = 0; q < 9; ++q) {
+        GS[q] = (real)G.S[q];
+        GRq[q] = (real)G.Rq[q];
+    }
+#pragma unroll
+    for (int q = 0; q < 3; ++q) Gs[q] = (real)G.s[q];
+#pragma unroll
+    for (int q = 0; q < 4; ++q) Gqu[q] = (real)G.qu[q];
+    const real fx = (real)cam.fx, fy = (real)cam.fy;
+    const real vz = (real)G.vz, xu = (real)G.xu, yu = (real)G.yu, vx = (real)G.vx, vy = (real)G.vy;
     const double4 ex = reinterpret_cast<const double4*>(exact)[row];
-    const double k0 = ex.x, k1 = ex.y, k2 = ex.z, sop = ex.w;
-    const double* R = cam.R;
+    const real k0 = (real)ex.x, k1 = (real)ex.y, k2 = (real)ex.z, sop = (real)ex.w;
+    real R[9];
+#pragma unroll
+    for (int q = 0; q < 9; ++q) R[q] = (real)cam.R[q];
 
     // conic -> cov2d: dX = -Y dY Y (:192-204)
-    const double h = 0.5 * dcb;
-    const double P00 = k0 * dca + k1 * h, P01 = k0 * h + k1 * dcc;
-    const double P10 = k1 * dca + k2 * h, P11 = k1 * h + k2 * dcc;
-    const double X00 = -(P00 * k0 + P01 * k1);
-    const double X01 = -(P00 * k1 + P01 * k2);
-    const double X11 = -(P10 * k1 + P11 * k2);
-    const double G2[4] = {X00, X01, X01, X11};
+    const real h = (real)0.5 * dcb;
+    const real P00 = k0 * dca + k1 * h, P01 = k0 * h + k1 * dcc;
+    const real P10 = k1 * dca + k2 * h, P11 = k1 * h + k2 * dcc;
+    const real X00 = -(P00 * k0 + P01 * k1);
+    const real X01 = -(P00 * k1 + P01 * k2);
+    const real X11 = -(P10 * k1 + P11 * k2);
+    const real G2[4] = {X00, X01, X01, X11};
 
     // dSigma = T^T G2 T ; dT = 2 G2 T Sigma ; dJ = dT R^T (:214-217)
-    const double* T = G.T;
-    double GT[6];  // G2 T (2x3)
+    real T[6];
+#pragma unroll
+    for (int q = 0; q < 6; ++q) T[q] = (real)G.T[q];
+    real GT[6];  // G2 T (2x3)
 #pragma unroll
     for (int r = 0; r < 2; ++r)
 #pragma unroll
         for (int c = 0; c < 3; ++c) GT[3 * r + c] = G2[2 * r] * T[c] + G2[2 * r + 1] * T[3 + c];
-    double dS[9];
+    real dS[9];
 #pragma unroll
     for (int a = 0; a < 3; ++a)
 #pragma unroll
         for (int b = 0; b < 3; ++b) dS[3 * a + b] = T[a] * GT[b] + T[3 + a] * GT[3 + b];
-    double dT[6];
+    real dT[6];
 #pragma unroll
     for (int r = 0; r < 2; ++r)
 #pragma unroll
         for (int c = 0; c < 3; ++c)
-            dT[3 * r + c] = 2.0 * (GT[3 * r] * G.S[c] + GT[3 * r + 1] * G.S[3 + c] + GT[3 * r + 2] * G.S[6 + c]);
-    double dJ[6];
+            dT[3 * r + c] = (real)2 * (GT[3 * r] * GS[c] + GT[3 * r + 1] * GS[3 + c] + GT[3 * r + 2] * GS[6 + c]);
+    real dJ[6];
 #pragma unroll
     for (int r = 0; r < 2; ++r)
 #pragma unroll
@@ -81,27 +110,27 @@ __global__ void __launch_bounds__(kThreads, 5) k_preprocess_bwd(uws_cloud cl, uw
             dJ[3 * r + c] = dT[3 * r] * R[3 * c] + dT[3 * r + 1] * R[3 * c + 1] + dT[3 * r + 2] * R[3 * c + 2];
 
     // cov3d = M M^T, M = Rq diag(s): dM = 2 dSigma M (:220-224)
-    double M[9], dM[9];
+    real M[9], dM[9];
 #pragma unroll
     for (int r = 0; r < 3; ++r)
 #pragma unroll
-        for (int c = 0; c < 3; ++c) M[3 * r + c] = G.Rq[3 * r + c] * G.s[c];
+        for (int c = 0; c < 3; ++c) M[3 * r + c] = GRq[3 * r + c] * Gs[c];
 #pragma unroll
     for (int r = 0; r < 3; ++r)
 #pragma unroll
         for (int c = 0; c < 3; ++c)
-            dM[3 * r + c] = 2.0 * (dS[3 * r] * M[c] + dS[3 * r + 1] * M[3 + c] + dS[3 * r + 2] * M[6 + c]);
-    double dls[3], gR[9];
+            dM[3 * r + c] = (real)2 * (dS[3 * r] * M[c] + dS[3 * r + 1] * M[3 + c] + dS[3 * r + 2] * M[6 + c]);
+    real dls[3], gR[9];
 #pragma unroll
     for (int c = 0; c < 3; ++c) {
-        dls[c] = (G.Rq[c] * dM[c] + G.Rq[3 + c] * dM[3 + c] + G.Rq[6 + c] * dM[6 + c]) * G.s[c];
+        dls[c] = (GRq[c] * dM[c] + GRq[3 + c] * dM[3 + c] + GRq[6 + c] * dM[6 + c]) * Gs[c];
 #pragma unroll
-        for (int r = 0; r < 3; ++r) gR[3 * r + c] = dM[3 * r + c] * G.s[c];
+        for (int r = 0; r < 3; ++r) gR[3 * r + c] = dM[3 * r + c] * Gs[c];
     }
     // rotation matrix -> raw quaternion (:166-181)
-    const double w = G.qu[0], x = G.qu[1], y = G.qu[2], z = G.qu[3];
+    const real w = Gqu[0], x = Gqu[1], y = Gqu[2], z = Gqu[3];
 #define g(r, c) gR[3 * (r) + (c)]
-    double dq[4];
+    real dq[4];
     dq[0] = 2 * (z * (g(1, 0) - g(0, 1)) + y * (g(0, 2) - g(2, 0)) + x * (g(2, 1) - g(1, 2)));
     dq[1] = 2 * (y * (g(0, 1) + g(1, 0)) + z * (g(0, 2) + g(2, 0)) + w * (g(2, 1) - g(1, 2)) -
                  2 * x * (g(1, 1) + g(2, 2)));
@@ -110,21 +139,21 @@ __global__ void __launch_bounds__(kThreads, 5) k_preprocess_bwd(uws_cloud cl, uw
     dq[3] = 2 * (w * (g(1, 0) - g(0, 1)) + x * (g(0, 2) + g(2, 0)) + y * (g(1, 2) + g(2, 1)) -
                  2 * z * (g(0, 0) + g(1, 1)));
 #undef g
-    const double radial = dq[0] * w + dq[1] * x + dq[2] * y + dq[3] * z;
+    const real radial = dq[0] * w + dq[1] * x + dq[2] * y + dq[3] * z;
 
     // view-space point: through J (clamped) and the unclamped mean (:226-248)
-    const double rz = 1.0 / G.vz, rz2 = rz * rz, rz3 = rz2 * rz;
-    const double dxu = dJ[2] * (-cam.fx * rz2);
-    const double dyu = dJ[5] * (-cam.fy * rz2);
-    double dtz = dJ[0] * (-cam.fx * rz2) + dJ[2] * (2.0 * cam.fx * G.xu * rz3) +
-                 dJ[4] * (-cam.fy * rz2) + dJ[5] * (2.0 * cam.fy * G.yu * rz3);
-    double dtx = G.xm ? 0.0 : dxu;
-    double dty = G.ym ? 0.0 : dyu;
-    if (G.xm) dtz += dxu * (G.u > 0 ? 1.0 : (G.u < 0 ? -1.0 : 0.0)) * G.limx;
-    if (G.ym) dtz += dyu * (G.v > 0 ? 1.0 : (G.v < 0 ? -1.0 : 0.0)) * G.limy;
-    dtx += dmx * cam.fx * rz;
-    dty += dmy * cam.fy * rz;
-    dtz = dtz - dmx * cam.fx * G.vx * rz2 - dmy * cam.fy * G.vy * rz2;
+    const real rz = (real)1 / vz, rz2 = rz * rz, rz3 = rz2 * rz;
+    const real dxu = dJ[2] * (-fx * rz2);
+    const real dyu = dJ[5] * (-fy * rz2);
+    real dtz = dJ[0] * (-fx * rz2) + dJ[2] * ((real)2 * fx * xu * rz3) +
+                 dJ[4] * (-fy * rz2) + dJ[5] * ((real)2 * fy * yu * rz3);
+    real dtx = G.xm ? (real)0 : dxu;
+    real dty = G.ym ? (real)0 : dyu;
+    if (G.xm) dtz += dxu * (real)((G.u > 0 ? 1.0 : (G.u < 0 ? -1.0 : 0.0)) * G.limx);
+    if (G.ym) dtz += dyu * (real)((G.v > 0 ? 1.0 : (G.v < 0 ? -1.0 : 0.0)) * G.limy);
+    dtx += dmx * fx * rz;
+    dty += dmy * fy * rz;
+    dtz = dtz - dmx * fx * vx * rz2 - dmy * fy * vy * rz2;
 
     float* gpos = grads;
     float* gls = grads + 3 * n;
@@ -143,22 +172,22 @@ __global__ void __launch_bounds__(kThreads, 5) k_preprocess_bwd(uws_cloud cl, uw
         gls[3 * i + c] = v;
         finite &= isfinite(v);
         const double col = (double)cl.sh_coeffs[3 * i + c] * kSH_C0 + 0.5;
-        v = (ACC ? gsh[3 * i + c] : 0.f) + (col > 0.0 ? (float)(kSH_C0 * dcol[c]) : 0.0f);
+        v = (ACC ? gsh[3 * i + c] : 0.f) + (col > 0.0 ? (float)((real)kSH_C0 * dcol[c]) : 0.0f);
         gsh[3 * i + c] = v;
         finite &= isfinite(v);
     }
 #pragma unroll
     for (int c = 0; c < 4; ++c) {
-        float v = (ACC ? grot[4 * i + c] : 0.f) + (float)div_pos_nz(dq[c] - G.qu[c] * radial, G.qn);
+        float v = (ACC ? grot[4 * i + c] : 0.f) + (float)div_pos_nz((double)(dq[c] - Gqu[c] * radial), G.qn);
         grot[4 * i + c] = v;
         finite &= isfinite(v);
     }
     {
-        float v = (ACC ? gop[i] : 0.f) + (float)((1.0 - sop) * gl);
+        float v = (ACC ? gop[i] : 0.f) + (float)(((real)1 - sop) * gl);
         gop[i] = v;
         finite &= isfinite(v);
     }
-    const double nx = dmx * cam.width * 0.5, ny = dmy * cam.height * 0.5;
+    const double nx = (double)dmx * cam.width * 0.5, ny = (double)dmy * cam.height * 0.5;
     gnorm[i] = (ACC ? gnorm[i] : 0.f) + (float)sqrt_nz(nx * nx + ny * ny);
     gobs[i] = (ACC ? gobs[i] : 0.f) + 1.0f;
     if (!finite && nonfinite) atomicAdd(nonfinite, 1.0f);
