@@ -25,6 +25,9 @@
 namespace uws {
 namespace {
 
+#ifndef UWS_BWD_MINB
+#define UWS_BWD_MINB 12
+#endif
 constexpr int kBatch = 128;
 constexpr float kLn2 = 0.69314718055994531f;
 constexpr int kPix = 4;                          // pixels per thread
@@ -560,7 +563,7 @@ extern "C" int uws_raster_bwd(const uws_projected* proj, const int32_t* offsets,
     a.tile_rows = nullptr;
     a.tile_nrows = nullptr;
     a.tile_rows_cap = 0;
-    launch_serial(k_raster_bwd<false, 12>, dim3(a.gx * gy), dim3(kThreads), 0, as_stream(stream), a);
+    launch_serial(k_raster_bwd<false, UWS_BWD_MINB>, dim3(a.gx * gy), dim3(kThreads), 0, as_stream(stream), a);
     UWS_CHECK_LAUNCH("k_raster_bwd");
     return UWS_OK;
 }
@@ -597,7 +600,7 @@ extern "C" int uws_raster_bwd_rows(const uws_projected* proj, const int32_t* row
     a.dL = dL_dC;
     a.screen = screen_grads;
     a.medium_acc = medium_acc;
-    launch_serial(k_raster_bwd<true, 12>, dim3(a.gx * gy), dim3(kThreads), 0, as_stream(stream), a);
+    launch_serial(k_raster_bwd<true, UWS_BWD_MINB>, dim3(a.gx * gy), dim3(kThreads), 0, as_stream(stream), a);
     UWS_CHECK_LAUNCH("k_raster_bwd_rows");
     return UWS_OK;
 }
@@ -618,7 +621,7 @@ static int bwd_det(BwdArgs a, int gy, const int32_t* tile_base, int64_t r, int64
     a.part_row = p.part_row;
     a.none_row = (uint32_t)k;
     a.med_part = p.med_part;
-    launch_serial(k_raster_bwd<ROWS, 12, true>, dim3(tiles), dim3(kThreads), 0, st, a);
+    launch_serial(k_raster_bwd<ROWS, UWS_BWD_MINB, true>, dim3(tiles), dim3(kThreads), 0, st, a);
     UWS_CHECK_LAUNCH("k_raster_bwd_det");
     if (r > 0) {
         UWS_CUDA(radix::sort_pairs<uint32_t>(p.sort, p.part_row, nullptr, p.rows_sorted,
