@@ -280,6 +280,7 @@ class StepEngine:
             need_s = int(rec[_ST_TOTALS:_ST_TOTALS + 2].view(torch.int64)[1])
             self._set_capacity(int(need_s * 1.25) + 1024)
         self.out.mode = mode
+        self._latest = None      # the most recent frame is in the engine's own buffers
         return self.last_render()
 
     # -- one view: forward + loss + backward into self.grads -----------------------

@@ -406,6 +406,14 @@ def test_render_async_stream_matches_render(capacity):
     out = eng.render_flush()
     for k, v in want.items():
         np.testing.assert_array_equal(np_(getattr(out, k)), v)
+    # a synchronous render after an even stream: flush then returns that render
+    for c in (other, other):
+        eng.render_async(c)
+    eng.render_flush()
+    eng.render(cam)
+    out = eng.render_flush()
+    for k, v in want.items():
+        np.testing.assert_array_equal(np_(getattr(out, k)), v)
     gt = torch.as_tensor(g.gt, dtype=torch.float32).cuda()
     eng.render_async(other)
     st = eng.step([(cam, gt)])
