@@ -201,12 +201,14 @@ class StepEngine:
         k = self._async_frames % 2
         self._async_frames += 1
         cur = torch.cuda.current_stream()
+        if self._async_pending is None:
+            # a new frame stream: side-stream frames wait for everything queued before
+            # it (the parameters they read), not for the frames on the current stream
+            self._stream_start = torch.cuda.Event()
+            self._stream_start.record(cur)
         if k == 1:
             fs = self._frame_set()
-            if self._async_pending is None:
-                # first side-stream frame of a stream: after everything queued so far
-                # (the parameters it reads)
-                fs.stream.wait_stream(cur)
+            fs.stream.wait_event(self._stream_start)
             stream_ctx = torch.cuda.stream(fs.stream)
         else:
             fs = None
