@@ -41,3 +41,17 @@ def test_single_rank_default():
 def test_gpus_must_match_world_size():
     r = _run(["--gpus", "1", "--dry-run"], env={"WORLD_SIZE": "2"})
     assert r.returncode != 0 and "WORLD_SIZE" in r.stderr
+
+
+def test_reference_arm_json_line():
+    """`bench.py --impl reference` (the driver's reference arm): the unmodified
+    reference from baseline/_ref (or the oracle port) on a small tile sample prints
+    one JSON line with the reference-arm keys and the GPU arm's config dict."""
+    r = _run(["--impl", "reference", "--steps", "1", "--warmup", "0", "--cpu-tiles", "4"])
+    assert r.returncode == 0, r.stderr[-2000:]
+    d = _json_line(r.stdout)
+    assert d["impl"] == "reference" and d["n_gpus"] == 1 and d["value"] > 0
+    assert d["cpu_baseline"]["kind"] in ("reference", "port")
+    assert d["e2e"] == {"value": d["value"], "unit": d["unit"], "h2d_bytes_per_step": 0,
+                        "d2h_bytes_per_step": 0}
+    assert d["config"]["workload"].startswith("C3") and d["config"]["gaussians"] == 1_000_000
