@@ -68,6 +68,8 @@ class StepEngine:
     """Persistent-buffer, sync-free training step for one (cloud size, image size)."""
 
     OVERLAP_VIEWS = True   # default of ``overlap_views``
+    RENDER_SETS = 3        # frame-stream buffer sets / streams (the engine's own + side sets;
+                           # measured: 3 renders 1080p ~2 % faster than 2, 4K the same)
 
     def __init__(self, state: TrainState, width: int, height: int, cfg: OptimConfig,
                  spatial_scale: float = 1.0, max_views: int = 1, entry_capacity: int = 0,
@@ -99,9 +101,11 @@ class StepEngine:
         self._slots = [_Slot(max_views, dev) for _ in range(2)]
         self._render_stats = torch.zeros(_ST_SIZE + 2, dtype=torch.float64, device=dev)
         # render_async: two frame records, the pending (queued, unchecked) frame
-        self._async_stats = torch.zeros(2, _ST_SIZE + 2, dtype=torch.float64, device=dev)
-        self._async_flag = torch.zeros(2, 2, dtype=torch.int32).pin_memory()
-        self._async_done = [torch.cuda.Event(), torch.cuda.Event()]
+        nsets = self.RENDER_SETS
+        self._async_stats = torch.zeros(nsets, _ST_SIZE + 2, dtype=torch.float64, device=dev)
+        self._async_flag = torch.zeros(nsets, 2, dtype=torch.int32).pin_memory()
+        self._async_done = [torch.cuda.Event() for _ in range(nsets)]
+        self._more_sets = {}     # frame-stream buffer sets beyond the second (RENDER_SETS > 2)
         self._async_frames = 0
         self._async_pending = None
         self._fs = None          # the frame stream's second buffer set (lazy)
@@ -184,10 +188,10 @@ class StepEngine:
     def render_async(self, cam, mode: str = "underwater") -> RenderOutput:
         """Queue one render-only frame without waiting for it (a frame stream).
 
-        Consecutive frames alternate between two buffer sets and two streams (the
-        engine's own buffers on the current stream, a second set on a side
-        stream), so frame i+1's preprocess and depth order -- latency-bound
-        kernels that leave most SMs idle -- run while frame i composites.  The
+        Consecutive frames rotate over RENDER_SETS buffer sets and streams (the
+        engine's own buffers on the current stream, the others on side streams),
+        so frame i+1's preprocess and depth order -- latency-bound kernels that
+        leave most SMs idle -- run while frame i composites.  The
         row-list overflow flag of the PREVIOUS queued frame is read after this one
         is queued, so the host never idles the GPU between frames.  A frame's
         buffers hold its image only once ``render_flush()`` has returned
@@ -198,7 +202,7 @@ class StepEngine:
         cam = Camera.from_any(cam)
         if self._pending is None:
             self._sync_cloud()
-        k = self._async_frames % 2
+        k = self._async_frames % self.RENDER_SETS
         self._async_frames += 1
         cur = torch.cuda.current_stream()
         if self._async_pending is None:
@@ -206,8 +210,8 @@ class StepEngine:
             # it (the parameters they read), not for the frames on the current stream
             self._stream_start = torch.cuda.Event()
             self._stream_start.record(cur)
-        if k == 1:
-            fs = self._frame_set()
+        if k >= 1:
+            fs = self._frame_set() if k == 1 else self._extra_set(k)
             fs.stream.wait_event(self._stream_start)
             stream_ctx = torch.cuda.stream(fs.stream)
         else:
@@ -232,8 +236,9 @@ class StepEngine:
         """Wait for the queued frames; re-render the last one if its row lists overflowed.
         Returns the most recent frame."""
         frame, self._async_pending = self._async_pending, None
-        if self._fs is not None:
-            torch.cuda.current_stream().wait_stream(self._fs.stream)
+        for fs in [self._fs] + list(self._more_sets.values()):
+            if fs is not None:
+                torch.cuda.current_stream().wait_stream(fs.stream)
         if frame is not None and self._async_overflowed(frame[2]):
             self._latest = None
             return self.render(frame[0], frame[1])
@@ -253,6 +258,16 @@ class StepEngine:
         if train:
             self._fs.add_training(self)
         return self._fs
+
+    def _extra_set(self, k: int) -> "_FrameSet":
+        fs = self._more_sets.get(k)
+        if fs is None or fs.n != self.n or fs.s_cap != self.s_cap:
+            stream = fs.stream if fs is not None else torch.cuda.Stream(device=self.dev)
+            if fs is not None:
+                fs.stream.synchronize()
+            self._more_sets[k] = None
+            fs = self._more_sets[k] = _FrameSet(self, stream)
+        return fs
 
     def _frame_output(self, fs) -> RenderOutput:
         if fs is None:
