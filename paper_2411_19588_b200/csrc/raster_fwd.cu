@@ -34,6 +34,7 @@ __device__ unsigned char g_dbg_flag[3840 * 2160];  // the adaptive band would re
 // max rel err, max rel / adaptive band, #count mismatches the adaptive band misses,
 // #re-walked (the debug build re-walks the wide +-2e-3 band), #count mismatches
 __device__ unsigned g_dbg_max[5];
+__device__ unsigned long long g_dbg_ph2[2];   // pixels entering phase 2, phase-2 chunks scanned
 #endif
 
 struct FwdArgs {
@@ -466,7 +467,13 @@ __global__ void __launch_bounds__(256) k_raster_fix(FwdArgs a) {
         if (ROWS && !complete && !fw.done && fw.T >= kTStop) {
             int seen = 0;  // matches of this tile so far, in list order
             const int rend = a.row_start[ty + 1];
+#ifdef UWS_FIX_STATS
+            if (lane == 0) atomicAdd(&g_dbg_ph2[0], 1ull);
+#endif
             for (int c = a.row_start[ty]; c < rend && !fw.done; c += 32) {
+#ifdef UWS_FIX_STATS
+                if (lane == 0) atomicAdd(&g_dbg_ph2[1], 1ull);
+#endif
                 const int q = c + lane;
                 const uint2 it = q < rend ? __ldg(a.row_items + q) : make_uint2(0u, 0xffffu);
                 const bool m = (int)(it.y & 0xffffu) <= tx && tx <= (int)(it.y >> 16);
@@ -521,6 +528,12 @@ __global__ void __launch_bounds__(256) k_raster_fix(FwdArgs a) {
 using namespace uws;
 
 #ifdef UWS_FIX_STATS
+extern "C" int uws_debug_ph2_stats(unsigned long long* out2) {
+    cudaMemcpyFromSymbol(out2, g_dbg_ph2, sizeof(unsigned long long) * 2);
+    unsigned long long z[2] = {0, 0};
+    cudaMemcpyToSymbol(g_dbg_ph2, z, sizeof(z));
+    return 0;
+}
 extern "C" int uws_debug_fix_stats(unsigned* out5) {
     cudaMemcpyFromSymbol(out5, g_dbg_max, sizeof(unsigned) * 5);
     unsigned z[5] = {0, 0, 0, 0, 0};

@@ -30,5 +30,8 @@ for n, (w, h), op in cases:
         cam = uw.Camera.look_at(eye, (0, 0, 12), width=w, height=h, fx=1.2 * w, fy=1.2 * w)
         out = uw.render(cloud, cam, med, "underwater")
         torch.cuda.synchronize()
+        b = (ctypes.c_ulonglong * 2)()
+        lib.uws_debug_ph2_stats(b)
+        print("   phase-2 pixels", b[0], "chunks", b[1])
         print(n, w, h, op, k, "re-walked", int(out.fix_count[2]),
               "maxrel %.3e  max rel/band %.3f  missed-by-adaptive %d  n %d  cnt-mismatch %d" % stats())
