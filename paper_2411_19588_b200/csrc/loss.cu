@@ -103,7 +103,7 @@ __device__ __forceinline__ float block_sum_f(float v, float* sred) {
 
 // Pass 1.  Block = 32x32 valid windows (all channels); dynamic smem holds the
 // interleaved (a, b) patch [2][kP][kP*C + 1] and the horizontal moments
-// [5][kP][kT + 1] of the channel in flight.
+// [4][kP][kT + 1] of the channel in flight.
 template <int CT>  // compile-time channel count (0: runtime C)
 __global__ void __launch_bounds__(kThreads, 3) k_ssim_moments(const float* __restrict__ img_a,
                                                               const float* __restrict__ img_b,
@@ -116,7 +116,7 @@ __global__ void __launch_bounds__(kThreads, 3) k_ssim_moments(const float* __res
     const int pitch = kP * C + 1;
     float* sa = smem;
     float* sb = sa + kP * pitch;
-    float* hs = sb + kP * pitch;  // [5][kP][kT + 1]
+    float* hs = sb + kP * pitch;  // [4][kP][kT + 1]
     __shared__ float sred[kThreads / 32];
     const int x0 = blockIdx.x * kT, y0 = blockIdx.y * kT;  // valid-window origin == image pixel
     const int VW = W - 2 * kR, VH = H - 2 * kR;
@@ -163,21 +163,19 @@ __global__ void __launch_bounds__(kThreads, 3) k_ssim_moments(const float* __res
         // horizontal: item = (row, group of 8 columns)
         for (int it = threadIdx.x; it < kP * (kT / kHR); it += kThreads) {
             const int r = it >> 2, c0 = (it & 3) * kHR;
-            // (mu_a, mu_b) and (E[a^2], E[b^2]) accumulate in FFMA2 pairs
+            // (mu_a, mu_b) and (E[a^2] + E[b^2], E[ab]) accumulate in FFMA2 pairs: SSIM
+            // uses sigma_a^2 and sigma_b^2 only through their sum (B2) and its
+            // derivative coefficient is shared, so four moments suffice
             float2 m01[kHR], m23[kHR];
-            float m4[kHR];
 #pragma unroll
-            for (int j = 0; j < kHR; ++j) {
-                m01[j] = m23[j] = make_float2(0.f, 0.f);
-                m4[j] = 0.f;
-            }
+            for (int j = 0; j < kHR; ++j) m01[j] = m23[j] = make_float2(0.f, 0.f);
             const float* pa = sa + r * pitch + c0 * C + ch;
             const float* pb = sb + r * pitch + c0 * C + ch;
 #pragma unroll
             for (int q = 0; q < kHR + kN - 1; ++q) {
                 const float2 x01 = make_float2(pa[q * C], pb[q * C]);
-                const float2 x23 = mul2(x01, x01);
-                const float ab = x01.x * x01.y;
+                const float2 sq = mul2(x01, x01);
+                const float2 x23 = make_float2(sq.x + sq.y, x01.x * x01.y);
 #pragma unroll
                 for (int j = 0; j < kHR; ++j) {
                     const int t = q - j;
@@ -185,7 +183,6 @@ __global__ void __launch_bounds__(kThreads, 3) k_ssim_moments(const float* __res
                     const float2 w2 = c_taps2[t];
                     m01[j] = fma2(w2, x01, m01[j]);
                     m23[j] = fma2(w2, x23, m23[j]);
-                    m4[j] = fmaf(c_taps[t], ab, m4[j]);
                 }
             }
 #pragma unroll
@@ -194,7 +191,6 @@ __global__ void __launch_bounds__(kThreads, 3) k_ssim_moments(const float* __res
                 hs[(1 * kP + r) * (kT + 1) + c0 + j] = m01[j].y;
                 hs[(2 * kP + r) * (kT + 1) + c0 + j] = m23[j].x;
                 hs[(3 * kP + r) * (kT + 1) + c0 + j] = m23[j].y;
-                hs[(4 * kP + r) * (kT + 1) + c0 + j] = m4[j];
             }
         }
         __syncthreads();
@@ -202,18 +198,13 @@ __global__ void __launch_bounds__(kThreads, 3) k_ssim_moments(const float* __res
         {
             const int c = threadIdx.x & (kT - 1), r0 = (threadIdx.x >> 5) * kVR;
             float2 u01[kVR], u23[kVR];
-            float u4[kVR];
 #pragma unroll
-            for (int j = 0; j < kVR; ++j) {
-                u01[j] = u23[j] = make_float2(0.f, 0.f);
-                u4[j] = 0.f;
-            }
+            for (int j = 0; j < kVR; ++j) u01[j] = u23[j] = make_float2(0.f, 0.f);
 #pragma unroll
             for (int q = 0; q < kVR + kN - 1; ++q) {
                 const float* hq = hs + (r0 + q) * (kT + 1) + c;
                 const float2 h01 = make_float2(hq[0 * kP * (kT + 1)], hq[1 * kP * (kT + 1)]);
                 const float2 h23 = make_float2(hq[2 * kP * (kT + 1)], hq[3 * kP * (kT + 1)]);
-                const float h4 = hq[4 * kP * (kT + 1)];
 #pragma unroll
                 for (int j = 0; j < kVR; ++j) {
                     const int t = q - j;
@@ -221,7 +212,6 @@ __global__ void __launch_bounds__(kThreads, 3) k_ssim_moments(const float* __res
                     const float2 w2 = c_taps2[t];
                     u01[j] = fma2(w2, h01, u01[j]);
                     u23[j] = fma2(w2, h23, u23[j]);
-                    u4[j] = fmaf(c_taps[t], h4, u4[j]);
                 }
             }
             const int ox = x0 + c;
@@ -229,11 +219,12 @@ __global__ void __launch_bounds__(kThreads, 3) k_ssim_moments(const float* __res
             for (int j = 0; j < kVR; ++j) {
                 const int oy = y0 + r0 + j;
                 if (oy >= VH || ox >= VW) continue;
-                const float u1 = u01[j].x, u2 = u01[j].y, v1 = u23[j].x, v2 = u23[j].y, v12 = u4[j];
+                const float u1 = u01[j].x, u2 = u01[j].y, vs = u23[j].x, v12 = u23[j].y;
                 const float A1 = 2.0f * u1 * u2 + (float)kC1;
                 const float A2 = 2.0f * (v12 - u1 * u2) + (float)kC2;
-                const float B1 = u1 * u1 + u2 * u2 + (float)kC1;
-                const float B2 = (v1 - u1 * u1) + (v2 - u2 * u2) + (float)kC2;
+                const float uu = u1 * u1 + u2 * u2;
+                const float B1 = uu + (float)kC1;
+                const float B2 = (vs - uu) + (float)kC2;
                 // B1 >= C1 and B2 >= C2 (> 0): approximate reciprocals (rel. error ~2^-22)
                 const float r1 = rcp_approx(B1), r2 = rcp_approx(B2);
                 const float inv = r1 * r2;
@@ -504,10 +495,10 @@ extern "C" int uws_loss_fwd_bwd(const float* rendered, const float* gt, int32_t 
     cudaStream_t st = as_stream(stream);
     const int vh = h - 2 * kR, vw = w - 2 * kR;
     const double n_px = (double)h * w * c, n_win = (double)vh * vw * c;
-    const size_t smem1 = (size_t)(2 * kP * (kP * c + 1) + 5 * kP * (kT + 1)) * sizeof(float);
+    const size_t smem1 = (size_t)(2 * kP * (kP * c + 1) + 4 * kP * (kT + 1)) * sizeof(float);
     static bool attr_set = false;
     if (!attr_set) {
-        const int mx = (int)(2 * kP * (kP * kMaxC + 1) + 5 * kP * (kT + 1)) * (int)sizeof(float);
+        const int mx = (int)(2 * kP * (kP * kMaxC + 1) + 4 * kP * (kT + 1)) * (int)sizeof(float);
         UWS_CUDA(cudaFuncSetAttribute(k_ssim_moments<3>,
                                       cudaFuncAttributeMaxDynamicSharedMemorySize, mx));
         UWS_CUDA(cudaFuncSetAttribute(k_ssim_moments<0>,
