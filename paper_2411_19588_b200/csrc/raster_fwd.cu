@@ -152,7 +152,9 @@ __global__ void __launch_bounds__(kRasterThreads / PX, 4 * PX) k_raster_fwd(FwdA
     const int py = oy + ly;
 
     // pixel state; T = 0 marks a pixel outside the image as finished
-    float fx[PX], T[PX], cr[PX], cg[PX], cb[PX], dsum[PX], wsum[PX];
+    // (the blend weight sum is not accumulated: sum_i alpha_i T_i = 1 - T_final exactly,
+    // and 1 - T_final is the more accurate float32 value of it)
+    float fx[PX], T[PX], cr[PX], cg[PX], cb[PX], dsum[PX];
     float tb[PX];  // T before the last blend (fix-up band test)
 #if UWS_ADAPTIVE_BAND || defined(UWS_FIX_STATS)
     float eb[PX] = {};  // sum alpha / (1 - alpha) of the blends (float32 T error scale)
@@ -164,7 +166,7 @@ __global__ void __launch_bounds__(kRasterThreads / PX, 4 * PX) k_raster_fwd(FwdA
         fx[j] = (float)(lx0 + j) + 0.5f;
         inside[j] = ox + lx0 + j < a.width && py < a.height;
         T[j] = inside[j] ? 1.0f : 0.0f;
-        cr[j] = cg[j] = cb[j] = dsum[j] = wsum[j] = 0.f;
+        cr[j] = cg[j] = cb[j] = dsum[j] = 0.f;
         tb[j] = 1.0f;
         count[j] = last[j] = 0;
     }
@@ -284,7 +286,6 @@ __global__ void __launch_bounds__(kRasterThreads / PX, 4 * PX) k_raster_fwd(FwdA
                             cg[j] = fmaf(w, c.y, cg[j]);
                             cb[j] = fmaf(w, c.z, cb[j]);
                             dsum[j] = fmaf(w, p1.w, dsum[j]);
-                            wsum[j] += w;
                             tb[j] = T[j];
                             const float om = 1.0f - alpha;
 #if UWS_ADAPTIVE_BAND || defined(UWS_FIX_STATS)
@@ -329,9 +330,10 @@ __global__ void __launch_bounds__(kRasterThreads / PX, 4 * PX) k_raster_fwd(FwdA
     for (int j = 0; j < PX; ++j) {
         if (!inside[j]) continue;
         const int pix = py * a.width + ox + lx0 + j;
-        const float depth = count[j] > 0 ? dsum[j] / wsum[j] : a.far_plane;
+        const float wsum = 1.0f - T[j];
+        const float depth = count[j] > 0 ? dsum[j] / wsum : a.far_plane;
         const float c3[3] = {cr[j], cg[j], cb[j]};
-        store_pixel(a, pix, c3, depth, wsum[j], T[j], count[j], last[j]);
+        store_pixel(a, pix, c3, depth, wsum, T[j], count[j], last[j]);
 #ifdef UWS_FIX_STATS
         g_dbg_eb[pix] = eb[j];
         g_dbg_t32[pix] = T[j];
