@@ -190,23 +190,41 @@ __global__ void __launch_bounds__(kThreads) k_band_count(const uint32_t* __restr
     }
 }
 
-// 32 items (one per lane, lane order == list order) appended to the buckets
-// [lo, hi] they cover: bucket by bucket, the covering lanes write consecutive
-// slots from the bucket's cursor (coalesced runs, no per-item serial chain)
-__device__ __forceinline__ void warp_append_bands(int lo, int hi, uint2 val, int* cur, uint2* out,
-                                                  int lane) {
-    const int umin = __reduce_min_sync(0xffffffffu, lo);
-    const int umax = __reduce_max_sync(0xffffffffu, hi);
+// The warp's kRankChunks x 32 items (chunk-major, lane order == list order)
+// appended to the bands [lo, hi] they cover: band by band, the covering items
+// of all chunks write consecutive slots from the band's cursor (coalesced runs,
+// no per-item serial chain).  Each band is visited once per warp, so the
+// cursor is read once and never written back (the warp owns cur[] and consumes
+// it here).
+__device__ __forceinline__ void warp_append_bands(const int (&lo)[kRankChunks],
+                                                  const int (&hi)[kRankChunks],
+                                                  const uint2 (&val)[kRankChunks],
+                                                  const int* cur, uint2* out, int lane) {
+    int l = lo[0], h = hi[0];
+#pragma unroll
+    for (int i = 1; i < kRankChunks; ++i) {
+        l = min(l, lo[i]);
+        h = max(h, hi[i]);
+    }
+    const int umin = __reduce_min_sync(0xffffffffu, l);
+    const int umax = __reduce_max_sync(0xffffffffu, h);
     const unsigned lt = lanemask_lt();
     for (int b = umin; b <= umax; ++b) {
-        const bool in = lo <= b && b <= hi;
-        const unsigned m = __ballot_sync(0xffffffffu, in);
-        if (m == 0) continue;
-        const int base = cur[b];
-        if (in) out[base + __popc(m & lt)] = val;
-        __syncwarp();
-        if (lane == 0) cur[b] = base + __popc(m);
-        __syncwarp();
+        bool in[kRankChunks];
+        unsigned m[kRankChunks], any = 0u;
+#pragma unroll
+        for (int i = 0; i < kRankChunks; ++i) {
+            in[i] = lo[i] <= b && b <= hi[i];
+            m[i] = __ballot_sync(0xffffffffu, in[i]);
+            any |= m[i];
+        }
+        if (any == 0u) continue;
+        int base = cur[b];
+#pragma unroll
+        for (int i = 0; i < kRankChunks; ++i) {
+            if (in[i]) out[base + __popc(m[i] & lt)] = val[i];
+            base += __popc(m[i]);
+        }
     }
 }
 
@@ -246,14 +264,17 @@ __global__ void __launch_bounds__(kThreads) k_band_scatter(const uint32_t* __res
         }
     }
     __syncthreads();
+    int b0[kRankChunks], b1[kRankChunks];
+    uint2 val[kRankChunks];
 #pragma unroll
     for (int i = 0; i < kRankChunks; ++i) {
         const short4 rc = rcv[i];
         const bool ok = rect_ok(rc);
-        const int b0 = ok ? rc.y / kBand : (1 << 30);
-        const int b1 = ok ? rc.w / kBand : -1;
-        warp_append_bands(b0, b1, row_item(rowv[i], rc), diff[warp], seg, lane);
+        b0[i] = ok ? rc.y / kBand : (1 << 30);
+        b1[i] = ok ? rc.w / kBand : -1;
+        val[i] = row_item(rowv[i], rc);
     }
+    warp_append_bands(b0, b1, val, diff[warp], seg, lane);
 }
 
 // capacity check: E <= e_cap and S <= s_cap, else every later stage is a no-op

@@ -94,6 +94,12 @@ __device__ __forceinline__ float butterfly8(const float v[8], int lane) {
 
 constexpr int kMaxMarks = 64;   // recorded batch starts per tile (row-list source)
 
+#ifdef UWS_BWD_STATS
+// debug build: [0..32] (warp, entry) iterations by number of lanes with a pair,
+// [33] pairs, [34] iterations culled by the band test
+__device__ unsigned long long g_bwd_hist[35];
+#endif
+
 template <bool ROWS, int MINB, bool DET = false>
 __global__ void __launch_bounds__(kThreads, MINB) k_raster_bwd(BwdArgs a) {
     // launched serially (no pdl_entry): the per-CTA L1 invalidation costs more here
@@ -266,7 +272,12 @@ __global__ void __launch_bounds__(kThreads, MINB) k_raster_bwd(BwdArgs a) {
             const float4 D = lds128(ra + 48u);
             const float xlo = warp ? D.z : D.x, xhi = warp ? D.w : D.y;
             // the pass region misses this warp's band within the tile's columns (uniform)
-            if (xhi < 0.5f || xlo > (float)kTile - 0.5f) continue;
+            if (xhi < 0.5f || xlo > (float)kTile - 0.5f) {
+#ifdef UWS_BWD_STATS
+                if (lane == 0) atomicAdd(&g_bwd_hist[34], 1ull);
+#endif
+                continue;
+            }
             const int jrel = lo + k;
             // A thread's kPix pixels share one column, hence dx: the dx-weighted
             // partials are formed once after the pixel loop from sum(dp) and sum(dp dy).
@@ -283,6 +294,9 @@ __global__ void __launch_bounds__(kThreads, MINB) k_raster_bwd(BwdArgs a) {
                 // one pair's contribution: alpha = min(araw, 0.99), d power masked by the clamp
                 auto pair = [&](int p, float dy, float araw, bool unclamped) {
                     hit = true;
+#ifdef UWS_BWD_STATS
+                    atomicAdd(&g_bwd_hist[33], 1ull);
+#endif
                     const float alpha = fminf(araw, kClampF);
                     const float inv_om = rcp_ftz(1.0f - alpha);
                     const float Ti = T[p] * inv_om;
@@ -344,6 +358,12 @@ __global__ void __launch_bounds__(kThreads, MINB) k_raster_bwd(BwdArgs a) {
             }
             const float sdpx = sdp * dx;
             float v[9] = {sdp, sdpx, sdpy, sdpx * dx, sdpy * dx, sdpyy, wg0, wg1, wg2};
+#ifdef UWS_BWD_STATS
+            {
+                const unsigned hb = __ballot_sync(0xffffffffu, hit);
+                if (lane == 0) atomicAdd(&g_bwd_hist[__popc(hb)], 1ull);
+            }
+#endif
             if (!__any_sync(0xffffffffu, hit)) continue;
             const float r8 = butterfly8(v, lane);
             const float r9 = warp_sum(v[8]);
@@ -506,6 +526,15 @@ inline void det_plan(Workspace& ws, int tiles, int64_t r, int64_t k, DetPlan& p)
 }  // namespace uws
 
 using namespace uws;
+
+#ifdef UWS_BWD_STATS
+extern "C" int uws_debug_bwd_stats(unsigned long long* out35) {
+    cudaMemcpyFromSymbol(out35, g_bwd_hist, sizeof(unsigned long long) * 35);
+    unsigned long long z[35] = {};
+    cudaMemcpyToSymbol(g_bwd_hist, z, sizeof(z));
+    return 0;
+}
+#endif
 
 extern "C" int uws_raster_bwd_det_prefix(const uws_camera* cam, const uws_raster_out* fwd,
                                          int32_t* tile_count, int32_t* tile_base, void* stream) {
