@@ -321,15 +321,18 @@ __global__ void __launch_bounds__(kThreads, MINB) k_raster_bwd(BwdArgs a) {
                     for (int p = 0; p < kPix; ++p) {
                         const float dy = fy[p] - A.my;
                         const float power = dx * fmaf(A.B, dy, tA) + B.C * dy * dy;
+                        // the sure pass first: one test on the common path
+                        if (power >= B.hi) {
+                            pair(p, dy, B.op * ex2_ftz(power), true);
+                            continue;
+                        }
                         if (power < skipv) continue;
                         const float araw = B.op * ex2_ftz(power);
-                        if (power < B.hi) {
-                            if (araw < kFloorLo) continue;
-                            if (araw < kFloorHi &&
-                                !(alpha_raw_f64_cold(a.splat, a.exact, C.row, ox + lx,
-                                                     oy + ly0 + 2 * p) >= kFloor))
-                                continue;
-                        }
+                        if (araw < kFloorLo) continue;
+                        if (araw < kFloorHi &&
+                            !(alpha_raw_f64_cold(a.splat, a.exact, C.row, ox + lx,
+                                                 oy + ly0 + 2 * p) >= kFloor))
+                            continue;
                         pair(p, dy, araw, true);
                     }
                 } else {

@@ -271,30 +271,34 @@ __global__ void __launch_bounds__(kRasterThreads / PX, 4 * PX) k_raster_fwd(FwdA
                 for (int j = 0; j < PX; ++j) {
                     const float dx = fx[j] - p0.x;
                     const float power = dx * fmaf(p0.w, dy, p0.z * dx) + qy;
-                    if (power >= p1.z - kSkipDelta && T[j] >= kTStopF) {
-                        const float araw = p1.y * ex2_ftz(power);
-                        bool take = true;
-                        if (power < p1.z)  // near the 1/255 floor (rare): float64 in the guard band
-                            take = araw >= kFloorHi ||
-                                   (araw >= kFloorLo &&
-                                    alpha_raw_f64_cold(a.splat, a.exact, __float_as_int(c.w),
-                                                       ox + lx0 + j, py) >= kFloor);
-                        if (take) {
-                            const float alpha = fminf(araw, kClampF);
-                            const float w = alpha * T[j];
-                            cr[j] = fmaf(w, c.x, cr[j]);
-                            cg[j] = fmaf(w, c.y, cg[j]);
-                            cb[j] = fmaf(w, c.z, cb[j]);
-                            dsum[j] = fmaf(w, p1.w, dsum[j]);
-                            tb[j] = T[j];
-                            const float om = 1.0f - alpha;
+                    auto blend = [&](float araw) {
+                        const float alpha = fminf(araw, kClampF);
+                        const float w = alpha * T[j];
+                        cr[j] = fmaf(w, c.x, cr[j]);
+                        cg[j] = fmaf(w, c.y, cg[j]);
+                        cb[j] = fmaf(w, c.z, cb[j]);
+                        dsum[j] = fmaf(w, p1.w, dsum[j]);
+                        tb[j] = T[j];
+                        const float om = 1.0f - alpha;
 #if UWS_ADAPTIVE_BAND || defined(UWS_FIX_STATS)
-                            eb[j] = fmaf(alpha, rcp_ftz(om), eb[j]);
+                        eb[j] = fmaf(alpha, rcp_ftz(om), eb[j]);
 #endif
-                            T[j] = T[j] * om;
-                            ++count[j];
-                            last[j] = rel + idx[u];
-                        }
+                        T[j] = T[j] * om;
+                        ++count[j];
+                        last[j] = rel + idx[u];
+                    };
+                    // the sure pass first: one test on the common path
+                    const bool live = T[j] >= kTStopF;
+                    if (power >= p1.z && live) {
+                        blend(p1.y * ex2_ftz(power));
+                    } else if (power >= p1.z - kSkipDelta && live) {
+                        // near the 1/255 floor (rare): float64 in the guard band
+                        const float araw = p1.y * ex2_ftz(power);
+                        if (araw >= kFloorHi ||
+                            (araw >= kFloorLo &&
+                             alpha_raw_f64_cold(a.splat, a.exact, __float_as_int(c.w),
+                                                ox + lx0 + j, py) >= kFloor))
+                            blend(araw);
                     }
                 }
             }
