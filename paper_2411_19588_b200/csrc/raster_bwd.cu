@@ -290,7 +290,6 @@ __global__ void __launch_bounds__(kThreads, MINB) k_raster_bwd(BwdArgs a) {
                 const StageC C{c4.x, c4.y, c4.z, __float_as_int(c4.w)};
                 dx = fx - A.mx;
                 const float tA = A.A * dx;
-                const float skipv = B.hi - kSkipDelta;
                 // one pair's contribution: alpha = min(araw, 0.99), d power masked by the clamp
                 auto pair = [&](int p, float dy, float araw, bool unclamped) {
                     hit = true;
@@ -314,20 +313,20 @@ __global__ void __launch_bounds__(kThreads, MINB) k_raster_bwd(BwdArgs a) {
                     wg1 = fmaf(w, G[p][1], wg1);
                     wg2 = fmaf(w, G[p][2], wg2);
                 };
-                if (jrel < minl && B.op < kClampLo) {
+                if (jrel < minl && B.lop < kLopClampLo) {
                     // every pixel of the thread still consumes this entry and alpha_raw
                     // <= opacity stays below the clamp band: only the floor gate remains
 #pragma unroll
                     for (int p = 0; p < kPix; ++p) {
                         const float dy = fy[p] - A.my;
-                        const float power = dx * fmaf(A.B, dy, tA) + B.C * dy * dy;
+                        const float power = dx * fmaf(A.B, dy, tA) + fmaf(B.C * dy, dy, B.lop);
                         // the sure pass first: one test on the common path
-                        if (power >= B.hi) {
-                            pair(p, dy, B.op * ex2_ftz(power), true);
+                        if (power >= kPassLg2) {
+                            pair(p, dy, ex2_ftz(power), true);
                             continue;
                         }
-                        if (power < skipv) continue;
-                        const float araw = B.op * ex2_ftz(power);
+                        if (power < kSkipLg2) continue;
+                        const float araw = ex2_ftz(power);
                         if (araw < kFloorLo) continue;
                         if (araw < kFloorHi &&
                             !(alpha_raw_f64_cold(a.splat, a.exact, C.row, ox + lx,
@@ -340,11 +339,11 @@ __global__ void __launch_bounds__(kThreads, MINB) k_raster_bwd(BwdArgs a) {
                     for (int p = 0; p < kPix; ++p) {
                         if (jrel >= mylast[p]) continue;
                         const float dy = fy[p] - A.my;
-                        const float power = dx * fmaf(A.B, dy, tA) + B.C * dy * dy;
-                        if (power < skipv) continue;
-                        const float araw = B.op * ex2_ftz(power);
+                        const float power = dx * fmaf(A.B, dy, tA) + fmaf(B.C * dy, dy, B.lop);
+                        if (power < kSkipLg2) continue;
+                        const float araw = ex2_ftz(power);
                         bool unclamped = araw < kClampLo;
-                        if (power < B.hi || fabsf(araw - kClampMid) < kClampHalf) {
+                        if (power < kPassLg2 || fabsf(araw - kClampMid) < kClampHalf) {
                             // near a gate (rare): the full decision from alpha_raw, with
                             // both gates re-decided from the float64 record in the guard bands
                             if (araw < kFloorLo) continue;

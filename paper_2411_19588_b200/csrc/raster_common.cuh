@@ -7,10 +7,14 @@
 // re-decided from the float64 record exactly as the reference computes it.
 //
 // Staged record layout (per tile-list entry, shared memory): the conic is
-// pre-scaled by -0.5*log2(e) (and -log2(e) for the cross term) so that
-//     alpha_raw = opacity * 2^(dx*(A*dx + B*dy) + C*dy*dy)
-// costs 2 FADD + 5 FMUL/FFMA + 1 MUFU.EX2 per pair, and the mean is stored
-// relative to the tile origin (computed in float64 -> exact local offsets).
+// pre-scaled by -0.5*log2(e) (and -log2(e) for the cross term) and the opacity
+// is staged as its log2, so that
+//     alpha_raw = 2^(dx*(A*dx + B*dy) + (C*dy*dy + lg2(opacity)))
+// costs 2 FADD + 4 FMUL/FFMA + 1 MUFU.EX2 per pair (the C*dy*dy + lg2 term is
+// one FFMA shared by the pixels of a row), and the mean is stored relative to
+// the tile origin (computed in float64 -> exact local offsets).  Folding the
+// opacity into the exponent adds at most half an ulp of |power| <= 8 to the
+// exponent (3.3e-7 relative in alpha_raw), two orders below the guard band.
 #pragma once
 
 #include "common.cuh"
@@ -24,7 +28,9 @@ struct __align__(16) StageA {
     float mx, my, A, B;  // tile-local mean; -0.5*ca*log2e, -cb*log2e
 };
 struct __align__(16) StageB {
-    float C, op, hi, depth;  // -0.5*cc*log2e, opacity, log2-domain sure-pass threshold, depth
+    // -0.5*cc*log2e, lg2(opacity), sure-pass threshold of the power WITHOUT the
+    // opacity term (kPassLg2 - lop: used by the pass-region pre-filter), depth
+    float C, lop, hi, depth;
 };
 
 // power >= hi       : alpha_raw is certainly >= kFloorHi (passes the 1/255 floor)
@@ -34,6 +40,14 @@ struct __align__(16) StageB {
 // hi = lg2(kFloorHi/op) + 2e-3 and the old reject threshold lg2(kFloorLo/op) - 2e-3
 // differ by log2(kFloorHi/kFloorLo) + 4e-3 = 0.0040866; the constant rounds up.
 constexpr float kSkipDelta = 0.0041f;
+// The same thresholds on the folded exponent power + lg2(opacity):
+// lg2(kFloorHi) + 2e-3 = -7.99231 (rounded up), and below kSkipLg2 alpha_raw is
+// certainly < kFloorLo (lg2(kFloorLo) = -7.99440).
+constexpr float kPassLg2 = -7.9923f;
+constexpr float kSkipLg2 = kPassLg2 - kSkipDelta;
+// lg2(opacity) below this: alpha_raw <= opacity stays below the clamp guard
+// band (lg2(kClampLo) - 1e-3 = -0.015543, rounded down)
+constexpr float kLopClampLo = -0.0156f;
 struct __align__(16) StageC {
     float r, g, b;
     int row;
@@ -188,10 +202,10 @@ __device__ __forceinline__ void stage_entry(const uws_splat* __restrict__ splat,
     a.A = (-0.5f * kLog2e) * w1.x;
     a.B = (-kLog2e) * w1.y;
     b.C = (-0.5f * kLog2e) * w1.z;
-    b.op = w1.w;
-    // alpha_raw >= floor_hi  <=  power2 >= log2(floor_hi / op) + margin; the
+    b.lop = lg2_ftz(w1.w);
+    // alpha_raw >= floor_hi  <=  power + lop >= log2(floor_hi) + margin; the
     // margin (0.14% of alpha_raw) dwarfs the float32 lg2/ex2 error
-    b.hi = lg2_ftz(kFloorHi / w1.w) + 2e-3f;
+    b.hi = kPassLg2 - b.lop;
     b.depth = w2.w;
     c.r = w2.x;
     c.g = w2.y;

@@ -178,7 +178,7 @@ __global__ void __launch_bounds__(kRasterThreads / PX, 4 * PX) k_raster_fwd(FwdA
     };
     if (threadIdx.x == 0) {
         sRec[3 * kBatch + 0] = make_float4(0.f, 0.f, 0.f, 0.f);
-        sRec[3 * kBatch + 1] = make_float4(0.f, 0.f, __int_as_float(0x7f800000), 0.f);  // hi = +inf
+        sRec[3 * kBatch + 1] = make_float4(0.f, __int_as_float(0xff800000), __int_as_float(0x7f800000), 0.f);  // lg2(op) = -inf
         sRec[3 * kBatch + 2] = make_float4(0.f, 0.f, 0.f, 0.f);
     }
 
@@ -224,7 +224,7 @@ __global__ void __launch_bounds__(kRasterThreads / PX, 4 * PX) k_raster_fwd(FwdA
                 StageC sc;
                 stage_entry(a.splat, row, ox, oy, sa, sb, sc);
                 sRec[3 * i + 0] = make_float4(sa.mx, sa.my, sa.A, sa.B);
-                sRec[3 * i + 1] = make_float4(sb.C, sb.op, sb.hi, sb.depth);
+                sRec[3 * i + 1] = make_float4(sb.C, sb.lop, sb.hi, sb.depth);
                 sRec[3 * i + 2] = make_float4(sc.r, sc.g, sc.b, __int_as_float(sc.row));
                 // bands whose rows the pass region reaches within the tile's columns
                 PassRegion pr;
@@ -265,7 +265,7 @@ __global__ void __launch_bounds__(kRasterThreads / PX, 4 * PX) k_raster_fwd(FwdA
                 const float4 p0 = lds128(ra);
                 const float4 p1 = lds128(ra + 16u);
                 const float dy = fy - p0.y;
-                const float qy = p1.x * dy * dy;
+                const float qy = fmaf(p1.x * dy, dy, p1.y);  // + lg2(opacity)
                 const float4 c = lds128(ra + 32u);
 #pragma unroll
                 for (int j = 0; j < PX; ++j) {
@@ -289,11 +289,11 @@ __global__ void __launch_bounds__(kRasterThreads / PX, 4 * PX) k_raster_fwd(FwdA
                     };
                     // the sure pass first: one test on the common path
                     const bool live = T[j] >= kTStopF;
-                    if (power >= p1.z && live) {
-                        blend(p1.y * ex2_ftz(power));
-                    } else if (power >= p1.z - kSkipDelta && live) {
+                    if (power >= kPassLg2 && live) {
+                        blend(ex2_ftz(power));
+                    } else if (power >= kSkipLg2 && live) {
                         // near the 1/255 floor (rare): float64 in the guard band
-                        const float araw = p1.y * ex2_ftz(power);
+                        const float araw = ex2_ftz(power);
                         if (araw >= kFloorHi ||
                             (araw >= kFloorLo &&
                              alpha_raw_f64_cold(a.splat, a.exact, __float_as_int(c.w),
