@@ -163,38 +163,21 @@ __global__ void __launch_bounds__(kThreads, MINB) k_adam_cloud(float* __restrict
 
 // Vector form for even n (the rotation block [6n, 10n) is then 16-byte aligned
 // and every float4 group holds either one quaternion or four scalars of the
-// other fields): one thread per group, 16-byte loads of p, m, v and g; the
-// first n threads also fold the densify statistics of Gaussian t.
-__global__ void __launch_bounds__(kThreads, 4) k_adam_cloud4(float* __restrict__ P,
-                                                             float* __restrict__ M,
-                                                             float* __restrict__ V,
-                                                             float* __restrict__ Gr, int64_t n,
-                                                             uws_adam_params hp, AdamCtl ctl,
-                                                             int64_t g_begin, int64_t g_end) {
-    // launched serially (no pdl_entry): the per-CTA L1 invalidation costs more here
-    // groups [g_begin, g_end) of the 14n/4 (all of them for a whole step)
-    const int64_t t = g_begin + (int64_t)blockIdx.x * kThreads + threadIdx.x;
-    if (t >= g_end) return;
-    const bool skip = ctl.skip && (ctl.skip[0] > 0.0f || ctl.skip[1] > 0.0f);
-    if (t < n) {
-        if (!skip && ctl.grad_accum) {
-            ctl.grad_accum[t] += Gr[14 * n + t];
-            ctl.obs_count[t] += (int32_t)Gr[15 * n + t];
-        }
-        if (ctl.zero_grads) {
-            Gr[14 * n + t] = 0.f;
-            Gr[15 * n + t] = 0.f;
-        }
-    }
-    float4* const G4 = reinterpret_cast<float4*>(Gr) + t;
-    if (skip) {
-        if (ctl.zero_grads) *G4 = make_float4(0.f, 0.f, 0.f, 0.f);
-        return;
-    }
-    const float4 p4 = reinterpret_cast<const float4*>(P)[t];
-    const float4 m4 = reinterpret_cast<const float4*>(M)[t];
-    const float4 v4 = reinterpret_cast<const float4*>(V)[t];
-    const float4 g4 = *G4;
+// other fields): 16-byte loads of p, m, v and g; group t < n also folds the
+// densify statistics of Gaussian t.  Persistent grid (kAdamBlocksPerSM CTAs per
+// SM), software-pipelined: each thread issues the next group's four loads
+// before the float64 math of the current one, so HBM stays busy through the
+// FP64 phase.
+#ifndef UWS_ADAM_MINB
+#define UWS_ADAM_MINB 3
+#endif
+constexpr int kAdamBlocksPerSM = UWS_ADAM_MINB;
+
+__device__ __forceinline__ void adam_group(float* __restrict__ P, float* __restrict__ M,
+                                           float* __restrict__ V, float* __restrict__ Gr,
+                                           int64_t n, const uws_adam_params& hp,
+                                           const AdamCtl& ctl, int64_t t, float4 p4, float4 m4,
+                                           float4 v4, float4 g4) {
     float p[4] = {p4.x, p4.y, p4.z, p4.w}, m[4] = {m4.x, m4.y, m4.z, m4.w};
     float v[4] = {v4.x, v4.y, v4.z, v4.w};
     const float g[4] = {g4.x, g4.y, g4.z, g4.w};
@@ -222,7 +205,58 @@ __global__ void __launch_bounds__(kThreads, 4) k_adam_cloud4(float* __restrict__
     reinterpret_cast<float4*>(P)[t] = make_float4(p[0], p[1], p[2], p[3]);
     reinterpret_cast<float4*>(M)[t] = make_float4(m[0], m[1], m[2], m[3]);
     reinterpret_cast<float4*>(V)[t] = make_float4(v[0], v[1], v[2], v[3]);
-    if (ctl.zero_grads) *G4 = make_float4(0.f, 0.f, 0.f, 0.f);
+    if (ctl.zero_grads) reinterpret_cast<float4*>(Gr)[t] = make_float4(0.f, 0.f, 0.f, 0.f);
+}
+
+__global__ void __launch_bounds__(kThreads, kAdamBlocksPerSM) k_adam_cloud4(
+    float* __restrict__ P, float* __restrict__ M, float* __restrict__ V, float* __restrict__ Gr,
+    int64_t n, uws_adam_params hp, AdamCtl ctl, int64_t g_begin, int64_t g_end) {
+    // launched serially (no pdl_entry): the per-CTA L1 invalidation costs more here
+    // groups [g_begin, g_end) of the 14n/4 (all of them for a whole step)
+    const bool skip = ctl.skip && (ctl.skip[0] > 0.0f || ctl.skip[1] > 0.0f);
+    const int64_t stride = (int64_t)gridDim.x * kThreads;
+    int64_t t = g_begin + (int64_t)blockIdx.x * kThreads + threadIdx.x;
+    const float4* P4 = reinterpret_cast<const float4*>(P);
+    const float4* M4 = reinterpret_cast<const float4*>(M);
+    const float4* V4 = reinterpret_cast<const float4*>(V);
+    float4* G4 = reinterpret_cast<float4*>(Gr);
+    const float4 z4 = make_float4(0.f, 0.f, 0.f, 0.f);
+    float4 p4 = z4, m4 = z4, v4 = z4, g4 = z4;
+    if (t < g_end && !skip) {
+        p4 = P4[t]; m4 = M4[t]; v4 = V4[t]; g4 = G4[t];
+    }
+    for (; t < g_end; t += stride) {
+        const int64_t tn = t + stride;
+        float4 pn = z4, mn = z4, vn = z4, gn = z4;
+        if (tn < g_end && !skip) {  // next group's loads in flight during this group's math
+            pn = P4[tn]; mn = M4[tn]; vn = V4[tn]; gn = G4[tn];
+        }
+        if (t < n) {
+            if (!skip && ctl.grad_accum) {
+                ctl.grad_accum[t] += Gr[14 * n + t];
+                ctl.obs_count[t] += (int32_t)Gr[15 * n + t];
+            }
+            if (ctl.zero_grads) {
+                Gr[14 * n + t] = 0.f;
+                Gr[15 * n + t] = 0.f;
+            }
+        }
+        if (skip) {
+            if (ctl.zero_grads) G4[t] = z4;
+        } else {
+            adam_group(P, M, V, Gr, n, hp, ctl, t, p4, m4, v4, g4);
+        }
+        p4 = pn; m4 = mn; v4 = vn; g4 = gn;
+    }
+}
+
+inline unsigned adam_grid(int64_t groups) {
+    static int sms = 0;
+    if (sms == 0 && cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0) != cudaSuccess)
+        sms = 148;
+    const int64_t need = ceil_div(groups, kThreads);
+    const int64_t cap = (int64_t)sms * kAdamBlocksPerSM;
+    return (unsigned)(need < cap ? need : cap);
 }
 
 __global__ void k_adam_medium(float* __restrict__ P, float* __restrict__ M, float* __restrict__ V,
@@ -285,7 +319,7 @@ extern "C" int uws_adam_step(float* params, float* exp_avg, float* exp_avg_sq, f
                              ((uintptr_t)params | (uintptr_t)exp_avg | (uintptr_t)exp_avg_sq |
                               (uintptr_t)grads) % 16 == 0;
         if (aligned) {
-            launch_serial(k_adam_cloud4, dim3((unsigned)ceil_div(14 * n / 4, kThreads)),
+            launch_serial(k_adam_cloud4, dim3(adam_grid(14 * n / 4)),
                           dim3(kThreads), 0, st, params, exp_avg, exp_avg_sq, grads, n, *hp, ctl,
                           (int64_t)0, 14 * n / 4);
             UWS_CHECK_LAUNCH("k_adam_cloud4");
@@ -323,7 +357,7 @@ extern "C" int uws_adam_step_range(float* params, float* exp_avg, float* exp_avg
                 "uws_adam_step_range: group range out of bounds");
     if (group_end == group_begin) return UWS_OK;
     AdamCtl ctl{skip, grad_accum, obs_count, zero_grads};
-    launch_serial(k_adam_cloud4, dim3((unsigned)ceil_div(group_end - group_begin, kThreads)),
+    launch_serial(k_adam_cloud4, dim3(adam_grid(group_end - group_begin)),
                   dim3(kThreads), 0, as_stream(stream), params, exp_avg, exp_avg_sq, grads, n, *hp,
                   ctl, group_begin, group_end);
     UWS_CHECK_LAUNCH("k_adam_cloud4");
