@@ -25,7 +25,7 @@ namespace {
 #define UWS_PRE_IPT 2
 #endif
 #ifndef UWS_PRE_MINB
-#define UWS_PRE_MINB 8
+#define UWS_PRE_MINB 6
 #endif
 constexpr int kThreads = 128;
 constexpr int kIpt = UWS_PRE_IPT;
@@ -37,8 +37,9 @@ struct Proj {
     int16_t x0, y0, x1, y1;
 };
 
-__device__ __forceinline__ bool project_one(const uws_cloud& cl, const uws_camera& cam, int64_t i,
-                                            int gx, int gy, Proj& o) {
+__device__ __forceinline__ bool project_one(const uws_cloud& cl, const uws_camera& cam,
+                                            const FrustumLim& lim, int64_t i, int gx, int gy,
+                                            Proj& o) {
     Geo G;
     geo_view(cl, cam, i, G);                                                  // :112
     const double vz = G.vz;
@@ -46,7 +47,7 @@ __device__ __forceinline__ bool project_one(const uws_cloud& cl, const uws_camer
     double logit = cl.opacity_logits[i];
     double s = 1.0 / (1.0 + exp(-logit));                                      // expit, :116
     if (!(s >= kFloor)) return false;                                          // :117
-    geo_shape(cl, cam, i, G);                                                 // :126-153
+    geo_shape(cl, cam, i, lim, G);                                              // :126-153
     const double* T = G.T;
     const double* S = G.S;
     const double u = G.u, v = G.v;
@@ -80,7 +81,8 @@ __device__ __forceinline__ bool project_one(const uws_cloud& cl, const uws_camer
 
     o.mx = mx; o.my = my; o.depth = vz;
     o.a = a; o.b = b; o.c = c; o.radius = rad; o.s = s;
-    o.k0 = c / det; o.k1 = (-b) / det; o.k2 = a / det;                        // :174-175
+    const double rdet = __drcp_rn(det);                                       // :174-175
+    o.k0 = div_rcp(c, det, rdet); o.k1 = div_rcp(-b, det, rdet); o.k2 = div_rcp(a, det, rdet);
     // colour: max(f * C0 + 0.5, 0) (scene.py:136-139)
     o.r = (float)fmax((double)cl.sh_coeffs[3 * i + 0] * kSH_C0 + 0.5, 0.0);
     o.g = (float)fmax((double)cl.sh_coeffs[3 * i + 1] * kSH_C0 + 0.5, 0.0);
@@ -127,6 +129,7 @@ __device__ __forceinline__ void emit_row(uws_projected& out, unsigned long long 
 // kIpt consecutive Gaussians per thread (independent float64 chains the
 // scheduler can interleave); a block covers kThreads * kIpt Gaussians.
 __global__ void __launch_bounds__(kThreads, kMinBlocks) k_preprocess(uws_cloud cl, uws_camera cam,
+                                                                     FrustumLim lim,
                                                                      uws_projected out, int gx,
                                                                      int gy,
                                                                      unsigned long long* status,
@@ -144,7 +147,7 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) k_preprocess(uws_cloud c
     unsigned cnt = 0;
 #pragma unroll
     for (int q = 0; q < kIpt; ++q) {
-        vis[q] = i0 + q < cl.n && project_one(cl, cam, i0 + q, gx, gy, p[q]);
+        vis[q] = i0 + q < cl.n && project_one(cl, cam, lim, i0 + q, gx, gy, p[q]);
         cnt += vis[q];
     }
     unsigned long long total;
@@ -223,7 +226,7 @@ extern "C" int uws_preprocess_fwd(const uws_cloud* cloud, const uws_camera* cam,
     UWS_REQUIRE(ws.ok(), "uws_preprocess_fwd: workspace too small");
     UWS_CUDA(zero_async(status, (char*)(ticket + 1) - (char*)status, st));
     if (out->depth_range) UWS_CUDA(zero_async(out->depth_range, 2 * sizeof(uint32_t), st));
-    launch_serial(k_preprocess, dim3((unsigned)blocks), dim3(kThreads), 0, st, *cloud, *cam, *out, gx, gy, status, ticket);
+    launch_serial(k_preprocess, dim3((unsigned)blocks), dim3(kThreads), 0, st, *cloud, *cam, frustum_lim(*cam), *out, gx, gy, status, ticket);
     UWS_CHECK_LAUNCH("k_preprocess");
     return UWS_OK;
 }

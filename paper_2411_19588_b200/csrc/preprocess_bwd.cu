@@ -18,20 +18,21 @@ namespace {
 
 constexpr int kThreads = 128;
 
-// Arithmetic type of the chain rule below the recomputed float64 geometry.  The
-// geometry itself, and with it every frustum-clamp / sign decision, stays float64;
-// the chain rule runs in float32 (its inputs are the float32 screen-space sums of
-// K8): within the gradient contract on every parity test, no spills (float64: 148 B
-// of spills at 96 registers), 0.076 -> 0.071 ms at C3.  -DUWS_PBWD_F64 restores
-// float64.
-#ifdef UWS_PBWD_F64
-typedef double real;
-#else
+// Arithmetic type of the chain rule below the recomputed float64 geometry (float64,
+// as the reference).  With the projection's divisions by one divisor done as one
+// correctly rounded reciprocal + Markstein corrections (project_math.cuh) and every
+// record load issued up front, the float64 chain rule is the faster one at C3:
+// 0.064 ms vs 0.115 ms for a float32 chain rule (-DUWS_PBWD_F32), whose schedule
+// exposes the load latencies (ncu: long_scoreboard 21 cycles per issue).
+#ifdef UWS_PBWD_F32
 typedef float real;
+#else
+typedef double real;
 #endif
 
 template <bool ACC>  // add into the gradient buffer (else store: it is known to be zero)
 __global__ void __launch_bounds__(kThreads, 5) k_preprocess_bwd(uws_cloud cl, uws_camera cam,
+                                                             FrustumLim lim,
                                                              const int32_t* __restrict__ src_index,
                                                              const double* __restrict__ exact,
                                                              const int32_t* __restrict__ k_dev,
@@ -51,9 +52,13 @@ __global__ void __launch_bounds__(kThreads, 5) k_preprocess_bwd(uws_cloud cl, uw
 #pragma unroll
     for (int v = 0; v < 9; ++v) sg[v] = 0.f;
 
+    const double4 ex = reinterpret_cast<const double4*>(exact)[row];  // conic, opacity
+    float sh[3];  // issued with the record loads of geo_view
+#pragma unroll
+    for (int c = 0; c < 3; ++c) sh[c] = cl.sh_coeffs[3 * i + c];
     Geo G;
     geo_view(cl, cam, i, G);
-    geo_shape(cl, cam, i, G);
+    geo_shape(cl, cam, i, lim, G);
     // geometry in the chain rule's type (float64 decisions above are kept: xm, ym, signs)
     real GS[9], GRq[9], Gs[3], Gqu[4];
 #pragma unroll
@@ -67,7 +72,6 @@ __global__ void __launch_bounds__(kThreads, 5) k_preprocess_bwd(uws_cloud cl, uw
     for (int q = 0; q < 4; ++q) Gqu[q] = (real)G.qu[q];
     const real fx = (real)cam.fx, fy = (real)cam.fy;
     const real vz = (real)G.vz, xu = (real)G.xu, yu = (real)G.yu, vx = (real)G.vx, vy = (real)G.vy;
-    const double4 ex = reinterpret_cast<const double4*>(exact)[row];
     const real k0 = (real)ex.x, k1 = (real)ex.y, k2 = (real)ex.z, sop = (real)ex.w;
     real R[9];
 #pragma unroll
@@ -171,14 +175,14 @@ __global__ void __launch_bounds__(kThreads, 5) k_preprocess_bwd(uws_cloud cl, uw
         v = (ACC ? gls[3 * i + c] : 0.f) + (float)dls[c];
         gls[3 * i + c] = v;
         finite &= isfinite(v);
-        const double col = (double)cl.sh_coeffs[3 * i + c] * kSH_C0 + 0.5;
+        const double col = (double)sh[c] * kSH_C0 + 0.5;
         v = (ACC ? gsh[3 * i + c] : 0.f) + (col > 0.0 ? (float)((real)kSH_C0 * dcol[c]) : 0.0f);
         gsh[3 * i + c] = v;
         finite &= isfinite(v);
     }
 #pragma unroll
     for (int c = 0; c < 4; ++c) {
-        float v = (ACC ? grot[4 * i + c] : 0.f) + (float)div_pos_nz((double)(dq[c] - Gqu[c] * radial), G.qn);
+        float v = (ACC ? grot[4 * i + c] : 0.f) + (float)div_rcp((double)(dq[c] - Gqu[c] * radial), G.qn, G.rqn);
         grot[4 * i + c] = v;
         finite &= isfinite(v);
     }
@@ -230,11 +234,11 @@ extern "C" int uws_preprocess_bwd(const uws_cloud* cloud, const uws_camera* cam,
         UWS_REQUIRE(screen_grads != nullptr, "uws_preprocess_bwd: screen_grads missing");
         const unsigned nb = (unsigned)ceil_div(k_cap, kThreads);
         if (accumulate)
-            launch_serial(k_preprocess_bwd<true>, dim3(nb), dim3(kThreads), 0, st, *cloud, *cam, proj->source_index,
+            launch_serial(k_preprocess_bwd<true>, dim3(nb), dim3(kThreads), 0, st, *cloud, *cam, frustum_lim(*cam), proj->source_index,
                                                            proj->exact, proj->num_visible,
                                                            screen_grads, grads, nonfinite);
         else
-            launch_serial(k_preprocess_bwd<false>, dim3(nb), dim3(kThreads), 0, st, *cloud, *cam, proj->source_index,
+            launch_serial(k_preprocess_bwd<false>, dim3(nb), dim3(kThreads), 0, st, *cloud, *cam, frustum_lim(*cam), proj->source_index,
                                                             proj->exact, proj->num_visible,
                                                             screen_grads, grads, nonfinite);
         UWS_CHECK_LAUNCH("k_preprocess_bwd");
