@@ -27,7 +27,10 @@ namespace {
 #ifndef UWS_PRE_MINB
 #define UWS_PRE_MINB 6
 #endif
-constexpr int kThreads = 128;
+#ifndef UWS_PRE_THREADS
+#define UWS_PRE_THREADS 128
+#endif
+constexpr int kThreads = UWS_PRE_THREADS;
 constexpr int kIpt = UWS_PRE_IPT;
 constexpr int kMinBlocks = UWS_PRE_MINB;
 
