@@ -827,16 +827,22 @@ def run_reference(args):
     smp = CpuStepSampler(args.cpu_tiles, cores)
     for _ in range(args.warmup):
         smp.step()
-    times, det = [], {}
+    times, walls, det = [], [], {}
     for _ in range(args.steps):
+        t0 = time.perf_counter()
         full, det = smp.step()
+        walls.append(time.perf_counter() - t0)
         times.append(full)
     per_step = float(np.mean(times))
     value = W * H / per_step / 1e6      # one view per step on the host, whatever N is
     return {
         "impl": "reference", "metric": METRIC, "value": round(value, 6), "unit": "Mpixels/s",
         "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
-        "ms_per_step": round(per_step * 1e3, 1), "higher_is_better": True, "scaling": "weak",
+        # a step of this arm is the bounded sample (its wall time); value is the full C3
+        # step extrapolated from it (extrapolated_step_ms)
+        "ms_per_step": round(float(np.mean(walls)) * 1e3, 1),
+        "extrapolated_step_ms": round(per_step * 1e3, 1),
+        "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": "f64",
         "data": "synthetic (survey generator, random-init 1M Gaussians, U(0,1) ground truth)",
         "config": workload_config(world, "C3", N_GAUSS, world),
