@@ -15,7 +15,7 @@
 // The 9 per-(pixel, Gaussian) partials (dpower, dpower*dx, dpower*dy,
 // dpower*dx^2, dpower*dx*dy, dpower*dy^2, w*G) are first summed over the
 // thread's kPix pixels, then across the warp with a transposed butterfly
-// (14 shuffles instead of 45), accumulated over the CTA's warps in shared
+// (12 shuffles instead of 45), accumulated over the CTA's warps in shared
 // memory, chained through the conic once per (tile, Gaussian) and only then
 // sent to HBM with 9 atomics.
 #include "radix.cuh"
@@ -67,10 +67,14 @@ struct BwdArgs {
     double* med_part;          // [tiles][9]
 };
 
-// Reduce v[0..7] across the warp; returns the full sum of value index
-// ((lane>>4)&1)*4 + ((lane>>3)&1)*2 + ((lane>>2)&1) (valid in every lane).
-__device__ __forceinline__ float butterfly8(const float v[8], int lane) {
-    const bool b4 = lane & 16, b3 = lane & 8, b2 = lane & 4;
+// Reduce v[0..8] across the warp.  v[0..7] by a transposed butterfly (each stage
+// sends half of the values still held, so stages 16/8/4 cost 4+2+1 shuffles),
+// v[8] by plain stages 16/8/4, and the last two stages exchange (r, v8-partial)
+// transposed: 12 shuffles.  Lanes with (lane & 3) == 0 return the full sum of
+// value ((lane>>4)&1)*4 + ((lane>>3)&1)*2 + ((lane>>2)&1); lanes with
+// (lane & 3) == 2 the full sum of v[8].
+__device__ __forceinline__ float butterfly9(const float v[9], int lane) {
+    const bool b4 = lane & 16, b3 = lane & 8, b2 = lane & 4, b1 = lane & 2;
     float h[4];
 #pragma unroll
     for (int i = 0; i < 4; ++i) {
@@ -78,6 +82,7 @@ __device__ __forceinline__ float butterfly8(const float v[8], int lane) {
         float keep = b4 ? v[i + 4] : v[i];
         h[i] = keep + __shfl_xor_sync(0xffffffffu, send, 16);
     }
+    float e = v[8] + __shfl_xor_sync(0xffffffffu, v[8], 16);
     float q[2];
 #pragma unroll
     for (int i = 0; i < 2; ++i) {
@@ -85,11 +90,21 @@ __device__ __forceinline__ float butterfly8(const float v[8], int lane) {
         float keep = b3 ? h[i + 2] : h[i];
         q[i] = keep + __shfl_xor_sync(0xffffffffu, send, 8);
     }
+    e += __shfl_xor_sync(0xffffffffu, e, 8);
     float send = b2 ? q[0] : q[1];
     float r = (b2 ? q[1] : q[0]) + __shfl_xor_sync(0xffffffffu, send, 4);
-    r += __shfl_xor_sync(0xffffffffu, r, 2);
-    r += __shfl_xor_sync(0xffffffffu, r, 1);
-    return r;
+    e += __shfl_xor_sync(0xffffffffu, e, 4);
+    send = b1 ? r : e;
+    float x = (b1 ? e : r) + __shfl_xor_sync(0xffffffffu, send, 2);
+    x += __shfl_xor_sync(0xffffffffu, x, 1);
+    return x;
+}
+
+__device__ __forceinline__ void sts_f32(uint32_t addr, float v) {
+    asm volatile("st.shared.f32 [%0], %1;" ::"r"(addr), "f"(v) : "memory");
+}
+__device__ __forceinline__ void sts_u8(uint32_t addr, unsigned v) {
+    asm volatile("st.shared.u8 [%0], %1;" ::"r"(addr), "r"(v) : "memory");
 }
 
 constexpr int kMaxMarks = 64;   // recorded batch starts per tile (row-list source)
@@ -234,6 +249,14 @@ __global__ void __launch_bounds__(kThreads, MINB) k_raster_bwd(BwdArgs a) {
         __syncthreads();
     }
 
+    // per-lane shared-memory store slot of the reduced partials: lanes with
+    // (lane & 3) == 0 hold butterfly value idx, lane 2 the ninth value; lane 0 the hit flag
+    const int accRow = (lane & 3) == 0
+                           ? ((lane >> 4) & 1) * 4 + ((lane >> 3) & 1) * 2 + ((lane >> 2) & 1)
+                           : 8;
+    const bool accStore = (lane & 3) == 0 || lane == 2;
+    const uint32_t accBase = (uint32_t)__cvta_generic_to_shared(&sAcc[warp][accRow][0]);
+    const uint32_t hitBase = (uint32_t)__cvta_generic_to_shared(&sHit[warp][0]);
     for (int bi = nbatch - 1; bi >= 0; --bi) {
         const int lo = bi * kBatch;
         const int nb = min(kBatch, maxlast - lo);
@@ -291,12 +314,13 @@ __global__ void __launch_bounds__(kThreads, MINB) k_raster_bwd(BwdArgs a) {
                 dx = fx - A.mx;
                 const float tA = A.A * dx;
                 // one pair's contribution: alpha = min(araw, 0.99), d power masked by the clamp
-                auto pair = [&](int p, float dy, float araw, bool unclamped) {
+                auto pair = [&](int p, float dy, float araw, bool unclamped, bool clampfree) {
                     hit = true;
 #ifdef UWS_BWD_STATS
                     atomicAdd(&g_bwd_hist[33], 1ull);
 #endif
-                    const float alpha = fminf(araw, kClampF);
+                    // clampfree: alpha_raw <= opacity < the clamp band (the fast path)
+                    const float alpha = clampfree ? araw : fminf(araw, kClampF);
                     const float inv_om = rcp_ftz(1.0f - alpha);
                     const float Ti = T[p] * inv_om;
                     const float w = alpha * Ti;
@@ -322,7 +346,7 @@ __global__ void __launch_bounds__(kThreads, MINB) k_raster_bwd(BwdArgs a) {
                         const float power = dx * fmaf(A.B, dy, tA) + fmaf(B.C * dy, dy, B.lop);
                         // the sure pass first: one test on the common path
                         if (power >= kPassLg2) {
-                            pair(p, dy, ex2_ftz(power), true);
+                            pair(p, dy, ex2_ftz(power), true, true);
                             continue;
                         }
                         if (power < kSkipLg2) continue;
@@ -332,7 +356,7 @@ __global__ void __launch_bounds__(kThreads, MINB) k_raster_bwd(BwdArgs a) {
                             !(alpha_raw_f64_cold(a.splat, a.exact, C.row, ox + lx,
                                                  oy + ly0 + 2 * p) >= kFloor))
                             continue;
-                        pair(p, dy, araw, true);
+                        pair(p, dy, araw, true, true);
                     }
                 } else {
 #pragma unroll
@@ -354,7 +378,7 @@ __global__ void __launch_bounds__(kThreads, MINB) k_raster_bwd(BwdArgs a) {
                                 unclamped = e < kClamp;
                             }
                         }
-                        pair(p, dy, araw, unclamped);
+                        pair(p, dy, araw, unclamped, false);
                     }
                 }
             }
@@ -367,16 +391,9 @@ __global__ void __launch_bounds__(kThreads, MINB) k_raster_bwd(BwdArgs a) {
             }
 #endif
             if (!__any_sync(0xffffffffu, hit)) continue;
-            const float r8 = butterfly8(v, lane);
-            const float r9 = warp_sum(v[8]);
-            if ((lane & 3) == 0) {
-                const int idx = ((lane >> 4) & 1) * 4 + ((lane >> 3) & 1) * 2 + ((lane >> 2) & 1);
-                sAcc[warp][idx][k] = r8;
-            }
-            if (lane == 0) {
-                sAcc[warp][8][k] = r9;
-                sHit[warp][k] = 1;
-            }
+            const float r = butterfly9(v, lane);
+            if (accStore) sts_f32(accBase + 4u * (uint32_t)k, r);
+            if (lane == 0) sts_u8(hitBase + (uint32_t)k, 1u);
         }
         __syncthreads();
         for (int k = threadIdx.x; k < nb; k += kThreads) {
