@@ -257,6 +257,7 @@ __global__ void __launch_bounds__(kThreads, MINB) k_raster_bwd(BwdArgs a) {
     const bool accStore = (lane & 3) == 0 || lane == 2;
     const uint32_t accBase = (uint32_t)__cvta_generic_to_shared(&sAcc[warp][accRow][0]);
     const uint32_t hitBase = (uint32_t)__cvta_generic_to_shared(&sHit[warp][0]);
+    const uint32_t dOff = 48u + 8u * (uint32_t)warp;  // this warp's x-range in Rec::D
     for (int bi = nbatch - 1; bi >= 0; --bi) {
         const int lo = bi * kBatch;
         const int nb = min(kBatch, maxlast - lo);
@@ -292,8 +293,8 @@ __global__ void __launch_bounds__(kThreads, MINB) k_raster_bwd(BwdArgs a) {
         // back to front over the entries this warp's pixels consumed
         for (int k = min(nb, wmax - lo) - 1; k >= 0; --k) {
             const uint32_t ra = sbase + 64u * (uint32_t)k;
-            const float4 D = lds128(ra + 48u);
-            const float xlo = warp ? D.z : D.x, xhi = warp ? D.w : D.y;
+            float xlo, xhi;
+            asm volatile("ld.shared.v2.f32 {%0, %1}, [%2];" : "=f"(xlo), "=f"(xhi) : "r"(ra + dOff) : "memory");
             // the pass region misses this warp's band within the tile's columns (uniform)
             if (xhi < 0.5f || xlo > (float)kTile - 0.5f) {
 #ifdef UWS_BWD_STATS
@@ -307,6 +308,7 @@ __global__ void __launch_bounds__(kThreads, MINB) k_raster_bwd(BwdArgs a) {
             float sdp = 0.f, sdpy = 0.f, sdpyy = 0.f, wg0 = 0.f, wg1 = 0.f, wg2 = 0.f, dx = 0.f;
             bool hit = false;
             if (fx >= xlo && fx <= xhi) {  // column inside the band's range
+                hit = true;  // (a lane whose column reaches the pass region; its partials may be 0)
                 const float4 a4 = lds128(ra), b4 = lds128(ra + 16u), c4 = lds128(ra + 32u);
                 const StageA A{a4.x, a4.y, a4.z, a4.w};
                 const StageB B{b4.x, b4.y, b4.z, b4.w};
@@ -315,7 +317,6 @@ __global__ void __launch_bounds__(kThreads, MINB) k_raster_bwd(BwdArgs a) {
                 const float tA = A.A * dx;
                 // one pair's contribution: alpha = min(araw, 0.99), d power masked by the clamp
                 auto pair = [&](int p, float dy, float araw, bool unclamped, bool clampfree) {
-                    hit = true;
 #ifdef UWS_BWD_STATS
                     atomicAdd(&g_bwd_hist[33], 1ull);
 #endif
@@ -329,10 +330,12 @@ __global__ void __launch_bounds__(kThreads, MINB) k_raster_bwd(BwdArgs a) {
                     S[p] = fmaf(w, U, S[p]);
                     T[p] = Ti;
                     const float dp = unclamped ? dalpha * araw : 0.f;
-                    const float dpy = dp * dy;
+                    // moments about the first pixel's row: dy = dy0 + 2p
                     sdp += dp;
-                    sdpy += dpy;
-                    sdpyy = fmaf(dpy, dy, sdpyy);
+                    if (p > 0) {
+                        sdpy = fmaf(2.0f * p, dp, sdpy);         // sum 2p dp
+                        sdpyy = fmaf(4.0f * p * p, dp, sdpyy);   // sum 4p^2 dp
+                    }
                     wg0 = fmaf(w, G[p][0], wg0);
                     wg1 = fmaf(w, G[p][1], wg1);
                     wg2 = fmaf(w, G[p][2], wg2);
@@ -380,6 +383,12 @@ __global__ void __launch_bounds__(kThreads, MINB) k_raster_bwd(BwdArgs a) {
                         }
                         pair(p, dy, araw, unclamped, false);
                     }
+                }
+                {
+                    const float dy0 = fy[0] - A.my;
+                    const float y1 = fmaf(dy0, sdp, sdpy);        // sum dp dy
+                    sdpyy = fmaf(dy0, y1 + sdpy, sdpyy);          // sum dp dy^2
+                    sdpy = y1;
                 }
             }
             const float sdpx = sdp * dx;
