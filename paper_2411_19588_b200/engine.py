@@ -583,6 +583,9 @@ class _FrameSet:
         self.row_items = torch.empty_like(eng.row_items)
         self.out = _alloc_output(eng.height, eng.width, dev, "underwater", False)
         self.dL = None
+        # the zero fills above are queued on the current stream: the set's stream
+        # must not run a frame on these buffers before them
+        self.stream.wait_stream(torch.cuda.current_stream())
 
     def add_training(self, eng: StepEngine):
         if self.dL is None:
@@ -590,6 +593,7 @@ class _FrameSet:
             self.loss_ws = torch.empty_like(eng.loss_ws)
             self.screen = torch.zeros_like(eng.screen)
             self.med_acc = torch.zeros_like(eng.med_acc)
+            self.stream.wait_stream(torch.cuda.current_stream())
 
 
 class _Slot:
