@@ -307,6 +307,9 @@ __global__ void __launch_bounds__(kThreads, MINB) k_raster_bwd(BwdArgs a) {
             // partials are formed once after the pixel loop from sum(dp) and sum(dp dy).
             float sdp = 0.f, sdpy = 0.f, sdpyy = 0.f, wg0 = 0.f, wg1 = 0.f, wg2 = 0.f, dx = 0.f;
             bool hit = false;
+#ifdef UWS_BWD_STATS
+            bool paired = false;
+#endif
             if (fx >= xlo && fx <= xhi) {  // column inside the band's range
                 hit = true;  // (a lane whose column reaches the pass region; its partials may be 0)
                 const float4 a4 = lds128(ra), b4 = lds128(ra + 16u), c4 = lds128(ra + 32u);
@@ -319,6 +322,7 @@ __global__ void __launch_bounds__(kThreads, MINB) k_raster_bwd(BwdArgs a) {
                 auto pair = [&](int p, float dy, float araw, bool unclamped, bool clampfree) {
 #ifdef UWS_BWD_STATS
                     atomicAdd(&g_bwd_hist[33], 1ull);
+                    paired = true;
 #endif
                     // clampfree: alpha_raw <= opacity < the clamp band (the fast path)
                     const float alpha = clampfree ? araw : fminf(araw, kClampF);
@@ -395,7 +399,7 @@ __global__ void __launch_bounds__(kThreads, MINB) k_raster_bwd(BwdArgs a) {
             float v[9] = {sdp, sdpx, sdpy, sdpx * dx, sdpy * dx, sdpyy, wg0, wg1, wg2};
 #ifdef UWS_BWD_STATS
             {
-                const unsigned hb = __ballot_sync(0xffffffffu, hit);
+                const unsigned hb = __ballot_sync(0xffffffffu, paired);
                 if (lane == 0) atomicAdd(&g_bwd_hist[__popc(hb)], 1ull);
             }
 #endif
