@@ -158,7 +158,7 @@ __global__ void __launch_bounds__(kRasterThreads / PX, UWS_FWD_MINB(PX)) k_raste
     // (the blend weight sum is not accumulated: sum_i alpha_i T_i = 1 - T_final exactly,
     // and 1 - T_final is the more accurate float32 value of it)
     float fx[PX], T[PX], cr[PX], cg[PX], cb[PX], dsum[PX];
-    float tb[PX];  // T before the last blend (fix-up band test)
+    float oml[PX];  // 1 - alpha of the last blend: T before it = T / oml (fix-up band test)
 #if UWS_ADAPTIVE_BAND || defined(UWS_FIX_STATS)
     float eb[PX] = {};  // sum alpha / (1 - alpha) of the blends (float32 T error scale)
 #endif
@@ -170,7 +170,7 @@ __global__ void __launch_bounds__(kRasterThreads / PX, UWS_FWD_MINB(PX)) k_raste
         inside[j] = ox + lx0 + j < a.width && py < a.height;
         T[j] = inside[j] ? 1.0f : 0.0f;
         cr[j] = cg[j] = cb[j] = dsum[j] = 0.f;
-        tb[j] = 1.0f;
+        oml[j] = 1.0f;
         count[j] = last[j] = 0;
     }
     auto alive = [&]() {
@@ -284,8 +284,8 @@ __global__ void __launch_bounds__(kRasterThreads / PX, UWS_FWD_MINB(PX)) k_raste
                         cg[j] = fmaf(w, c.y, cg[j]);
                         cb[j] = fmaf(w, c.z, cb[j]);
                         dsum[j] = fmaf(w, p1.w, dsum[j]);
-                        tb[j] = T[j];
                         const float om = 1.0f - alpha;
+                        oml[j] = om;
 #if UWS_ADAPTIVE_BAND || defined(UWS_FIX_STATS)
                         eb[j] = fmaf(alpha, rcp_ftz(om), eb[j]);
 #endif
@@ -340,6 +340,7 @@ __global__ void __launch_bounds__(kRasterThreads / PX, UWS_FWD_MINB(PX)) k_raste
     for (int j = 0; j < PX; ++j) {
         if (!inside[j]) continue;
         const int pix = py * a.width + ox + lx0 + j;
+        const float tbj = T[j] / oml[j];  // within ~1 ulp of the float32 T before the last blend
         const float wsum = 1.0f - T[j];
         const float depth = count[j] > 0 ? dsum[j] / wsum : a.far_plane;
         const float c3[3] = {cr[j], cg[j], cb[j]};
@@ -350,12 +351,12 @@ __global__ void __launch_bounds__(kRasterThreads / PX, UWS_FWD_MINB(PX)) k_raste
         g_dbg_cnt32[pix] = count[j];
 #endif
 #if defined(UWS_FIX_STATS)
-        g_dbg_flag[pix] = t_ambiguous_eb(T[j], eb[j]) || t_ambiguous_eb(tb[j], eb[j]);
-        const bool amb = fabsf(T[j] - 1e-4f) <= 2e-7f || fabsf(tb[j] - 1e-4f) <= 2e-7f;
+        g_dbg_flag[pix] = t_ambiguous_eb(T[j], eb[j]) || t_ambiguous_eb(tbj, eb[j]);
+        const bool amb = fabsf(T[j] - 1e-4f) <= 2e-7f || fabsf(tbj - 1e-4f) <= 2e-7f;
 #elif UWS_ADAPTIVE_BAND
-        const bool amb = t_ambiguous_eb(T[j], eb[j]) || t_ambiguous_eb(tb[j], eb[j]);
+        const bool amb = t_ambiguous_eb(T[j], eb[j]) || t_ambiguous_eb(tbj, eb[j]);
 #else
-        const bool amb = t_ambiguous(T[j]) || t_ambiguous(tb[j]);
+        const bool amb = t_ambiguous(T[j]) || t_ambiguous(tbj);
 #endif
         if (a.out.fix_pixels && amb) {
             const int slot = atomicAdd(a.out.fix_count, 1);
