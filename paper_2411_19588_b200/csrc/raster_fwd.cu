@@ -127,7 +127,7 @@ __device__ __forceinline__ unsigned band_mask(float ylo, float yhi) {
 
 // PX horizontally adjacent pixels per thread (1 or 2); a warp owns a band of
 // 32*PX/16 rows.  The PX pixels of a thread share the record loads, dy and the
-// C*dy*dy and B*dy terms; each pixel's power is A*dx^2 + B*dx*dy + C*dy^2 + lg2(op) as in K8.
+// C*dy*dy term; each pixel's power is the same float expression as in K8.
 #ifndef UWS_FWD_MINB  // CTAs per SM (6 and 7 measured slower than 8 at PX = 2)
 #define UWS_FWD_MINB(PX) (4 * (PX))
 #endif
@@ -269,14 +269,14 @@ __global__ void __launch_bounds__(kRasterThreads / PX, UWS_FWD_MINB(PX)) k_raste
                 const float4 p1 = lds128(ra + 16u);
                 const float dy = fy - p0.y;
                 const float qy = fmaf(p1.x * dy, dy, p1.y);  // + lg2(opacity)
-                const float bdy = p0.w * dy;  // B*dy, shared by the thread's pixels
                 const float4 c = lds128(ra + 32u);
 #pragma unroll
                 for (int j = 0; j < PX; ++j) {
                     const float dx = fx[j] - p0.x;
-                    // (K8 rounds the inner sum as B*dy + RN(A*dx): the two differ by ulps
-                    // of the exponent, far inside the gates' guard bands)
-                    const float power = fmaf(dx, fmaf(p0.z, dx, bdy), qy);
+                    // bitwise K8's expression: the forward and backward gate decisions agree
+                    // even where float32 cancellation makes both differ from float64
+                    // (thin, long ellipses far from their centre)
+                    const float power = dx * fmaf(p0.w, dy, p0.z * dx) + qy;
                     auto blend = [&](float araw) {
                         const float alpha = fminf(araw, kClampF);
                         const float w = alpha * T[j];
