@@ -255,8 +255,10 @@ __global__ void __launch_bounds__(kThreads, MINB) k_raster_bwd(BwdArgs a) {
                            ? ((lane >> 4) & 1) * 4 + ((lane >> 3) & 1) * 2 + ((lane >> 2) & 1)
                            : 8;
     const bool accStore = (lane & 3) == 0 || lane == 2;
-    const uint32_t accBase = (uint32_t)__cvta_generic_to_shared(&sAcc[warp][accRow][0]);
-    const uint32_t hitBase = (uint32_t)__cvta_generic_to_shared(&sHit[warp][0]);
+    // opaque (kept in registers, not rematerialised from the CTA's shared window per use)
+    uint32_t accBase, hitBase;
+    asm volatile("mov.u32 %0, %1;" : "=r"(accBase) : "r"((uint32_t)__cvta_generic_to_shared(&sAcc[warp][accRow][0])));
+    asm volatile("mov.u32 %0, %1;" : "=r"(hitBase) : "r"((uint32_t)__cvta_generic_to_shared(&sHit[warp][0])));
     const uint32_t dOff = 48u + 8u * (uint32_t)warp;  // this warp's x-range in Rec::D
     for (int bi = nbatch - 1; bi >= 0; --bi) {
         const int lo = bi * kBatch;
@@ -291,10 +293,15 @@ __global__ void __launch_bounds__(kThreads, MINB) k_raster_bwd(BwdArgs a) {
         }
         __syncthreads();
         // back to front over the entries this warp's pixels consumed
-        for (int k = min(nb, wmax - lo) - 1; k >= 0; --k) {
-            const uint32_t ra = sbase + 64u * (uint32_t)k;
+        // one induction variable (this warp's x-range address of entry k); k itself is
+        // recovered opaquely (asm) on the non-culled path only, so the compiler keeps no
+        // strength-reduced copies of the k-linear addresses alive across the loop
+        uint32_t rbeg;
+        asm volatile("mov.u32 %0, %1;" : "=r"(rbeg) : "r"(sbase + dOff));
+        for (uint32_t rd = rbeg + 64u * (uint32_t)max(min(nb, wmax - lo), 0); rd != rbeg;) {
+            rd -= 64u;
             float xlo, xhi;
-            asm volatile("ld.shared.v2.f32 {%0, %1}, [%2];" : "=f"(xlo), "=f"(xhi) : "r"(ra + dOff) : "memory");
+            asm volatile("ld.shared.v2.f32 {%0, %1}, [%2];" : "=f"(xlo), "=f"(xhi) : "r"(rd) : "memory");
             // the pass region misses this warp's band within the tile's columns (uniform)
             if (xhi < 0.5f || xlo > (float)kTile - 0.5f) {
 #ifdef UWS_BWD_STATS
@@ -302,6 +309,10 @@ __global__ void __launch_bounds__(kThreads, MINB) k_raster_bwd(BwdArgs a) {
 #endif
                 continue;
             }
+            int k;
+            asm("{\n\t.reg .u32 t;\n\tsub.u32 t, %1, %2;\n\tshr.u32 %0, t, 6;\n\t}"
+                : "=r"(k) : "r"(rd), "r"(rbeg));
+            const uint32_t ra = rd - dOff;
             const int jrel = lo + k;
             // A thread's kPix pixels share one column, hence dx: the dx-weighted
             // partials are formed once after the pixel loop from sum(dp) and sum(dp dy).
