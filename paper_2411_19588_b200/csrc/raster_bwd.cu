@@ -107,6 +107,15 @@ __device__ __forceinline__ void sts_u8(uint32_t addr, unsigned v) {
     asm volatile("st.shared.u8 [%0], %1;" ::"r"(addr), "r"(v) : "memory");
 }
 
+// The float64 records for the guard-band re-decisions, read by the out-of-line
+// re-decision from shared memory: the hot loop then passes no pointers to the call
+// (passing them made the compiler reload four kernel-parameter words per entry).
+__shared__ const uws_splat* s_bwd_splat;
+__shared__ const double* s_bwd_exact;
+static __device__ __noinline__ double alpha_raw_f64_bwd(int row, int px, int py) {
+    return alpha_raw_f64(s_bwd_splat, s_bwd_exact, row, px, py);
+}
+
 constexpr int kMaxMarks = 64;   // recorded batch starts per tile (row-list source)
 
 #ifdef UWS_BWD_STATS
@@ -145,7 +154,11 @@ __global__ void __launch_bounds__(kThreads, MINB) k_raster_bwd(BwdArgs a) {
     const float fx = (float)lx + 0.5f;
     const int start = ROWS ? 0 : a.offsets[tile];
 
-    if (threadIdx.x == 0) sMaxLast = 0;
+    if (threadIdx.x == 0) {
+        sMaxLast = 0;
+        s_bwd_splat = a.splat;
+        s_bwd_exact = a.exact;
+    }
     for (int i = threadIdx.x; i < kWarps * kBatch; i += kThreads) (&sHit[0][0])[i] = 0;
 
     float G[kPix][3], T[kPix], S[kPix], fy[kPix];
@@ -371,7 +384,7 @@ __global__ void __launch_bounds__(kThreads, MINB) k_raster_bwd(BwdArgs a) {
                         const float araw = ex2_ftz(power);
                         if (araw < kFloorLo) continue;
                         if (araw < kFloorHi &&
-                            !(alpha_raw_f64_cold(a.splat, a.exact, C.row, ox + lx,
+                            !(alpha_raw_f64_bwd(C.row, ox + lx,
                                                  oy + ly0 + 2 * p) >= kFloor))
                             continue;
                         pair(p, dy, araw, true, true);
@@ -390,7 +403,7 @@ __global__ void __launch_bounds__(kThreads, MINB) k_raster_bwd(BwdArgs a) {
                             // both gates re-decided from the float64 record in the guard bands
                             if (araw < kFloorLo) continue;
                             if (araw < kFloorHi || fabsf(araw - kClampMid) < kClampHalf) {
-                                const double e = alpha_raw_f64_cold(a.splat, a.exact, C.row,
+                                const double e = alpha_raw_f64_bwd(C.row,
                                                                     ox + lx, oy + ly0 + 2 * p);
                                 if (!(e >= kFloor)) continue;
                                 unclamped = e < kClamp;
