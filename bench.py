@@ -261,7 +261,9 @@ class StageTimer:
         timer = self
 
         def call(name, *args):
-            if not timer.enabled or name.endswith("_size"):
+            # (the compositing schedule runs on a side stream, overlapping the loss:
+            # not a stage of the critical path)
+            if not timer.enabled or name.endswith("_size") or name == "uws_tile_order":
                 return orig(name, *args)
             s = timer.torch.cuda.Event(enable_timing=True)
             e = timer.torch.cuda.Event(enable_timing=True)

@@ -108,6 +108,11 @@ typedef struct uws_raster_out {
      * number of pixels re-walked.  NULL to skip. */
     int32_t* fix_pixels;
     int32_t* fix_count;
+    /* optional [tiles] permutation of the tiles: CTA b of the forward and of the
+     * backward composites tile tile_order[b].  A schedule only (tiles are
+     * independent): heaviest tiles first shortens the kernels' tails.  NULL =
+     * raster order.  uws_tile_order computes it from a forward's tile_nrows. */
+    const int32_t* tile_order;
 } uws_raster_out;
 
 /* Adam hyper-parameters for one apply_gradients call (optim.py:69-120).
@@ -180,6 +185,12 @@ int uws_bin_rows(const uws_projected* proj, int64_t k_cap, int64_t s_cap, const 
  *      backscatter[3]; NULL selects clean mode. ---------------------------- */
 int uws_raster_fwd(const uws_projected* proj, const int32_t* offsets, const int32_t* entries,
                    const uws_camera* cam, const float* medium, uws_raster_out* out, void* stream);
+/* Schedule for the next compositing launches over the same view and buffers:
+ * the tiles by descending consumed-prefix length (tile_nrows of a forward,
+ * low 30 bits / 4, capped at 255), written to order [n_tiles].  One CTA, async on
+ * stream.  (No reference counterpart: the reference composites tiles in a
+ * worker pool, rasterizer.py:186-241.) */
+int uws_tile_order(const int32_t* tile_nrows, int32_t n_tiles, int32_t* order, void* stream);
 int uws_raster_fwd_rows(const uws_projected* proj, const int32_t* row_start,
                         const void* row_items, const uws_camera* cam, const float* medium,
                         uws_raster_out* out, void* stream);

@@ -43,7 +43,7 @@ class RasterOutC(ctypes.Structure):
                 ("weight", c_void_p), ("final_T", c_void_p), ("count", c_void_p),
                 ("last", c_void_p), ("attenuation", c_void_p), ("backscatter", c_void_p),
                 ("tile_rows", c_void_p), ("tile_nrows", c_void_p), ("tile_rows_cap", c_int32),
-                ("fix_pixels", c_void_p), ("fix_count", c_void_p)]
+                ("fix_pixels", c_void_p), ("fix_count", c_void_p), ("tile_order", c_void_p)]
 
 
 class AdamParamsC(ctypes.Structure):
@@ -77,6 +77,7 @@ _SIGS = {
                              c_void_p]),
     "uws_raster_fwd": (c_int, [POINTER(ProjectedC), c_void_p, c_void_p, POINTER(CameraC),
                                c_void_p, POINTER(RasterOutC), c_void_p]),
+    "uws_tile_order": (c_int, [c_void_p, c_int32, c_void_p, c_void_p]),
     "uws_raster_fwd_rows": (c_int, [POINTER(ProjectedC), c_void_p, c_void_p, POINTER(CameraC),
                                     c_void_p, POINTER(RasterOutC), c_void_p]),
     "uws_loss_workspace_size": (c_int, [c_int32, c_int32, c_int32, POINTER(c_size_t)]),

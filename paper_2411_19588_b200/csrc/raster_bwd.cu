@@ -49,6 +49,7 @@ struct BwdArgs {
     const int32_t* tile_rows;    // the forward's staged rows per tile (optional)
     const int32_t* tile_nrows;
     int tile_rows_cap;
+    const int32_t* order;        // CTA b handles tile order[b] (NULL: raster order)
     int width, height, gx;
     const float* medium;
     const float* color_clean;
@@ -145,7 +146,7 @@ __global__ void __launch_bounds__(kThreads, MINB) k_raster_bwd(BwdArgs a) {
     __shared__ float sMed[kWarps][9];
     __shared__ int sMaxLast;
 
-    const int tile = blockIdx.x;
+    const int tile = a.order ? __ldg(a.order + blockIdx.x) : (int)blockIdx.x;
     const int ty = tile / a.gx, tx = tile - ty * a.gx;
     const int ox = tx * kTile, oy = ty * kTile;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -648,6 +649,7 @@ extern "C" int uws_raster_bwd(const uws_projected* proj, const int32_t* offsets,
     a.tile_rows = nullptr;
     a.tile_nrows = nullptr;
     a.tile_rows_cap = 0;
+    a.order = fwd->tile_order;
     launch_serial(k_raster_bwd<false, UWS_BWD_MINB>, dim3(a.gx * gy), dim3(kThreads), 0, as_stream(stream), a);
     UWS_CHECK_LAUNCH("k_raster_bwd");
     return UWS_OK;
@@ -673,6 +675,7 @@ extern "C" int uws_raster_bwd_rows(const uws_projected* proj, const int32_t* row
     a.tile_rows = fwd->tile_rows;
     a.tile_nrows = fwd->tile_nrows;
     a.tile_rows_cap = fwd->tile_rows_cap;
+    a.order = fwd->tile_order;
     a.width = cam->width;
     a.height = cam->height;
     a.gx = (int)ceil_div(cam->width, kTile);
@@ -753,6 +756,7 @@ extern "C" int uws_raster_bwd_det(const uws_projected* proj, const int32_t* offs
         a.tile_nrows = fwd->tile_nrows;
         a.tile_rows_cap = fwd->tile_rows_cap;
     }
+    a.order = fwd->tile_order;
     a.width = cam->width;
     a.height = cam->height;
     a.gx = (int)ceil_div(cam->width, kTile);

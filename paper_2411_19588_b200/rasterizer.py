@@ -164,6 +164,8 @@ class RenderOutput:
     # and its {count, ticket} pair (zero between calls)
     fix_pixels: Optional[torch.Tensor] = None
     fix_count: Optional[torch.Tensor] = None
+    # compositing schedule (heaviest tiles first), kept by the engine's buffer sets
+    tile_order: Optional[torch.Tensor] = None
 
     def c_struct(self) -> _lib.RasterOutC:
         cap = self.tile_rows.shape[1] if self.tile_rows is not None else 0
@@ -173,7 +175,7 @@ class RenderOutput:
                                _lib.ptr(self.last), _lib.ptr(self.attenuation_map),
                                _lib.ptr(self.backscatter_map), _lib.ptr(self.tile_rows),
                                _lib.ptr(self.tile_nrows), cap, _lib.ptr(self.fix_pixels),
-                               _lib.ptr(self.fix_count))
+                               _lib.ptr(self.fix_count), _lib.ptr(self.tile_order))
 
 
 # staged rows kept per tile for the backward (the consumed prefix is ~140 rows on

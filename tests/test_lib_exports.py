@@ -61,7 +61,7 @@ def test_struct_layouts_match_header():
     assert ctypes.sizeof(_lib.CloudC) == 6 * 8
     assert ctypes.sizeof(_lib.ProjectedC) == 9 * 8
     # 11 pointers, int32 cap + padding, 2 fix-up pointers
-    assert ctypes.sizeof(_lib.RasterOutC) == 11 * 8 + 8 + 2 * 8
+    assert ctypes.sizeof(_lib.RasterOutC) == 11 * 8 + 8 + 3 * 8   # + fix_pixels, fix_count, tile_order
     assert ctypes.sizeof(_lib.AdamParamsC) == 45 * 8
 
 
