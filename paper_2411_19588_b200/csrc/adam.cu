@@ -32,6 +32,15 @@ __device__ __forceinline__ double div_by_const(double a, double b, double r) {
     return __fma_rn(e, r, q0);
 }
 
+// RN(a / b) from rb = RN(1 / b) (Markstein, as div_by_const); signed zeros kept
+// (the FMA residual of a = -0 would give +0)
+__device__ __forceinline__ double div_shared(double a, double b, double rb) {
+    const double q0 = __dmul_rn(a, rb);
+    const double e = __fma_rn(-b, q0, a);
+    const double q = __fma_rn(e, rb, q0);
+    return a == 0.0 ? a : q;
+}
+
 __device__ __forceinline__ void adam1(float& p, float& m, float& v, float g, const AdamK& k,
                                       const uws_adam_params& hp) {
     const double gd = (double)g;
@@ -155,10 +164,11 @@ __global__ void __launch_bounds__(kThreads, MINB) k_adam_cloud(float* __restrict
                                               __dmul_rn(c, c)),
                                      __dmul_rn(d, d)));
     nr = fmax(nr, 1e-12);
-    P[o + 0] = (float)__ddiv_rn(a, nr);
-    P[o + 1] = (float)__ddiv_rn(b, nr);
-    P[o + 2] = (float)__ddiv_rn(c, nr);
-    P[o + 3] = (float)__ddiv_rn(d, nr);
+    const double rn = __drcp_rn(nr);  // four quotients by one divisor: RN(x / nr) each
+    P[o + 0] = (float)div_shared(a, nr, rn);
+    P[o + 1] = (float)div_shared(b, nr, rn);
+    P[o + 2] = (float)div_shared(c, nr, rn);
+    P[o + 3] = (float)div_shared(d, nr, rn);
 }
 
 // Vector form for even n (the rotation block [6n, 10n) is then 16-byte aligned
@@ -197,10 +207,11 @@ __device__ __forceinline__ void adam_group(float* __restrict__ P, float* __restr
                                                   __dmul_rn(c, c)),
                                          __dmul_rn(d, d)));
         nr = fmax(nr, 1e-12);
-        p[0] = (float)__ddiv_rn(a, nr);
-        p[1] = (float)__ddiv_rn(b, nr);
-        p[2] = (float)__ddiv_rn(c, nr);
-        p[3] = (float)__ddiv_rn(d, nr);
+        const double rn = __drcp_rn(nr);  // four quotients by one divisor: RN(x / nr) each
+        p[0] = (float)div_shared(a, nr, rn);
+        p[1] = (float)div_shared(b, nr, rn);
+        p[2] = (float)div_shared(c, nr, rn);
+        p[3] = (float)div_shared(d, nr, rn);
     }
     reinterpret_cast<float4*>(P)[t] = make_float4(p[0], p[1], p[2], p[3]);
     reinterpret_cast<float4*>(M)[t] = make_float4(m[0], m[1], m[2], m[3]);
