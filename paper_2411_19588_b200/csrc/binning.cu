@@ -71,11 +71,21 @@ __global__ void __launch_bounds__(kThreads) k_scan_u32(const uint32_t* __restric
     const uint32_t first = (uint32_t)tile * kThreads * kScanIpt + threadIdx.x * kScanIpt;
     uint32_t v[kScanIpt];
     unsigned long long sum = 0;
+    // a full run of kScanIpt from 16-byte-aligned buffers: vector loads and stores
+    const bool full = first + kScanIpt <= n &&
+                      ((reinterpret_cast<uintptr_t>(in) | reinterpret_cast<uintptr_t>(out)) & 15) == 0;
+    if (full) {
 #pragma unroll
-    for (int j = 0; j < kScanIpt; ++j) {
-        v[j] = first + j < n ? in[first + j] : 0u;
-        sum += v[j];
+        for (int j = 0; j < kScanIpt; j += 4) {
+            const uint4 q = *reinterpret_cast<const uint4*>(in + first + j);
+            v[j] = q.x; v[j + 1] = q.y; v[j + 2] = q.z; v[j + 3] = q.w;
+        }
+    } else {
+#pragma unroll
+        for (int j = 0; j < kScanIpt; ++j) v[j] = first + j < n ? in[first + j] : 0u;
     }
+#pragma unroll
+    for (int j = 0; j < kScanIpt; ++j) sum += v[j];
     unsigned long long tot;
     unsigned long long ex = block_exclusive_sum<kThreads, unsigned long long>(sum, s_scan, &tot);
     if (threadIdx.x < 32) {
@@ -84,10 +94,20 @@ __global__ void __launch_bounds__(kThreads) k_scan_u32(const uint32_t* __restric
     }
     __syncthreads();
     unsigned long long run = s_base + ex;
+    uint32_t o[kScanIpt];
 #pragma unroll
     for (int j = 0; j < kScanIpt; ++j) {
-        if (first + j < n) out[first + j] = (uint32_t)run;
+        o[j] = (uint32_t)run;
         run += v[j];
+    }
+    if (full) {
+#pragma unroll
+        for (int j = 0; j < kScanIpt; j += 4)
+            *reinterpret_cast<uint4*>(out + first + j) = make_uint4(o[j], o[j + 1], o[j + 2], o[j + 3]);
+    } else {
+#pragma unroll
+        for (int j = 0; j < kScanIpt; ++j)
+            if (first + j < n) out[first + j] = o[j];
     }
     if (tile == (int)gridDim.x - 1 && threadIdx.x == kThreads - 1 && total)
         *total = (uint32_t)(s_base + tot);
