@@ -47,7 +47,10 @@ constexpr int kSegBlock = kWarpsB * kSegPerWarp;  // 512
 constexpr int kSegChunks = kSegPerWarp / 32;
 constexpr int kXS = kMaxGX + 1;                // cursor row stride (room for x1+1)
 constexpr int kStageCap = 12288;               // entries staged in shared memory per block
-constexpr int kScanIpt = 8;
+#ifndef UWS_SCAN_IPT
+#define UWS_SCAN_IPT 8
+#endif
+constexpr int kScanIpt = UWS_SCAN_IPT;
 
 __device__ __forceinline__ int rect_nx(short4 r) { return (int)r.z - (int)r.x + 1; }
 __device__ __forceinline__ int rect_ny(short4 r) { return (int)r.w - (int)r.y + 1; }
