@@ -387,26 +387,56 @@ __global__ void __launch_bounds__(kThreads, 3) k_ssim_grad(const float* __restri
     if (threadIdx.x == 0) part_l1[blockIdx.y * gridDim.x + blockIdx.x] = (double)bs;
 }
 
-__global__ void __launch_bounds__(kThreads) k_loss_finalize(const double* __restrict__ part_s,
+constexpr int kFinThreads = 1024;
+
+__global__ void __launch_bounds__(kFinThreads) k_loss_finalize(const double* __restrict__ part_s,
                                                             int n_s, const double* __restrict__ part_l1,
                                                             int n_l1, double n_px, double n_win,
                                                             const float* medium, int has_guidance,
                                                             double lam_s, double lam_g,
                                                             double* result, float* nonfinite) {
     pdl_entry();
-    __shared__ double rs[kThreads], rl[kThreads];
+    __shared__ double rs[kFinThreads / 32], rl[kFinThreads / 32];
+    // fixed-order (deterministic) sums; each thread's loads are all issued before its adds
     double s = 0, l = 0;
-    for (int i = threadIdx.x; i < n_s; i += kThreads) s += part_s[i];
-    for (int i = threadIdx.x; i < n_l1; i += kThreads) l += part_l1[i];
-    rs[threadIdx.x] = s;
-    rl[threadIdx.x] = l;
-    __syncthreads();
-    for (int o = kThreads / 2; o > 0; o >>= 1) {
-        if (threadIdx.x < o) {
-            rs[threadIdx.x] += rs[threadIdx.x + o];
-            rl[threadIdx.x] += rl[threadIdx.x + o];
+    const int n = max(n_s, n_l1);
+    for (int i0 = 0; i0 < n; i0 += 4 * kFinThreads) {
+        double a[4], b[4];
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+            const int i = i0 + q * kFinThreads + (int)threadIdx.x;
+            a[q] = i < n_s ? part_s[i] : 0.0;
+            b[q] = i < n_l1 ? part_l1[i] : 0.0;
         }
-        __syncthreads();
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+            s += a[q];
+            l += b[q];
+        }
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        s += __shfl_down_sync(0xffffffffu, s, o);
+        l += __shfl_down_sync(0xffffffffu, l, o);
+    }
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    if (lane == 0) {
+        rs[warp] = s;
+        rl[warp] = l;
+    }
+    __syncthreads();
+    if (warp == 0) {
+        s = rs[lane];
+        l = rl[lane];
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+            s += __shfl_down_sync(0xffffffffu, s, o);
+            l += __shfl_down_sync(0xffffffffu, l, o);
+        }
+        if (lane == 0) {
+            rs[0] = s;
+            rl[0] = l;
+        }
     }
     if (threadIdx.x == 0) {
         double l1 = rl[0] / n_px;
@@ -525,7 +555,7 @@ extern "C" int uws_loss_fwd_bwd(const float* rendered, const float* gt, int32_t 
         launch_serial(k_ssim_grad<0>, dim3(g2), dim3(kThreads), kGradSmem, st, rendered, gt, h, w, c, p.maps, k_ssim,
                                                         k_l1, dL_dC, p.part_l1);
     UWS_CHECK_LAUNCH("k_ssim_grad");
-    launch(k_loss_finalize, dim3(1), dim3(kThreads), 0, st, p.part_s, p.n_s, p.part_l1, p.n_l1, n_px, n_win, medium,
+    launch(k_loss_finalize, dim3(1), dim3(kFinThreads), 0, st, p.part_s, p.n_s, p.part_l1, p.n_l1, n_px, n_win, medium,
                                             has_guidance, lambda_ssim, lambda_guide, result,
                                             nonfinite);
     UWS_CHECK_LAUNCH("k_loss_finalize");
