@@ -187,7 +187,7 @@ int uws_raster_fwd(const uws_projected* proj, const int32_t* offsets, const int3
                    const uws_camera* cam, const float* medium, uws_raster_out* out, void* stream);
 /* Schedule for the next compositing launches over the same view and buffers:
  * the tiles by descending consumed-prefix length (tile_nrows of a forward,
- * low 30 bits / 4, capped at 255), written to order [n_tiles].  One CTA, async on
+ * low 30 bits / 8, capped at 127), written to order [n_tiles].  One CTA, async on
  * stream.  (No reference counterpart: the reference composites tiles in a
  * worker pool, rasterizer.py:186-241.) */
 int uws_tile_order(const int32_t* tile_nrows, int32_t n_tiles, int32_t* order, void* stream);

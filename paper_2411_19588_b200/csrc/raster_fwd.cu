@@ -537,12 +537,12 @@ __global__ void __launch_bounds__(256) k_raster_fix(FwdArgs a) {
 }
 
 // Compositing schedule: the tiles by descending consumed-prefix length (the forward's
-// tile_nrows / 4, capped at 255), by a one-CTA counting sort.  Tiles are independent, so
+// tile_nrows / 8, capped at 127), by a one-CTA counting sort.  Tiles are independent, so
 // any permutation gives the same images and gradients; launching the heaviest tiles
 // first keeps a few long tiles from running alone at the end of the grid (measured:
 // the forward's SMs were busy only ~79 % of its duration in raster order).
-constexpr int kOrderThreads = 1024, kOrderIpt = 16;  // tiles per thread per chunk
-constexpr int kOrderBuckets = 256;                     // cost / 4, capped
+constexpr int kOrderThreads = 1024, kOrderIpt = 8;  // tiles per thread per chunk (8160 at 1080p)
+constexpr int kOrderBuckets = 128;                    // cost / 8, capped
 
 __device__ __forceinline__ void order_costs(const int32_t* __restrict__ nrows, int n, int c0,
                                             int (&bkt)[kOrderIpt]) {
@@ -554,8 +554,8 @@ __device__ __forceinline__ void order_costs(const int32_t* __restrict__ nrows, i
 #pragma unroll
     for (int q = 0; q < kOrderIpt; ++q) {
         const int i = c0 + (int)threadIdx.x + q * kOrderThreads;
-        const int c = i < n ? min(__ldg(nrows + i) & ~kRowsComplete, 4 * kOrderBuckets - 1) : 0;
-        bkt[q] = i < n ? (kOrderBuckets - 1 - (c >> 2)) * 32 + lane : -1;
+        const int c = i < n ? min(__ldg(nrows + i) & ~kRowsComplete, 8 * kOrderBuckets - 1) : 0;
+        bkt[q] = i < n ? (kOrderBuckets - 1 - (c >> 3)) * 32 + lane : -1;
     }
 }
 
