@@ -347,8 +347,8 @@ extern "C" int uws_adam_step(float* params, float* exp_avg, float* exp_avg_sq, f
         // medium slots and pad zeroed after every reader is done; the skip
         // counters (slots 9, 10) are left alone: non-zero they keep skipping
         // later steps until the host has handled the skip and cleared them
-        UWS_CUDA(zero_async(medium_grads, 9 * sizeof(float), st));
-        UWS_CUDA(zero_async(medium_grads + 11, 5 * sizeof(float), st));
+        UWS_CUDA(zero_async2(medium_grads, 9 * sizeof(float), medium_grads + 11,
+                             5 * sizeof(float), st));
     }
     return UWS_OK;
 }

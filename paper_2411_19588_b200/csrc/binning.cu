@@ -697,20 +697,24 @@ extern "C" int uws_bin_count(const uws_projected* proj, int64_t k_cap, const uws
     grid_of(cam, &gx, &gy, &nbands);
     UWS_REQUIRE(gx <= kMaxGX && nbands <= kMaxBands, "uws_bin_count: image larger than 4096 px");
     cudaStream_t st = as_stream(stream);
-    UWS_CUDA(zero_async(totals, 2 * sizeof(int64_t), st));
-    if (k_cap == 0) return UWS_OK;
+    if (k_cap == 0) {
+        UWS_CUDA(zero_async(totals, 2 * sizeof(int64_t), st));
+        return UWS_OK;
+    }
     Workspace ws(count_ws, count_bytes);
     CountPlan p;
     plan_count(ws, (uint32_t)k_cap, nbands, p);
     UWS_REQUIRE(ws.ok(), "uws_bin_count: workspace too small");
+    namespace db = depth_bucket;
+    // totals and the bucket sort's meta + counts, in one launch
+    UWS_CUDA(zero_async2(totals, 2 * sizeof(int64_t), p.meta,
+                         (char*)(p.bcount + db::kBuckets) - (char*)p.meta, st));
     const uint32_t kc = (uint32_t)k_cap;
     const uint32_t* k_dev = (const uint32_t*)proj->num_visible;
     // 0. order of the rows by (float64 depth bits, row): bucket the high words,
     //    then sort each bucket (depth_bucket.cuh)
     const uint64_t* dbits = (const uint64_t*)proj->depth;
-    namespace db = depth_bucket;
     const unsigned kb = (unsigned)ceil_div(kc, 256);
-    UWS_CUDA(zero_async(p.meta, (char*)(p.bcount + db::kBuckets) - (char*)p.meta, st));
     // the visible depths' high-word range: from the preprocess kernel when it wrote it
     const uint32_t* range = proj->depth_range;
     if (!range) {

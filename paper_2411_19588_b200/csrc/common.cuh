@@ -112,6 +112,7 @@ inline void launch(void (*kernel)(P...), dim3 grid, dim3 block, size_t smem, cud
 // serialized kernels does not order the second one after it (a kernel launched
 // right after a memset could run before the memset had landed).
 cudaError_t zero_async(void* ptr, size_t bytes, cudaStream_t st);
+cudaError_t zero_async2(void* p, size_t pbytes, void* q, size_t qbytes, cudaStream_t st);
 
 // Launch after the previous grid has fully drained: for a kernel that depends on
 // the L1 / shared-memory split its SMs are configured with (an early-launched

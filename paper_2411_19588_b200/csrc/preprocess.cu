@@ -227,8 +227,8 @@ extern "C" int uws_preprocess_fwd(const uws_cloud* cloud, const uws_camera* cam,
     auto* status = ws.take<unsigned long long>(blocks);
     auto* ticket = ws.take<unsigned>(1);
     UWS_REQUIRE(ws.ok(), "uws_preprocess_fwd: workspace too small");
-    UWS_CUDA(zero_async(status, (char*)(ticket + 1) - (char*)status, st));
-    if (out->depth_range) UWS_CUDA(zero_async(out->depth_range, 2 * sizeof(uint32_t), st));
+    UWS_CUDA(zero_async2(status, (char*)(ticket + 1) - (char*)status, out->depth_range,
+                         out->depth_range ? 2 * sizeof(uint32_t) : 0, st));
     launch_serial(k_preprocess, dim3((unsigned)blocks), dim3(kThreads), 0, st, *cloud, *cam, frustum_lim(*cam), *out, gx, gy, status, ticket);
     UWS_CHECK_LAUNCH("k_preprocess");
     return UWS_OK;
